@@ -1,0 +1,185 @@
+/* helio_gpu.h — C ABI of the B200 placement-scoring engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj, "helio"):
+ *
+ *   reference interface (file:line)                 replaced by
+ *   ------------------------------------------------------------------------
+ *   FlowGraph build_flow_graph(c, p, partial)       helio_gpu_flows_host (graph + flows)
+ *       include/helio/flow_graph.hpp:43, src/flow_graph.cpp:45-136
+ *   double max_flow(FlowGraph&)                     helio_gpu_maxflow_raw_host
+ *       include/helio/flow_graph.hpp:46, src/flow_graph.cpp:138-229
+ *   build_flow_graph + max_flow per candidate       helio_gpu_score / helio_gpu_score_host
+ *       (the pair at tests/oracles/enumerate.hpp:56-57, bindings/pymodule.cpp:170-171,
+ *        src/placement.cpp:358-359 and :441-442)
+ *   strict-'>' argmax over candidates               helio_gpu_argmax
+ *       tests/oracles/enumerate.hpp:59
+ *   compute_edge_capacity / ClusterSpec::max_layers helio_gpu_set_cluster (K0, precomputed once)
+ *       src/flow_graph.cpp:38-43, src/cluster.cpp:62-100
+ *   iwrr_weights + IwrrPicker + Scheduler::admit    helio_gpu_route_host
+ *       src/scheduler.cpp:28-56, :157-190 (AC8 admit/complete loop)
+ *
+ * Conventions: every entry returns an int status (HELIO_OK == 0); nothing
+ * throws across the ABI; helio_gpu_last_error() holds the message of the last
+ * failure.  Buffers are caller-owned.  "d_" pointers are device memory,
+ * "h_" pointers host memory (pinned or pageable).  A context is bound to one
+ * device and is thread-compatible, not thread-safe.  `stream` is a
+ * cudaStream_t (NULL = the context's own stream).
+ *
+ * Placements are int16 [B][N][2] rows (start, end) in the cluster's declared
+ * node order; a row with end <= start is an idle node, exactly like an empty
+ * Interval in the reference's Placement map (src/flow_graph.cpp:53).
+ */
+#ifndef HELIO_GPU_H
+#define HELIO_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* call status */
+#define HELIO_OK 0
+#define HELIO_ERR_INVALID 1     /* bad argument / cluster */
+#define HELIO_ERR_CUDA 2        /* CUDA runtime failure */
+#define HELIO_ERR_NO_CLUSTER 3  /* helio_gpu_set_cluster not called */
+#define HELIO_ERR_TOO_LARGE 4   /* graph exceeds the device limits */
+
+/* per-candidate status (values[i] is 0 when status[i] != 0) */
+#define HELIO_CAND_OK 0
+#define HELIO_CAND_UNKNOWN_NODE 1 /* "placement references unknown node" (flow_graph.cpp:55) */
+#define HELIO_CAND_RANGE 2        /* "placement ... outside [0, L)" (flow_graph.cpp:56-57) */
+#define HELIO_CAND_VRAM 3         /* "exceeds its VRAM layer capacity" (flow_graph.cpp:58-59) */
+#define HELIO_CAND_TOO_LARGE 4    /* graph does not fit one SM's shared memory */
+#define HELIO_CAND_EDGE_BUFFER 5  /* flows: caller's max_edges too small (num_edges holds the need) */
+
+/* edge kinds, same numbering as helio::EdgeKind (flow_graph.hpp:21) */
+#define HELIO_EDGE_COMPUTE 0
+#define HELIO_EDGE_COORD_OUT 1
+#define HELIO_EDGE_COORD_IN 2
+#define HELIO_EDGE_INTERCONNECT 3
+
+typedef struct helio_gpu_ctx helio_gpu_ctx;
+
+/* A ClusterSpec (cluster.hpp:10-58) with ids replaced by indices.  Derived
+ * quantities (k_i, T_j, NIC clamps, token capacities) are computed by the
+ * library with the reference's own expressions. */
+typedef struct {
+  int32_t num_nodes;
+  int32_t num_links;
+  int32_t num_layers;               /* ModelSpec::num_layers */
+  double param_bytes;               /* ModelSpec::param_bytes */
+  double token_bytes;               /* ModelSpec::token_bytes */
+  double activation_bytes;          /* ModelSpec::activation_bytes */
+  double kv_bytes_per_token_layer;  /* ModelSpec::kv_bytes_per_token_layer (0 = 2*act) */
+  const double* vram_bytes;         /* [N] NodeSpec::vram_bytes */
+  const double* kv_reserve;         /* [N] */
+  const double* peak_layer_tokens;  /* [N] */
+  const double* nic_in_bps;         /* [N] 0 = max incident link bandwidth */
+  const double* nic_out_bps;        /* [N] */
+  const int32_t* table_off;         /* [N+1] throughput_table values for keys 1..len, or NULL */
+  const double* table_val;
+  const int32_t* lex_rank;          /* [N] rank of node id in byte-lexicographic order */
+  const int32_t* link_src;          /* [M] node index, -1 = coordinator, -2 = undeclared id */
+  const int32_t* link_dst;          /* [M] */
+  const double* link_bandwidth_bps; /* [M] */
+} helio_cluster_desc;
+
+/* One FlowEdge (flow_graph.hpp:23-31) in g.edges order. */
+typedef struct {
+  int32_t u, v;
+  int32_t kind;
+  int32_t exec_start, exec_end;
+  int32_t src_node, dst_node; /* node index, -1 = coordinator */
+  int32_t pad;
+  double cap;
+  double flow;
+} helio_edge;
+
+/* One PlanEdge (placement.hpp:47-51): src/dst node index, -1 = coordinator. */
+typedef struct {
+  int32_t src_node, dst_node;
+  int32_t exec_start, exec_end;
+  double flow;
+} helio_plan_edge;
+
+int helio_gpu_create(int device, helio_gpu_ctx** out);
+void helio_gpu_destroy(helio_gpu_ctx* ctx);
+const char* helio_gpu_last_error(const helio_gpu_ctx* ctx);
+int helio_gpu_sync(helio_gpu_ctx* ctx);
+
+/* K0: compile and upload a cluster.  k_out (optional, [N]) receives k_i. */
+int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* desc, int32_t* k_out);
+
+/* compute_edge_capacity(c, node, j) for 1 <= j <= k_i, from the compiled table. */
+int helio_gpu_compute_edge_capacity(const helio_gpu_ctx* ctx, int32_t node, int32_t j, double* out);
+
+/* Batched build_flow_graph + max_flow value, device buffers, async on stream. */
+int helio_gpu_score(helio_gpu_ctx* ctx, const int16_t* d_placements, int64_t B, int allow_partial,
+                    double* d_values, int32_t* d_status, void* stream);
+
+/* Same, host buffers (host<->device copies inside, pipelined); synchronous. */
+int helio_gpu_score_host(helio_gpu_ctx* ctx, const int16_t* h_placements, int64_t B,
+                         int allow_partial, double* h_values, int32_t* h_status);
+
+/* Full FlowGraph (edges in reference order, with max_flow's per-edge flows)
+ * for K candidates; synchronous, host buffers.  h_edges is [K][max_edges]. */
+int helio_gpu_flows_host(helio_gpu_ctx* ctx, const int16_t* h_placements, int64_t K,
+                         int allow_partial, int32_t max_edges, int32_t* h_num_vertices,
+                         int32_t* h_num_edges, helio_edge* h_edges, double* h_values,
+                         int32_t* h_status);
+
+/* max_flow on G raw graphs (any source/sink, self-loops, parallel edges, zero
+ * capacities — flow_graph.cpp:138-229).  Edges of graph g are
+ * [edge_off[g], edge_off[g+1]).  h_flows (optional) receives per-edge flows. */
+int helio_gpu_maxflow_raw_host(helio_gpu_ctx* ctx, int64_t G, const int32_t* h_n,
+                               const int32_t* h_source, const int32_t* h_sink,
+                               const int64_t* h_edge_off, const int32_t* h_u, const int32_t* h_v,
+                               const double* h_cap, double* h_values, double* h_flows);
+
+/* First index of the maximum value among status==0 candidates with value > 0
+ * (enumerate.hpp:59 strict '>' from best = 0).  Writes (0, -1) if none.
+ * index_base is added to the index (global candidate numbering). */
+int helio_gpu_argmax(helio_gpu_ctx* ctx, const double* d_values, const int32_t* d_status,
+                     int64_t B, int64_t index_base, double* d_best, int64_t* d_index,
+                     void* stream);
+
+/* Candidate generator G(seed, i): random covering chains,
+ * counter-based (splitmix64), identical on host and device.  p_uniform_ppm
+ * mixes in uniform random intervals (parts per million per node). */
+int helio_gpu_generate(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B,
+                       uint32_t p_uniform_ppm, int16_t* d_out, void* stream);
+void helio_generate_host(const int32_t* k, int32_t num_nodes, int32_t num_layers, uint64_t seed,
+                         int64_t first, int64_t B, uint32_t p_uniform_ppm, int16_t* h_out);
+
+/* IWRR routing of R requests over a plan (scheduler.cpp:58-190) in the AC8
+ * admit/complete order: request r is admitted with in_len[r] and completed at
+ * once with out_len[r].  Plan edges in plan order; placement is the plan's
+ * int16 [N][2] row.  hop arrays are [R][max_hops]; h_num_hops[r] = -1 for a
+ * deferred request.  *h_deferred receives the number of deferrals. */
+int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_placement,
+                         const helio_plan_edge* h_plan_edges, int32_t num_plan_edges, int64_t R,
+                         const int32_t* h_in_len, const int32_t* h_out_len, int32_t max_hops,
+                         int32_t* h_num_hops, int32_t* h_hop_node, int32_t* h_hop_start,
+                         int32_t* h_hop_end, int64_t* h_deferred);
+
+/* iwrr_weights (scheduler.cpp:46-56) of one candidate list, on the device. */
+int helio_gpu_iwrr_weights(helio_gpu_ctx* ctx, const double* h_flows, int32_t n, int64_t* h_weights);
+
+/* IwrrPicker::next (scheduler.cpp:28-44) `calls` times on the device.  The
+ * picker state (round, idx) is read from and written back to *h_round/*h_idx
+ * (a fresh picker is round 1, idx 0).  h_masks holds, per call, ceil(n/64)
+ * little-endian words of eligibility bits.  h_out[k] = candidate or -1. */
+int helio_gpu_iwrr_picks(helio_gpu_ctx* ctx, const int64_t* h_weights, int32_t n, int64_t* h_round,
+                         int64_t* h_idx, int32_t calls, const uint64_t* h_masks, int32_t* h_out);
+
+/* Introspection for benchmarks: kernels launched by this context so far, and
+ * the device time (ms) of the last score call's dominant kernel. */
+int64_t helio_gpu_launch_count(const helio_gpu_ctx* ctx);
+double helio_gpu_last_kernel_ms(const helio_gpu_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HELIO_GPU_H */

@@ -1,0 +1,328 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// A thin extern "C" harness around the UNMODIFIED reference library (compiled
+// from /root/reference/proj/src by oracle/Makefile into oracle/_ref/).  It lets
+// the Python test-suite, the golden-vector generator (tests/golden/make_golden.py)
+// and bench.py's reference arm call the reference's own public API:
+//
+//   build_flow_graph + max_flow      proj/src/flow_graph.cpp:45-229
+//   plan_from_placement              proj/src/placement.cpp:459-469
+//   iwrr_weights / IwrrPicker        proj/src/scheduler.cpp:28-56
+//   Scheduler::admit / complete      proj/src/scheduler.cpp:58-190
+//   generate_trace                   proj/src/workload.cpp:37-57
+//   AC1 random raw graphs            proj/tests/acceptance/acceptance_main.cpp:266-295
+//   test_flow random graphs          proj/tests/test_flow.cpp:141-188
+//
+// Placements cross this boundary as int16 [N][2] (start, end) rows in the
+// cluster's declared node order; rows with end <= start are idle, exactly like
+// an empty Interval in the reference's Placement map (flow_graph.cpp:53).
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "helio/cluster.hpp"
+#include "helio/errors.hpp"
+#include "helio/flow_graph.hpp"
+#include "helio/placement.hpp"
+#include "helio/rng.hpp"
+#include "helio/scheduler.hpp"
+#include "helio/workload.hpp"
+
+using namespace helio;
+
+namespace {
+
+void set_err(char* err, int errlen, const std::string& msg) {
+  if (err && errlen > 0) {
+    std::strncpy(err, msg.c_str(), errlen - 1);
+    err[errlen - 1] = 0;
+  }
+}
+
+Placement to_placement(const ClusterSpec& c, const int16_t* pl) {
+  Placement p;
+  for (size_t k = 0; k < c.nodes.size(); ++k) {
+    int s = pl[2 * k], e = pl[2 * k + 1];
+    if (e > s) p[c.nodes[k].id] = {s, e};
+  }
+  return p;
+}
+
+// Map the reference's three ValidationError texts (flow_graph.cpp:55-59) to codes.
+int status_of(const std::string& what) {
+  if (what.find("unknown node") != std::string::npos) return 1;
+  if (what.find("outside [0,") != std::string::npos) return 2;
+  if (what.find("VRAM layer capacity") != std::string::npos) return 3;
+  return 9;
+}
+
+int node_idx(const ClusterSpec& c, const std::string& id) {
+  if (id == c.coordinator_id) return -1;
+  return c.node_index(id);
+}
+
+}  // namespace
+
+extern "C" {
+
+void* refh_cluster_from_json(const char* text, char* err, int errlen) {
+  try {
+    return new ClusterSpec(parse_cluster(text, "<refh>"));
+  } catch (const std::exception& ex) {
+    set_err(err, errlen, ex.what());
+    return nullptr;
+  }
+}
+
+void refh_cluster_free(void* c) { delete static_cast<ClusterSpec*>(c); }
+
+int refh_cluster_num_nodes(void* c) { return static_cast<int>(static_cast<ClusterSpec*>(c)->nodes.size()); }
+
+int refh_max_layers(void* cp, int k) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  return c.max_layers(c.nodes[k]);
+}
+
+double refh_compute_edge_capacity(void* cp, int k, int j) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  return compute_edge_capacity(c, c.nodes[k], j);
+}
+
+// Full FlowGraph + max_flow for one candidate.  Returns 0 ok, 1/2/3 for the
+// three ValidationErrors, -2 when max_e is too small (ne holds the need).
+int refh_graph(void* cp, const int16_t* pl, int allow_partial, int max_e, int32_t* nv, int32_t* ne,
+               int32_t* u, int32_t* v, int32_t* kind, int32_t* es, int32_t* ee, double* cap,
+               double* flow, double* value, char* err, int errlen) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  FlowGraph g;
+  try {
+    g = build_flow_graph(c, to_placement(c, pl), allow_partial != 0);
+  } catch (const ValidationError& ex) {
+    set_err(err, errlen, ex.what());
+    return status_of(ex.what());
+  }
+  *value = max_flow(g);
+  *nv = g.num_vertices;
+  *ne = static_cast<int32_t>(g.edges.size());
+  if (static_cast<int>(g.edges.size()) > max_e) return -2;
+  for (size_t i = 0; i < g.edges.size(); ++i) {
+    const FlowEdge& e = g.edges[i];
+    u[i] = e.u;
+    v[i] = e.v;
+    kind[i] = static_cast<int32_t>(e.kind);
+    es[i] = e.exec_start;
+    ee[i] = e.exec_end;
+    cap[i] = e.cap;
+    flow[i] = e.flow;
+  }
+  return 0;
+}
+
+// Bulk scoring: exactly the enumerate.hpp:56-57 pair per candidate, on a
+// std::thread pool with static chunks (flow_graph.cpp holds no shared state).
+int refh_score(void* cp, const int16_t* pl, int64_t B, int allow_partial, int nthreads,
+               double* values, int32_t* status) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  const int64_t N = static_cast<int64_t>(c.nodes.size());
+  if (nthreads < 1) nthreads = 1;
+  auto work = [&](int64_t lo, int64_t hi) {
+    for (int64_t b = lo; b < hi; ++b) {
+      try {
+        FlowGraph g = build_flow_graph(c, to_placement(c, pl + b * N * 2), allow_partial != 0);
+        values[b] = max_flow(g);
+        status[b] = 0;
+      } catch (const ValidationError& ex) {
+        values[b] = 0;
+        status[b] = status_of(ex.what());
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  int64_t chunk = (B + nthreads - 1) / nthreads;
+  for (int t = 0; t < nthreads; ++t) {
+    int64_t lo = t * chunk, hi = std::min(B, lo + chunk);
+    if (lo >= hi) break;
+    pool.emplace_back(work, lo, hi);
+  }
+  for (auto& th : pool) th.join();
+  return 0;
+}
+
+// Solve-only rate on pre-built graphs (reported beside the whole-eval rate).
+double refh_solve_only(void* cp, const int16_t* pl, int64_t B, int allow_partial) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  const int64_t N = static_cast<int64_t>(c.nodes.size());
+  std::vector<FlowGraph> gs;
+  gs.reserve(B);
+  for (int64_t b = 0; b < B; ++b) gs.push_back(build_flow_graph(c, to_placement(c, pl + b * N * 2), allow_partial != 0));
+  double acc = 0;
+  for (auto& g : gs) acc += max_flow(g);
+  return acc;
+}
+
+double refh_maxflow_raw(int n, int s, int t, int m, const int32_t* u, const int32_t* v,
+                        const double* cap, double* flow_out) {
+  FlowGraph g;
+  g.num_vertices = n;
+  g.source = s;
+  g.sink = t;
+  for (int i = 0; i < m; ++i) {
+    FlowEdge e;
+    e.u = u[i];
+    e.v = v[i];
+    e.cap = cap[i];
+    g.edges.push_back(e);
+  }
+  double val = max_flow(g);
+  for (int i = 0; i < m; ++i) flow_out[i] = g.edges[i].flow;
+  return val;
+}
+
+// AC1's random raw graphs, drawn with the reference's own Rng exactly as
+// acceptance_main.cpp:270-284 does.  sink = n-1, self-loops allowed.
+int64_t refh_ac1_graphs(uint64_t seed, int count, int32_t* n, int32_t* t, int32_t* m, int32_t* eu,
+                        int32_t* ev, double* ecap, int64_t cap_edges) {
+  Rng rng(seed);
+  int64_t off = 0;
+  for (int it = 0; it < count; ++it) {
+    int nv = 2 + static_cast<int>(rng.uniform_int(19));
+    int mm = 1 + static_cast<int>(rng.uniform_int(3 * nv));
+    n[it] = nv;
+    t[it] = nv - 1;
+    m[it] = mm;
+    for (int i = 0; i < mm; ++i) {
+      int a = static_cast<int>(rng.uniform_int(nv));
+      int b = static_cast<int>(rng.uniform_int(nv));
+      double cc = static_cast<double>(rng.uniform_int(51));
+      if (off < cap_edges) {
+        eu[off] = a;
+        ev[off] = b;
+        ecap[off] = cc;
+      }
+      ++off;
+    }
+  }
+  return off;
+}
+
+// test_flow.cpp:143-159 random_graph(rng, 19) x 400 with seed 20240811:
+// sink = 1, self-loops dropped.
+int64_t refh_testflow_graphs(uint64_t seed, int count, int max_vertices, int32_t* n, int32_t* m,
+                             int32_t* eu, int32_t* ev, double* ecap, int64_t cap_edges) {
+  Rng rng(seed);
+  int64_t off = 0;
+  for (int it = 0; it < count; ++it) {
+    int nv = 2 + static_cast<int>(rng.uniform_int(max_vertices - 1));
+    int mm = 1 + static_cast<int>(rng.uniform_int(3 * nv));
+    int kept = 0;
+    for (int i = 0; i < mm; ++i) {
+      int a = static_cast<int>(rng.uniform_int(nv));
+      int b = static_cast<int>(rng.uniform_int(nv));
+      if (a == b) continue;
+      double cc = static_cast<double>(rng.uniform_int(51));
+      if (off < cap_edges) {
+        eu[off] = a;
+        ev[off] = b;
+        ecap[off] = cc;
+      }
+      ++off;
+      ++kept;
+    }
+    n[it] = nv;
+    m[it] = kept;
+  }
+  return off;
+}
+
+void refh_iwrr_weights(const double* flows, int n, int64_t* out) {
+  std::vector<long> w = iwrr_weights(std::vector<double>(flows, flows + n));
+  for (int i = 0; i < n; ++i) out[i] = w[i];
+}
+
+// IwrrPicker sequence with an eligibility mask per call (mask bit i = eligible).
+void refh_picker_seq(const int64_t* weights, int n, int calls, const uint64_t* masks, int32_t* out) {
+  IwrrPicker p(std::vector<long>(weights, weights + n));
+  for (int k = 0; k < calls; ++k) {
+    uint64_t mk = masks[k];
+    out[k] = p.next([&](int i) { return ((mk >> i) & 1u) != 0; });
+  }
+}
+
+// plan_from_placement → PlanEdge list (src/dst as node index, -1 = coordinator).
+int refh_plan(void* cp, const int16_t* pl, int allow_partial, int max_edges, int32_t* src,
+              int32_t* dst, double* flow, int32_t* es, int32_t* ee, double* objective) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  PlacementPlan plan;
+  try {
+    plan = plan_from_placement(c, to_placement(c, pl), allow_partial != 0, "custom");
+  } catch (const ValidationError& ex) {
+    return -status_of(ex.what());
+  }
+  *objective = plan.objective;
+  int ne = static_cast<int>(plan.edges.size());
+  for (int i = 0; i < ne && i < max_edges; ++i) {
+    src[i] = node_idx(c, plan.edges[i].src);
+    dst[i] = node_idx(c, plan.edges[i].dst);
+    flow[i] = plan.edges[i].flow;
+    es[i] = plan.edges[i].exec_start;
+    ee[i] = plan.edges[i].exec_end;
+  }
+  return ne;
+}
+
+// The AC8 loop (acceptance_main.cpp:526-537): admit(i, in[i]) then, if
+// admitted, complete(i, out[i]).  Hop lists are written at stride max_hops.
+// Returns the number of deferred (nullopt) admissions, or -1 on a plan error.
+int64_t refh_route(void* cp, const int16_t* pl, int allow_partial, uint64_t seed, int64_t R,
+                   const int32_t* in_len, const int32_t* out_len, int max_hops, int32_t* nhops,
+                   int32_t* hop_node, int32_t* hop_s, int32_t* hop_e) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  PlacementPlan plan;
+  try {
+    plan = plan_from_placement(c, to_placement(c, pl), allow_partial != 0, "custom");
+  } catch (const std::exception&) {
+    return -1;
+  }
+  Scheduler sched(c, plan, SchedPolicy::kIwrr, seed);
+  int64_t denied = 0;
+  for (int64_t r = 0; r < R; ++r) {
+    auto route = sched.admit(static_cast<long>(r), in_len[r]);
+    if (!route) {
+      ++denied;
+      nhops[r] = -1;
+      continue;
+    }
+    int h = static_cast<int>(route->size());
+    nhops[r] = h;
+    for (int k = 0; k < h && k < max_hops; ++k) {
+      hop_node[r * max_hops + k] = c.node_index((*route)[k].node);
+      hop_s[r * max_hops + k] = (*route)[k].exec_start;
+      hop_e[r * max_hops + k] = (*route)[k].exec_end;
+    }
+    sched.complete(static_cast<long>(r), out_len[r]);
+  }
+  return denied;
+}
+
+int refh_trace(int count, double rate, int online, uint64_t seed, double mean_in, double mean_out,
+               int max_in, int max_out, double* arrival, int32_t* in_len, int32_t* out_len) {
+  LengthParams lp;
+  lp.mean_input = mean_in;
+  lp.mean_output = mean_out;
+  lp.max_input = max_in;
+  lp.max_output = max_out;
+  std::vector<Request> reqs =
+      generate_trace(count, rate, online ? TraceMode::kOnline : TraceMode::kOffline, lp, seed);
+  for (int i = 0; i < count; ++i) {
+    arrival[i] = reqs[i].arrival_s;
+    in_len[i] = reqs[i].input_len;
+    out_len[i] = reqs[i].output_len;
+  }
+  return count;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+"""In-tree build of the engine (sm_100a) and the drop-in bindings.
+
+Outputs (git-ignored, shipped to the GPU box by gpurun):
+  paper_2406_01566_b200/lib/libhelio_gpu.so   C ABI (include/helio_gpu.h): kernels + K0
+  paper_2406_01566_b200/lib/libhelio.so       C++ drop-in (namespace helio) over the C ABI
+  paper_2406_01566_b200/_helio*.so            Python bindings (`_helio`)
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+import sysconfig
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "lib")
+OBJ = os.path.join(ROOT, "build", "obj")
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
+              "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-sign-compare"]
+
+CU_SOURCES = ["helio_gpu.cu", "route.cu"]
+HEADERS = ["engine.h", "gen.h", "shim.hpp", "helio/cluster.hpp", "helio/errors.hpp",
+           "helio/flow_graph.hpp", "helio/placement.hpp", "helio/scheduler.hpp"]
+
+
+def _run(cmd, quiet=False):
+    if not quiet:
+        print("+", " ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"build step failed: {cmd[0]} ... ({r.returncode})")
+    return r.stdout + r.stderr
+
+
+def _newer(out, deps):
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def ext_suffix() -> str:
+    return sysconfig.get_config_var("EXT_SUFFIX") or ".so"
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    os.makedirs(LIB, exist_ok=True)
+    os.makedirs(OBJ, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "helio_gpu.h")]
+    objs = []
+    ptxas_log = []
+    for src in CU_SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        if force or _newer(o, [s] + hdrs):
+            ptxas_log.append(_run([NVCC, *ARCH, *NVCC_FLAGS, "-c", s, "-o", o], quiet=not verbose))
+        objs.append(o)
+    libgpu = os.path.join(LIB, "libhelio_gpu.so")
+    if force or _newer(libgpu, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", libgpu, *objs, "-lcudart_static"], quiet=not verbose)
+    if ptxas_log:
+        with open(os.path.join(ROOT, "build", "ptxas.log"), "w") as f:
+            f.write("\n".join(ptxas_log))
+
+    import pybind11  # noqa: WPS433 (build-time only)
+
+    inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include")]
+    libshim = os.path.join(LIB, "libhelio.so")
+    shim_src = os.path.join(CSRC, "shim.cpp")
+    if force or _newer(libshim, [shim_src, libgpu] + hdrs):
+        _run(["g++", *CXX_FLAGS, *inc, "-shared", shim_src, "-o", libshim,
+              "-L" + LIB, "-lhelio_gpu", "-Wl,-rpath,$ORIGIN"], quiet=not verbose)
+    pyext = os.path.join(PKG, "_helio" + ext_suffix())
+    py_src = os.path.join(CSRC, "pymodule.cpp")
+    if force or _newer(pyext, [py_src, libshim] + hdrs):
+        _run(["g++", *CXX_FLAGS, *inc, "-I" + pybind11.get_include(),
+              "-I" + sysconfig.get_paths()["include"], "-shared", py_src, "-o", pyext,
+              "-L" + LIB, "-lhelio", "-lhelio_gpu", "-Wl,-rpath,$ORIGIN/lib"], quiet=not verbose)
+
+
+def build_oracle() -> None:
+    """Test infrastructure: oracle/_ref (reference, when /root/reference exists) + C oracle."""
+    _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "-j8"], quiet=True)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)
+    build_oracle()

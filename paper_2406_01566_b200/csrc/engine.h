@@ -1,0 +1,96 @@
+// engine.h — internal types shared by the engine's translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/helio_gpu.h"
+
+namespace helio_engine {
+
+// ---------------------------------------------------------------------------
+// Device-side cluster constants (K0 output).
+struct ClusterDev {
+  int N, L, Mv;
+  const int16_t* kmax;      // [N]
+  const int32_t* lexrank;   // [N]
+  const int16_t* lexnode;   // [N] node at lex rank r
+  const int32_t* cap_off;   // [N] start of node's compute-capacity row (j = 1..k)
+  const double* cap_tab;    // compute_edge_capacity(c, node, j)
+  const uint32_t* link_pack;  // [Mv] (src+1) | (dst+1) << 16, 0 = coordinator
+  const double* link_cap;     // [Mv] link_token_capacity with the reference payload
+  const double* cin_cap;      // [N] capacity of node -> coordinator edge (value sum)
+};
+
+// Shared-memory slot layout of one graph (byte offsets from the slot base).
+struct Layout {
+  int V, A, N, M;  // vertex, arc, node, raw-edge capacities
+  int o_cap, o_ex, o_to, o_rv, o_abeg, o_h, o_cur, o_q, o_cnt, o_inq, o_ps, o_pe, o_vin, o_unode,
+      o_efwd;
+  int bytes;
+};
+
+}  // namespace helio_engine
+
+struct helio_gpu_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+
+  bool has_cluster = false;
+  int N = 0, L = 0, Mv = 0, Vmax = 0;
+  std::vector<int32_t> h_kmax;
+  std::vector<int32_t> h_cap_off;
+  std::vector<double> h_cap_tab;
+  std::vector<int32_t> h_lexrank;
+  std::vector<double> h_vram;
+  double bytes_per_layer = 0, kv_token_layer_bytes = 0;
+  helio_engine::ClusterDev cd{};
+  void* d_cluster = nullptr;  // one allocation for all constant arrays
+  int32_t* d_kmax32 = nullptr;
+  helio_engine::Layout small{}, big{};
+  int small_warps = 4, small_blocks = 0, big_blocks = 0;
+  bool big_ok = false;
+
+  // scratch, two sets (one per pipeline stream)
+  unsigned long long* d_work = nullptr;  // [4]
+  unsigned int* d_ovf_count = nullptr;   // [2]
+  int64_t* d_ovf[2] = {nullptr, nullptr};
+  int64_t ovf_cap[2] = {0, 0};
+  double* d_pv = nullptr;
+  long long* d_pi = nullptr;
+
+  // host-call staging
+  int16_t* d_pl[2] = {nullptr, nullptr};
+  double* d_val[2] = {nullptr, nullptr};
+  int32_t* d_st[2] = {nullptr, nullptr};
+  int16_t* h_pl_pin[2] = {nullptr, nullptr};
+  double* h_val_pin[2] = {nullptr, nullptr};
+  int32_t* h_st_pin[2] = {nullptr, nullptr};
+  int64_t stage_cap = 0;
+  cudaStream_t pipe[2] = {nullptr, nullptr};
+};
+
+
+namespace helio_engine {
+
+inline int fail(helio_gpu_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(ctx, HELIO_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+}  // namespace helio_engine

@@ -1,0 +1,522 @@
+// route.cu — K3: IWRR per-request route sampling on the GPU.
+//
+// Reference: iwrr_weights (scheduler.cpp:46-56), IwrrPicker::next (:28-44),
+// Scheduler ctor / admit / complete (:58-190), driven in the AC8 order
+// (acceptance_main.cpp:529-537): admit(r, in[r]); if admitted complete(r, out[r]).
+//
+// Closed form (the fast path).  With every hop eligible, IwrrPicker::next at
+// vertex x returns cycle_x[k mod W_x] on its k-th call, where cycle_x is one
+// full (round, index) sweep and W_x = sum of the weights.  In the AC8 order a
+// request's picks happen before the next request's, so the k-th pick at x
+// belongs to the request of rank k among those that reach x.  Every plan edge
+// goes from a node to one with a strictly larger end layer (flow_graph.cpp:121),
+// so processing vertices in end-layer order makes routing level-synchronous:
+// for each vertex, a stable rank (exclusive scan) of the requests waiting there
+// picks their out-edge.  KV masking can only bind when some hop's charge
+// (scheduler.cpp:100-108) may exceed 0.9 * kv_cap; in the AC8 order every
+// charge is released before the next admit, so the host checks that bound with
+// the largest possible running mean of output lengths.  If it may bind (or the
+// plan's exec intervals are not node-consistent) the exact sequential replay
+// kernel runs instead — still on the device.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "engine.h"
+
+using namespace helio_engine;
+
+namespace {
+
+constexpr int kDone = -1;
+
+// iwrr_weights (scheduler.cpp:46-56) for every vertex, then its IWRR cycle.
+__global__ void route_setup(int nv, const int32_t* __restrict__ obeg, const double* __restrict__ flow,
+                            long long* __restrict__ w, const int32_t* __restrict__ cyc_off,
+                            int16_t* __restrict__ cyc, long long* __restrict__ wmax_out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= nv) return;
+  const int b = obeg[x], e = obeg[x + 1];
+  long long wmax = 0;
+  for (int i = b; i < e; ++i) {
+    long long v = llround(1000.0 * flow[i]);
+    w[i] = v > 1 ? v : 1;
+    wmax = w[i] > wmax ? w[i] : wmax;
+  }
+  if (wmax > 32) {
+    for (int i = b; i < e; ++i) {
+      long long v = llround(w[i] * 32.0 / wmax);
+      w[i] = v > 1 ? v : 1;
+    }
+  }
+  long long wm = 1;  // IwrrPicker ctor: wmax_ starts at 1
+  for (int i = b; i < e; ++i) wm = w[i] > wm ? w[i] : wm;
+  wmax_out[x] = wm;
+  int p = cyc_off[x];
+  for (long long r = 1; r <= wm; ++r)
+    for (int i = b; i < e; ++i)
+      if (w[i] >= r) cyc[p++] = (int16_t)(i - b);
+}
+
+__global__ void route_init(int64_t R, int32_t* cur, int32_t* nh, int16_t* cov) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    cur[r] = 0;
+    nh[r] = 0;
+    cov[r] = 0;
+  }
+}
+
+__global__ void route_flag(int64_t R, int x, const int32_t* __restrict__ cur, int32_t* __restrict__ flag) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x)
+    flag[r] = cur[r] == x ? 1 : 0;
+}
+
+__global__ void route_apply(int64_t R, int x, int L, int max_hops, const int32_t* __restrict__ obeg,
+                            const int32_t* __restrict__ odst, const int32_t* __restrict__ oes,
+                            const int32_t* __restrict__ oee, const int32_t* __restrict__ node_of,
+                            const int32_t* __restrict__ cyc_off, const int16_t* __restrict__ cyc,
+                            const int32_t* __restrict__ rank, int32_t* cur, int32_t* nh, int16_t* cov,
+                            int32_t* hop_node, int32_t* hop_s, int32_t* hop_e, int* err) {
+  const int b = obeg[x], deg = obeg[x + 1] - b;
+  const int W = cyc_off[x + 1] - cyc_off[x];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (cur[r] != x) continue;
+    if (deg == 0) {  // IwrrPicker::next on no candidates returns -1: deferred
+      cur[r] = kDone;
+      nh[r] = -1;
+      continue;
+    }
+    const int i = cyc[cyc_off[x] + (int)(rank[r] % W)];
+    const int e = b + i;
+    const int d = odst[e];
+    if (d == 0 || oes[e] != cov[r]) {  // scheduler.cpp:170-171
+      atomicExch(err, 1);
+      cur[r] = kDone;
+      continue;
+    }
+    const int h = nh[r];
+    if (h < max_hops) {
+      hop_node[r * max_hops + h] = node_of[d];
+      hop_s[r * max_hops + h] = oes[e];
+      hop_e[r * max_hops + h] = oee[e];
+    }
+    nh[r] = h + 1;
+    cov[r] = (int16_t)oee[e];
+    cur[r] = oee[e] >= L ? kDone : d;
+  }
+}
+
+// Exact sequential replay of Scheduler::admit/complete (masking may bind).
+__global__ void route_sequential(int64_t R, int nv, int L, int max_hops, double kvb,
+                                 const int32_t* __restrict__ obeg, const int32_t* __restrict__ odst,
+                                 const int32_t* __restrict__ oes, const int32_t* __restrict__ oee,
+                                 const long long* __restrict__ w, const long long* __restrict__ wmaxv,
+                                 const int32_t* __restrict__ node_of, const double* __restrict__ kv_cap,
+                                 double* kv_est, long long* p_round, int32_t* p_idx,
+                                 const int32_t* __restrict__ in_len, const int32_t* __restrict__ out_len,
+                                 int32_t* nh, int32_t* hop_node, int32_t* hop_s, int32_t* hop_e,
+                                 int32_t* ch_v, double* ch_b, long long* deferred, int* err) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int x = 0; x < nv; ++x) {
+    p_round[x] = 1;
+    p_idx[x] = 0;
+    kv_est[x] = 0.0;
+  }
+  double avg = 232.0;
+  long long samples = 1, den = 0;
+  for (int64_t r = 0; r < R; ++r) {
+    int v = 0, covered = 0, n = 0;
+    bool ok = true;
+    while (covered < L) {
+      const int b = obeg[v], deg = obeg[v + 1] - b;
+      int pick = -1;
+      if (deg > 0) {
+        const long long wm = wmaxv[v];
+        const long long positions = wm * (long long)deg;
+        for (long long it = 0; it < positions; ++it) {
+          if (p_idx[v] == deg) {
+            p_idx[v] = 0;
+            p_round[v] = p_round[v] == wm ? 1 : p_round[v] + 1;
+          }
+          const int i = p_idx[v]++;
+          if (w[b + i] >= p_round[v]) {
+            const int d = odst[b + i];
+            bool elig = true;
+            if (d != 0) {
+              const double tokens = in_len[r] + avg;
+              const double charge = tokens * kvb * (double)(oee[b + i] - oes[b + i]);
+              elig = kv_est[d] + charge <= 0.9 * kv_cap[d];
+            }
+            if (elig) {
+              pick = i;
+              break;
+            }
+          }
+        }
+      }
+      if (pick < 0) {
+        for (int q = 0; q < n; ++q) kv_est[ch_v[q]] -= ch_b[q];
+        ok = false;
+        break;
+      }
+      const int e = b + pick, d = odst[e];
+      if (d == 0 || oes[e] != covered) {
+        *err = 1;
+        return;
+      }
+      const double tokens = in_len[r] + avg;
+      const double bytes = tokens * kvb * (double)(oee[e] - oes[e]);
+      kv_est[d] += bytes;
+      ch_v[n] = d;
+      ch_b[n] = bytes;
+      if (n < max_hops) {
+        hop_node[r * max_hops + n] = node_of[d];
+        hop_s[r * max_hops + n] = oes[e];
+        hop_e[r * max_hops + n] = oee[e];
+      }
+      ++n;
+      covered = oee[e];
+      v = d;
+    }
+    if (!ok) {
+      nh[r] = -1;
+      ++den;
+      continue;
+    }
+    nh[r] = n;
+    for (int q = 0; q < n; ++q) kv_est[ch_v[q]] -= ch_b[q];
+    ++samples;
+    avg += (out_len[r] - avg) / (double)samples;
+  }
+  *deferred = den;
+}
+
+template <typename T>
+int dalloc(helio_gpu_ctx* ctx, T** p, size_t n) {
+  CK(cudaMalloc(p, sizeof(T) * std::max<size_t>(n, 1)));
+  return HELIO_OK;
+}
+
+}  // namespace
+
+extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
+                                    const helio_plan_edge* pe, int32_t ne, int64_t R,
+                                    const int32_t* h_in, const int32_t* h_out, int32_t max_hops,
+                                    int32_t* h_nh, int32_t* h_hn, int32_t* h_hs, int32_t* h_he,
+                                    int64_t* h_deferred) {
+  if (!ctx) return HELIO_ERR_INVALID;
+  if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
+  if (!h_pl || (ne > 0 && !pe) || R < 0 || max_hops < 0 || (R > 0 && (!h_in || !h_out || !h_nh)) ||
+      (R > 0 && max_hops > 0 && (!h_hn || !h_hs || !h_he)))
+    return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  CK(cudaSetDevice(ctx->device));
+  const int N = ctx->N, L = ctx->L;
+  // Scheduler ctor (scheduler.cpp:58-98): vertex 0 = coordinator, then the
+  // plan's non-empty nodes in id order.
+  if (ne <= 0) return fail(ctx, HELIO_ERR_INVALID, "plan has no flow edges to schedule on");
+  std::vector<int> order(N);
+  for (int k = 0; k < N; ++k) order[k] = k;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return ctx->h_lexrank[a] < ctx->h_lexrank[b]; });
+  std::vector<int> vof(N, -1);
+  std::vector<int32_t> node_of(1, -1);
+  std::vector<double> kv_cap(1, 0.0);
+  std::vector<int> vend(1, 0);
+  for (int k : order) {
+    const int s = h_pl[2 * k], e = h_pl[2 * k + 1];
+    if (e <= s) continue;
+    vof[k] = (int)node_of.size();
+    node_of.push_back(k);
+    const double held = e - s;
+    const double cap = ctx->h_vram[k] - (e - s) * ctx->bytes_per_layer;
+    (void)held;
+    kv_cap.push_back(0.0 < cap ? cap : 0.0);
+    vend.push_back(e);
+  }
+  const int nv = (int)node_of.size();
+  std::vector<int> esrc(ne), edst(ne);
+  for (int i = 0; i < ne; ++i) {
+    const int a = pe[i].src_node, b = pe[i].dst_node;
+    if (a < -1 || a >= N || b < -1 || b >= N)
+      return fail(ctx, HELIO_ERR_INVALID, "plan edge endpoint out of range");
+    const int va = a < 0 ? 0 : vof[a], vb = b < 0 ? 0 : vof[b];
+    if (va < 0 || vb < 0) return fail(ctx, HELIO_ERR_INVALID, "plan edge references an unplaced node");
+    esrc[i] = va;
+    edst[i] = vb;
+  }
+  std::vector<int32_t> obeg(nv + 1, 0), odst(ne), oes(ne), oee(ne);
+  std::vector<double> oflow(ne);
+  for (int i = 0; i < ne; ++i) obeg[esrc[i] + 1]++;
+  for (int x = 0; x < nv; ++x) obeg[x + 1] += obeg[x];
+  if (obeg[1] == 0) return fail(ctx, HELIO_ERR_INVALID, "plan has no edge leaving the coordinator");
+  {
+    std::vector<int> fill(nv, 0);
+    for (int i = 0; i < ne; ++i) {
+      const int p = obeg[esrc[i]] + fill[esrc[i]]++;
+      odst[p] = edst[i];
+      oes[p] = pe[i].exec_start;
+      oee[p] = pe[i].exec_end;
+      oflow[p] = pe[i].flow;
+    }
+  }
+  // Fast-path eligibility: node-consistent exec intervals, and no hop that
+  // could ever be masked in the AC8 order.
+  bool closed = true;
+  int max_in = 0, max_out = 232;
+  for (int64_t r = 0; r < R; ++r) {
+    max_in = std::max(max_in, h_in[r]);
+    max_out = std::max(max_out, h_out[r]);
+  }
+  const double tok_max = (double)max_in + (double)max_out * (1.0 + 1e-9) + 1.0;
+  for (int x = 0; x < nv && closed; ++x)
+    for (int p = obeg[x]; p < obeg[x + 1]; ++p) {
+      const int d = odst[p];
+      if (d == 0) continue;
+      if (oee[p] != vend[d] || oes[p] != vend[x]) closed = false;
+      const double charge = tok_max * ctx->kv_token_layer_bytes * (double)(oee[p] - oes[p]);
+      if (!(charge * (1.0 + 1e-9) < 0.9 * kv_cap[d])) closed = false;
+    }
+  // weights / cycles: cycle length of x is sum(w) <= 32 * deg
+  std::vector<int32_t> cyc_off(nv + 1, 0);
+  for (int x = 0; x < nv; ++x) cyc_off[x + 1] = cyc_off[x] + 32 * (obeg[x + 1] - obeg[x]);
+
+  cudaStream_t st = ctx->stream;
+  int rc = HELIO_OK;
+  int32_t *d_obeg = nullptr, *d_odst = nullptr, *d_oes = nullptr, *d_oee = nullptr, *d_node = nullptr,
+          *d_cycoff = nullptr, *d_in = nullptr, *d_out = nullptr, *d_cur = nullptr, *d_nh = nullptr,
+          *d_flag = nullptr, *d_rank = nullptr, *d_hn = nullptr, *d_hs = nullptr, *d_he = nullptr,
+          *d_pidx = nullptr, *d_chv = nullptr;
+  double *d_flow = nullptr, *d_kvcap = nullptr, *d_kvest = nullptr, *d_chb = nullptr;
+  long long *d_w = nullptr, *d_wmax = nullptr, *d_pround = nullptr, *d_den = nullptr;
+  int16_t *d_cyc = nullptr, *d_cov = nullptr;
+  int* d_err = nullptr;
+  void* d_tmp = nullptr;
+  size_t tmp_bytes = 0;
+  const size_t HR = (size_t)R * std::max(max_hops, 1);
+#define TRY(x)               \
+  do {                       \
+    if (!rc) rc = (x);       \
+  } while (0)
+  TRY(dalloc(ctx, &d_obeg, nv + 1));
+  TRY(dalloc(ctx, &d_odst, ne));
+  TRY(dalloc(ctx, &d_oes, ne));
+  TRY(dalloc(ctx, &d_oee, ne));
+  TRY(dalloc(ctx, &d_flow, ne));
+  TRY(dalloc(ctx, &d_node, nv));
+  TRY(dalloc(ctx, &d_kvcap, nv));
+  TRY(dalloc(ctx, &d_w, ne));
+  TRY(dalloc(ctx, &d_wmax, nv));
+  TRY(dalloc(ctx, &d_cycoff, nv + 1));
+  TRY(dalloc(ctx, &d_cyc, cyc_off[nv]));
+  TRY(dalloc(ctx, &d_in, R));
+  TRY(dalloc(ctx, &d_out, R));
+  TRY(dalloc(ctx, &d_nh, R));
+  TRY(dalloc(ctx, &d_hn, HR));
+  TRY(dalloc(ctx, &d_hs, HR));
+  TRY(dalloc(ctx, &d_he, HR));
+  TRY(dalloc(ctx, &d_err, 1));
+  TRY(dalloc(ctx, &d_den, 1));
+  if (!rc) {
+    auto H2D = [&](void* d, const void* h, size_t bytes) {
+      if (bytes && !rc && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        rc = fail(ctx, HELIO_ERR_CUDA, "route H2D failed");
+    };
+    H2D(d_obeg, obeg.data(), 4 * (nv + 1));
+    H2D(d_odst, odst.data(), 4 * ne);
+    H2D(d_oes, oes.data(), 4 * ne);
+    H2D(d_oee, oee.data(), 4 * ne);
+    H2D(d_flow, oflow.data(), 8 * ne);
+    H2D(d_node, node_of.data(), 4 * nv);
+    H2D(d_kvcap, kv_cap.data(), 8 * nv);
+    H2D(d_cycoff, cyc_off.data(), 4 * (nv + 1));
+    H2D(d_in, h_in, 4 * R);
+    H2D(d_out, h_out, 4 * R);
+    if (!rc && (cudaMemsetAsync(d_err, 0, sizeof(int), st) != cudaSuccess ||
+                cudaMemsetAsync(d_den, 0, sizeof(long long), st) != cudaSuccess))
+      rc = fail(ctx, HELIO_ERR_CUDA, "route memset failed");
+  }
+  if (!rc) {
+    route_setup<<<(nv + 63) / 64, 64, 0, st>>>(nv, d_obeg, d_flow, d_w, d_cycoff, d_cyc, d_wmax);
+    ctx->launches++;
+    if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route_setup launch failed");
+  }
+  int64_t den = 0;
+  if (!rc && closed && R > 0) {
+    TRY(dalloc(ctx, &d_cur, R));
+    TRY(dalloc(ctx, &d_cov, R));
+    TRY(dalloc(ctx, &d_flag, R));
+    TRY(dalloc(ctx, &d_rank, R));
+    if (!rc) {
+      cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_flag, d_rank, (int)R, st);
+      if (cudaMalloc(&d_tmp, std::max<size_t>(tmp_bytes, 1)) != cudaSuccess)
+        rc = fail(ctx, HELIO_ERR_CUDA, "route scan alloc failed");
+    }
+    if (!rc) {
+      const int grid = (int)std::min<int64_t>((R + 255) / 256, 8 * ctx->sm_count);
+      route_init<<<grid, 256, 0, st>>>(R, d_cur, d_nh, d_cov);
+      ctx->launches++;
+      // vertices in end-layer order (coordinator first); sinks of routes
+      // (end == L) never pick.
+      std::vector<int> vorder;
+      for (int x = 0; x < nv; ++x) vorder.push_back(x);
+      std::stable_sort(vorder.begin(), vorder.end(), [&](int a, int b) { return vend[a] < vend[b]; });
+      for (int x : vorder) {
+        if (x != 0 && vend[x] >= L) continue;
+        route_flag<<<grid, 256, 0, st>>>(R, x, d_cur, d_flag);
+        cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_flag, d_rank, (int)R, st);
+        route_apply<<<grid, 256, 0, st>>>(R, x, L, max_hops, d_obeg, d_odst, d_oes, d_oee, d_node,
+                                           d_cycoff, d_cyc, d_rank, d_cur, d_nh, d_cov, d_hn, d_hs, d_he,
+                                           d_err);
+        ctx->launches += 3;
+      }
+      if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route kernels failed");
+    }
+  } else if (!rc && R > 0) {
+    TRY(dalloc(ctx, &d_kvest, nv));
+    TRY(dalloc(ctx, &d_pround, nv));
+    TRY(dalloc(ctx, &d_pidx, nv));
+    TRY(dalloc(ctx, &d_chv, L + 1));
+    TRY(dalloc(ctx, &d_chb, L + 1));
+    if (!rc) {
+      route_sequential<<<1, 1, 0, st>>>(R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst, d_oes,
+                                        d_oee, d_w, d_wmax, d_node, d_kvcap, d_kvest, d_pround, d_pidx,
+                                        d_in, d_out, d_nh, d_hn, d_hs, d_he, d_chv, d_chb, d_den, d_err);
+      ctx->launches++;
+      if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route_sequential failed");
+    }
+  }
+  int herr = 0;
+  if (!rc && R > 0) {
+    bool ok = cudaMemcpyAsync(h_nh, d_nh, 4 * R, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+              cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, st) == cudaSuccess;
+    if (ok && max_hops > 0)
+      ok = cudaMemcpyAsync(h_hn, d_hn, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+           cudaMemcpyAsync(h_hs, d_hs, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+           cudaMemcpyAsync(h_he, d_he, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+    long long dd = 0;
+    if (ok && !closed) ok = cudaMemcpyAsync(&dd, d_den, sizeof(long long), cudaMemcpyDeviceToHost, st) == cudaSuccess;
+    ok = ok && cudaStreamSynchronize(st) == cudaSuccess;
+    if (!ok) rc = fail(ctx, HELIO_ERR_CUDA, std::string("route: ") + cudaGetErrorString(cudaGetLastError()));
+    if (!rc && closed)
+      for (int64_t r = 0; r < R; ++r) den += h_nh[r] < 0;
+    else
+      den = dd;
+  }
+  if (!rc && herr) rc = fail(ctx, HELIO_ERR_INVALID, "plan edges do not tile the layer range");
+  if (!rc && h_deferred) *h_deferred = den;
+  cudaFree(d_obeg); cudaFree(d_odst); cudaFree(d_oes); cudaFree(d_oee); cudaFree(d_flow); cudaFree(d_node);
+  cudaFree(d_kvcap); cudaFree(d_w); cudaFree(d_wmax); cudaFree(d_cycoff); cudaFree(d_cyc); cudaFree(d_in);
+  cudaFree(d_out); cudaFree(d_nh); cudaFree(d_hn); cudaFree(d_hs); cudaFree(d_he); cudaFree(d_err);
+  cudaFree(d_den); cudaFree(d_cur); cudaFree(d_cov); cudaFree(d_flag); cudaFree(d_rank); cudaFree(d_tmp);
+  cudaFree(d_kvest); cudaFree(d_pround); cudaFree(d_pidx); cudaFree(d_chv); cudaFree(d_chb);
+#undef TRY
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// Stand-alone iwrr_weights / IwrrPicker::next on the device.
+namespace {
+
+__global__ void iwrr_weights_kernel(int n, const double* __restrict__ flow, long long* __restrict__ w) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  long long wmax = 0;
+  for (int i = 0; i < n; ++i) {
+    long long v = llround(1000.0 * flow[i]);
+    w[i] = v > 1 ? v : 1;
+    wmax = w[i] > wmax ? w[i] : wmax;
+  }
+  if (wmax > 32)
+    for (int i = 0; i < n; ++i) {
+      long long v = llround(w[i] * 32.0 / wmax);
+      w[i] = v > 1 ? v : 1;
+    }
+}
+
+__global__ void iwrr_picks_kernel(int n, const long long* __restrict__ w, long long* state, int calls,
+                                  const unsigned long long* __restrict__ masks, int* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  long long round = state[0], idx = state[1];
+  long long wmax = 1;
+  for (int i = 0; i < n; ++i) wmax = w[i] > wmax ? w[i] : wmax;
+  const int words = (n + 63) / 64;
+  for (int k = 0; k < calls; ++k) {
+    int pick = -1;
+    if (n > 0) {
+      const long long positions = wmax * (long long)n;
+      for (long long it = 0; it < positions; ++it) {
+        if (idx == n) {
+          idx = 0;
+          round = round == wmax ? 1 : round + 1;
+        }
+        const int i = (int)idx++;
+        if (w[i] >= round && ((masks[(size_t)k * words + (i >> 6)] >> (i & 63)) & 1ull)) {
+          pick = i;
+          break;
+        }
+      }
+    }
+    out[k] = pick;
+  }
+  state[0] = round;
+  state[1] = idx;
+}
+
+}  // namespace
+
+extern "C" int helio_gpu_iwrr_weights(helio_gpu_ctx* ctx, const double* h_flows, int32_t n, int64_t* h_w) {
+  if (!ctx) return HELIO_ERR_INVALID;
+  if (n < 0 || (n > 0 && (!h_flows || !h_w))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  if (n == 0) return HELIO_OK;
+  CK(cudaSetDevice(ctx->device));
+  double* d_f = nullptr;
+  long long* d_w = nullptr;
+  CK(cudaMalloc(&d_f, 8 * n));
+  CK(cudaMalloc(&d_w, 8 * n));
+  CK(cudaMemcpyAsync(d_f, h_flows, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+  iwrr_weights_kernel<<<1, 32, 0, ctx->stream>>>(n, d_f, d_w);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(h_w, d_w, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_f);
+  cudaFree(d_w);
+  return HELIO_OK;
+}
+
+extern "C" int helio_gpu_iwrr_picks(helio_gpu_ctx* ctx, const int64_t* h_w, int32_t n, int64_t* h_round,
+                                    int64_t* h_idx, int32_t calls, const uint64_t* h_masks, int32_t* h_out) {
+  if (!ctx) return HELIO_ERR_INVALID;
+  if (n < 0 || calls < 0 || !h_round || !h_idx || (n > 0 && !h_w) || (calls > 0 && (!h_out || (n > 0 && !h_masks))))
+    return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  if (calls == 0) return HELIO_OK;
+  CK(cudaSetDevice(ctx->device));
+  const int words = (n + 63) / 64;
+  long long *d_w = nullptr, *d_state = nullptr;
+  unsigned long long* d_m = nullptr;
+  int* d_out = nullptr;
+  long long st[2] = {(long long)*h_round, (long long)*h_idx};
+  CK(cudaMalloc(&d_w, 8 * std::max(n, 1)));
+  CK(cudaMalloc(&d_state, 16));
+  CK(cudaMalloc(&d_m, 8 * std::max<size_t>((size_t)calls * words, 1)));
+  CK(cudaMalloc(&d_out, 4 * calls));
+  if (n > 0) CK(cudaMemcpyAsync(d_w, h_w, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d_state, st, 16, cudaMemcpyHostToDevice, ctx->stream));
+  if (n > 0) CK(cudaMemcpyAsync(d_m, h_masks, 8 * (size_t)calls * words, cudaMemcpyHostToDevice, ctx->stream));
+  iwrr_picks_kernel<<<1, 32, 0, ctx->stream>>>(n, d_w, d_state, calls, d_m, d_out);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(h_out, d_out, 4 * calls, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(st, d_state, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *h_round = st[0];
+  *h_idx = st[1];
+  cudaFree(d_w);
+  cudaFree(d_state);
+  cudaFree(d_m);
+  cudaFree(d_out);
+  return HELIO_OK;
+}
