@@ -204,7 +204,10 @@ def main():
     N, L = eng.num_nodes, eng.num_layers
     B = args.per_gpu
     first = rank * B
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: its handle is what the engine launches on, and the
+    # CUDA events below are recorded on the same stream
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
 
     pl = torch.empty((B, N, 2), dtype=torch.int16, device=dev)

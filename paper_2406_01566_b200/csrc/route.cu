@@ -35,7 +35,8 @@ constexpr int kDone = -1;
 // iwrr_weights (scheduler.cpp:46-56) for every vertex, then its IWRR cycle.
 __global__ void route_setup(int nv, const int32_t* __restrict__ obeg, const double* __restrict__ flow,
                             long long* __restrict__ w, const int32_t* __restrict__ cyc_off,
-                            int16_t* __restrict__ cyc, long long* __restrict__ wmax_out) {
+                            int16_t* __restrict__ cyc, long long* __restrict__ wmax_out,
+                            int32_t* __restrict__ cyc_len) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= nv) return;
   const int b = obeg[x], e = obeg[x + 1];
@@ -58,6 +59,7 @@ __global__ void route_setup(int nv, const int32_t* __restrict__ obeg, const doub
   for (long long r = 1; r <= wm; ++r)
     for (int i = b; i < e; ++i)
       if (w[i] >= r) cyc[p++] = (int16_t)(i - b);
+  cyc_len[x] = p - cyc_off[x];  // W_x = sum of the weights
 }
 
 __global__ void route_init(int64_t R, int32_t* cur, int32_t* nh, int16_t* cov) {
@@ -78,11 +80,11 @@ __global__ void route_flag(int64_t R, int x, const int32_t* __restrict__ cur, in
 __global__ void route_apply(int64_t R, int x, int L, int max_hops, const int32_t* __restrict__ obeg,
                             const int32_t* __restrict__ odst, const int32_t* __restrict__ oes,
                             const int32_t* __restrict__ oee, const int32_t* __restrict__ node_of,
-                            const int32_t* __restrict__ cyc_off, const int16_t* __restrict__ cyc,
-                            const int32_t* __restrict__ rank, int32_t* cur, int32_t* nh, int16_t* cov,
+                            const int32_t* __restrict__ cyc_off, const int32_t* __restrict__ cyc_len,
+                            const int16_t* __restrict__ cyc, const int32_t* __restrict__ rank, int32_t* cur, int32_t* nh, int16_t* cov,
                             int32_t* hop_node, int32_t* hop_s, int32_t* hop_e, int* err) {
   const int b = obeg[x], deg = obeg[x + 1] - b;
-  const int W = cyc_off[x + 1] - cyc_off[x];
+  const int W = cyc_len[x];
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     if (cur[r] != x) continue;
@@ -289,7 +291,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   int32_t *d_obeg = nullptr, *d_odst = nullptr, *d_oes = nullptr, *d_oee = nullptr, *d_node = nullptr,
           *d_cycoff = nullptr, *d_in = nullptr, *d_out = nullptr, *d_cur = nullptr, *d_nh = nullptr,
           *d_flag = nullptr, *d_rank = nullptr, *d_hn = nullptr, *d_hs = nullptr, *d_he = nullptr,
-          *d_pidx = nullptr, *d_chv = nullptr;
+          *d_pidx = nullptr, *d_chv = nullptr, *d_cyclen = nullptr;
   double *d_flow = nullptr, *d_kvcap = nullptr, *d_kvest = nullptr, *d_chb = nullptr;
   long long *d_w = nullptr, *d_wmax = nullptr, *d_pround = nullptr, *d_den = nullptr;
   int16_t *d_cyc = nullptr, *d_cov = nullptr;
@@ -312,6 +314,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   TRY(dalloc(ctx, &d_wmax, nv));
   TRY(dalloc(ctx, &d_cycoff, nv + 1));
   TRY(dalloc(ctx, &d_cyc, cyc_off[nv]));
+  TRY(dalloc(ctx, &d_cyclen, nv));
   TRY(dalloc(ctx, &d_in, R));
   TRY(dalloc(ctx, &d_out, R));
   TRY(dalloc(ctx, &d_nh, R));
@@ -340,7 +343,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
       rc = fail(ctx, HELIO_ERR_CUDA, "route memset failed");
   }
   if (!rc) {
-    route_setup<<<(nv + 63) / 64, 64, 0, st>>>(nv, d_obeg, d_flow, d_w, d_cycoff, d_cyc, d_wmax);
+    route_setup<<<(nv + 63) / 64, 64, 0, st>>>(nv, d_obeg, d_flow, d_w, d_cycoff, d_cyc, d_wmax, d_cyclen);
     ctx->launches++;
     if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route_setup launch failed");
   }
@@ -369,7 +372,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
         route_flag<<<grid, 256, 0, st>>>(R, x, d_cur, d_flag);
         cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_flag, d_rank, (int)R, st);
         route_apply<<<grid, 256, 0, st>>>(R, x, L, max_hops, d_obeg, d_odst, d_oes, d_oee, d_node,
-                                           d_cycoff, d_cyc, d_rank, d_cur, d_nh, d_cov, d_hn, d_hs, d_he,
+                                           d_cycoff, d_cyclen, d_cyc, d_rank, d_cur, d_nh, d_cov, d_hn, d_hs, d_he,
                                            d_err);
         ctx->launches += 3;
       }
@@ -412,7 +415,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   cudaFree(d_kvcap); cudaFree(d_w); cudaFree(d_wmax); cudaFree(d_cycoff); cudaFree(d_cyc); cudaFree(d_in);
   cudaFree(d_out); cudaFree(d_nh); cudaFree(d_hn); cudaFree(d_hs); cudaFree(d_he); cudaFree(d_err);
   cudaFree(d_den); cudaFree(d_cur); cudaFree(d_cov); cudaFree(d_flag); cudaFree(d_rank); cudaFree(d_tmp);
-  cudaFree(d_kvest); cudaFree(d_pround); cudaFree(d_pidx); cudaFree(d_chv); cudaFree(d_chb);
+  cudaFree(d_cyclen); cudaFree(d_kvest); cudaFree(d_pround); cudaFree(d_pidx); cudaFree(d_chv); cudaFree(d_chb);
 #undef TRY
   return rc;
 }
