@@ -54,6 +54,17 @@ extern "C" {
 #define HELIO_CAND_TOO_LARGE 4    /* graph does not fit one SM's shared memory */
 #define HELIO_CAND_EDGE_BUFFER 5  /* flows: caller's max_edges too small (num_edges holds the need) */
 
+/* scoring modes (helio_gpu_set_mode):
+ *   PARITY — replays the reference's FIFO preflow-push discharge sequence
+ *            (flow_graph.cpp:138-229): values and per-edge flows are
+ *            bit-identical to the reference.  Default; used for every
+ *            per-edge-flow entry point.
+ *   SCORE  — value only (Edmonds-Karp shortest augmenting paths).  Exact on
+ *            integer capacities; within rounding (<= 1e-6 relative, asserted
+ *            by the tests) on float capacities.  For bulk placement search. */
+#define HELIO_MODE_PARITY 0
+#define HELIO_MODE_SCORE 1
+
 /* edge kinds, same numbering as helio::EdgeKind (flow_graph.hpp:21) */
 #define HELIO_EDGE_COMPUTE 0
 #define HELIO_EDGE_COORD_OUT 1
@@ -111,6 +122,9 @@ int helio_gpu_sync(helio_gpu_ctx* ctx);
 
 /* K0: compile and upload a cluster.  k_out (optional, [N]) receives k_i. */
 int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* desc, int32_t* k_out);
+
+int helio_gpu_set_mode(helio_gpu_ctx* ctx, int mode);
+int helio_gpu_get_mode(const helio_gpu_ctx* ctx);
 
 /* compute_edge_capacity(c, node, j) for 1 <= j <= k_i, from the compiled table. */
 int helio_gpu_compute_edge_capacity(const helio_gpu_ctx* ctx, int32_t node, int32_t j, double* out);

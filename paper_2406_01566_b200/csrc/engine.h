@@ -56,7 +56,8 @@ struct helio_gpu_ctx {
   void* d_cluster = nullptr;  // one allocation for all constant arrays
   int32_t* d_kmax32 = nullptr;
   helio_engine::Layout small{}, big{};
-  int small_warps = 4, small_blocks = 0, big_blocks = 0;
+  int small_warps = 4, small_blocks[2] = {0, 0}, big_blocks[2] = {0, 0};
+  int mode = 0;  // HELIO_MODE_PARITY
   bool big_ok = false;
 
   // scratch, two sets (one per pipeline stream)

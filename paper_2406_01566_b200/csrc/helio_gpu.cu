@@ -301,6 +301,79 @@ __device__ void solve_fifo(const Gs& g, const int n, const int s, const int t, c
 }
 
 // ---------------------------------------------------------------------------
+// SCORE mode: value-only Edmonds-Karp (shortest augmenting paths), one warp
+// per graph.  BFS dequeues one vertex at a time and tests all its arcs with
+// one ballot (built graphs have distinct targets per adjacency list); the
+// bottleneck to each discovered vertex rides along the BFS tree, so the path
+// is traced only once to apply the augmentation.  Exact on integer
+// capacities (every intermediate is an integer-valued double); on float
+// capacities the value differs from the reference's FIFO preflow-push only by
+// rounding (north_star tolerance 1e-6 relative; tests assert it).  Arc order
+// does not matter here.  Slot reuse: h = BFS parent arc, q = BFS queue,
+// ex = bottleneck capacity from the source.
+__device__ double solve_ek(const Gs& g, const int n, const int s, const int t, const int lane) {
+  double value = 0.0;
+  for (;;) {
+    for (int x = lane; x < n; x += 32) g.h[x] = -1;
+    __syncwarp();
+    if (lane == 0) {
+      g.h[s] = -2;
+      g.q[0] = (int16_t)s;
+      g.ex[s] = 1.0e300;
+    }
+    __syncwarp();
+    int qh = 0, qt = 1;
+    bool found = false;
+    while (qh < qt) {
+      const int u = g.q[qh++];
+      const double bu = g.ex[u];
+      const int b = g.abeg[u], e = g.abeg[u + 1];
+      for (int a0 = b; a0 < e; a0 += 32) {
+        const int a = a0 + lane;
+        bool ok = false;
+        int v = 0;
+        double c = 0.0;
+        if (a < e) {
+          c = g.cap[a];
+          if (c > FLOW_EPS) {
+            v = g.to[a];
+            ok = g.h[v] == -1;
+          }
+        }
+        const unsigned m = __ballot_sync(FULL, ok);
+        if (ok) {
+          g.h[v] = (int16_t)a;
+          g.q[qt + __popc(m & lanemask_lt())] = (int16_t)v;
+          g.ex[v] = ref_min(bu, c);
+        }
+        qt += __popc(m);
+        if (__any_sync(FULL, ok && v == t)) {
+          found = true;
+          break;
+        }
+      }
+      __syncwarp();
+      if (found) break;
+    }
+    if (!found) break;
+    const double f = g.ex[t];
+    if (lane == 0) {
+      int x = t;
+      while (x != s) {
+        const int a = g.h[x];
+        const int r = g.rv[a];
+        g.cap[a] -= f;
+        g.cap[r] += f;
+        x = g.to[r];
+      }
+    }
+    __syncwarp();
+    value += f;
+  }
+  return value;
+}
+
+// ---------------------------------------------------------------------------
 // K1: build the reference's FlowGraph for one placement row into the slot.
 // Vertex numbering (flow_graph.cpp:63-69): source 0, sink 1, then (in, out)
 // pairs of the used nodes in byte-lexicographic id order.  Edge order: compute
@@ -574,6 +647,7 @@ struct FlowOut {
 
 // Persistent: every warp loops fetching candidate indices.  big == 0: all B
 // candidates, overflowing graphs appended to ovf; big == 1: the ovf list.
+template <int MODE>
 __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restrict__ pl, int64_t B,
                              int partial, double* __restrict__ values, int32_t* __restrict__ status,
                              unsigned long long* work, int64_t* ovf, unsigned int* ovf_count,
@@ -599,7 +673,9 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
       st = HELIO_CAND_TOO_LARGE;
     }
     double value = 0.0;
-    if (st == 0) {
+    if (st == 0 && MODE == HELIO_MODE_SCORE) {
+      value = solve_ek(g, V, 0, 1, lane);
+    } else if (st == 0) {
       solve_fifo(g, V, 0, 1, lane);
       value = built_value(cd, g, lane);
       if (fo.edges) {
@@ -820,18 +896,23 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   }
   if ((size_t)ctx->small.bytes * ctx->small_warps > max_smem)
     return fail(ctx, HELIO_ERR_TOO_LARGE, "cluster too large: one graph slot exceeds shared memory");
-  CK(cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, 32 * ctx->small_warps,
-                                                   ctx->small.bytes * ctx->small_warps));
-  if (per_sm < 1) per_sm = 1;
-  ctx->small_blocks = per_sm * ctx->sm_count;
-  int per_sm_big = 0;
-  if (ctx->big_ok) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_big, score_kernel, 32, ctx->big.bytes));
-    if (per_sm_big < 1) per_sm_big = 1;
+  // occupancy of both instantiations (PARITY / SCORE)
+  void* fns[2] = {reinterpret_cast<void*>(score_kernel<HELIO_MODE_PARITY>),
+                  reinterpret_cast<void*>(score_kernel<HELIO_MODE_SCORE>)};
+  for (int m = 0; m < 2; ++m) {
+    CK(cudaFuncSetAttribute(fns[m], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[m], 32 * ctx->small_warps,
+                                                     ctx->small.bytes * ctx->small_warps));
+    if (per_sm < 1) per_sm = 1;
+    ctx->small_blocks[m] = per_sm * ctx->sm_count;
+    int per_sm_big = 1;
+    if (ctx->big_ok) {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_big, fns[m], 32, ctx->big.bytes));
+      if (per_sm_big < 1) per_sm_big = 1;
+    }
+    ctx->big_blocks[m] = per_sm_big * ctx->sm_count;
   }
-  ctx->big_blocks = per_sm_big * ctx->sm_count;
   return HELIO_OK;
 }
 
@@ -844,32 +925,35 @@ int ensure_ovf(helio_gpu_ctx* ctx, int set, int64_t B) {
   return HELIO_OK;
 }
 
+template <int MODE>
+void launch_score_mode(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, int partial, double* d_val,
+                       int32_t* d_st, cudaStream_t st, FlowOut fo, bool timed) {
+  unsigned long long* work = ctx->d_work + 2 * set;
+  unsigned int* oc = ctx->d_ovf_count + set;
+  if (timed) cudaEventRecord(ctx->ev0, st);
+  const int grid = (int)std::min<int64_t>(ctx->small_blocks[MODE], (B + ctx->small_warps - 1) / ctx->small_warps);
+  score_kernel<MODE><<<grid, 32 * ctx->small_warps, ctx->small.bytes * ctx->small_warps, st>>>(
+      ctx->cd, ctx->small, d_pl, B, partial, d_val, d_st, work, ctx->d_ovf[set], oc, 0, fo);
+  if (timed) cudaEventRecord(ctx->ev1, st);
+  // graphs that overflowed the small slot: same kernel, one warp per CTA, big slot
+  const Layout& bl = ctx->big_ok ? ctx->big : ctx->small;
+  score_kernel<MODE><<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
+                                                                   work + 1, ctx->d_ovf[set], oc, 1, fo);
+}
+
 int launch_score(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, int partial,
-                 double* d_val, int32_t* d_st, cudaStream_t st, FlowOut fo, bool timed) {
+                 double* d_val, int32_t* d_st, cudaStream_t st, FlowOut fo, bool timed, int mode) {
   if (B <= 0) return HELIO_OK;
   int rc = ensure_ovf(ctx, set, B);
   if (rc) return rc;
-  unsigned long long* work = ctx->d_work + 2 * set;
-  unsigned int* oc = ctx->d_ovf_count + set;
-  CK(cudaMemsetAsync(work, 0, 2 * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(oc, 0, sizeof(unsigned int), st));
-  if (timed) CK(cudaEventRecord(ctx->ev0, st));
-  int grid = (int)std::min<int64_t>(ctx->small_blocks, (B + ctx->small_warps - 1) / ctx->small_warps);
-  score_kernel<<<grid, 32 * ctx->small_warps, ctx->small.bytes * ctx->small_warps, st>>>(
-      ctx->cd, ctx->small, d_pl, B, partial, d_val, d_st, work, ctx->d_ovf[set], oc, 0, fo);
+  CK(cudaMemsetAsync(ctx->d_work + 2 * set, 0, 2 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(ctx->d_ovf_count + set, 0, sizeof(unsigned int), st));
+  if (mode == HELIO_MODE_SCORE && fo.edges == nullptr)
+    launch_score_mode<HELIO_MODE_SCORE>(ctx, set, d_pl, B, partial, d_val, d_st, st, fo, timed);
+  else
+    launch_score_mode<HELIO_MODE_PARITY>(ctx, set, d_pl, B, partial, d_val, d_st, st, fo, timed);
   CK(cudaGetLastError());
-  if (timed) CK(cudaEventRecord(ctx->ev1, st));
-  ctx->launches++;
-  if (ctx->big_ok) {
-    score_kernel<<<ctx->big_blocks, 32, ctx->big.bytes, st>>>(ctx->cd, ctx->big, d_pl, B, partial,
-                                                              d_val, d_st, work + 1, ctx->d_ovf[set],
-                                                              oc, 1, fo);
-  } else {
-    score_kernel<<<ctx->big_blocks > 0 ? ctx->big_blocks : ctx->sm_count, 32, ctx->small.bytes, st>>>(
-        ctx->cd, ctx->small, d_pl, B, partial, d_val, d_st, work + 1, ctx->d_ovf[set], oc, 1, fo);
-  }
-  CK(cudaGetLastError());
-  ctx->launches++;
+  ctx->launches += 2;
   if (timed) ctx->timed = true;
   return HELIO_OK;
 }
@@ -1130,6 +1214,15 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   return HELIO_OK;
 }
 
+int helio_gpu_set_mode(helio_gpu_ctx* ctx, int mode) {
+  if (!ctx) return HELIO_ERR_INVALID;
+  if (mode != HELIO_MODE_PARITY && mode != HELIO_MODE_SCORE) return fail(ctx, HELIO_ERR_INVALID, "unknown mode");
+  ctx->mode = mode;
+  return HELIO_OK;
+}
+
+int helio_gpu_get_mode(const helio_gpu_ctx* ctx) { return ctx ? ctx->mode : -1; }
+
 int helio_gpu_compute_edge_capacity(const helio_gpu_ctx* ctx, int32_t node, int32_t j, double* out) {
   if (!ctx || !ctx->has_cluster || !out) return HELIO_ERR_NO_CLUSTER;
   if (node < 0 || node >= ctx->N || j < 1 || j > ctx->h_kmax[node]) return HELIO_ERR_INVALID;
@@ -1145,7 +1238,7 @@ int helio_gpu_score(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int allo
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   FlowOut fo{nullptr, nullptr, nullptr, 0};
-  return launch_score(ctx, 0, d_pl, B, allow_partial ? 1 : 0, d_values, d_status, st, fo, true);
+  return launch_score(ctx, 0, d_pl, B, allow_partial ? 1 : 0, d_values, d_status, st, fo, true, ctx->mode);
 }
 
 int helio_gpu_score_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allow_partial,
@@ -1183,7 +1276,7 @@ int helio_gpu_score_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int
     }
     CK(cudaMemcpyAsync(ctx->d_pl[s], src, row * n, cudaMemcpyHostToDevice, st));
     rc = launch_score(ctx, s, ctx->d_pl[s], n, allow_partial ? 1 : 0, ctx->d_val[s], ctx->d_st[s], st, fo,
-                      false);
+                      false, ctx->mode);
     if (rc) return rc;
     double* vdst = pin_out ? h_values + lo : ctx->h_val_pin[s];
     int32_t* sdst = pin_out ? h_status + lo : ctx->h_st_pin[s];
@@ -1228,7 +1321,7 @@ int helio_gpu_flows_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t K, int
     rc = fail(ctx, HELIO_ERR_CUDA, "H2D failed in flows");
   if (!rc) {
     FlowOut fo{d_ed, d_nv, d_ne, max_edges};
-    rc = launch_score(ctx, 0, d_pl, K, allow_partial ? 1 : 0, d_val, d_st, st, fo, false);
+    rc = launch_score(ctx, 0, d_pl, K, allow_partial ? 1 : 0, d_val, d_st, st, fo, false, HELIO_MODE_PARITY);
   }
   if (!rc) {
     bool ok = cudaMemcpyAsync(h_values, d_val, 8 * K, cudaMemcpyDeviceToHost, st) == cudaSuccess &&

@@ -662,6 +662,14 @@ PYBIND11_MODULE(_helio, m) {
       .def_property_readonly("device", [](const PyEngine& e) { return e.eng->device(); })
       .def_property_readonly("launch_count", [](const PyEngine& e) { return helio_gpu_launch_count(e.eng->ctx()); })
       .def("last_kernel_ms", [](const PyEngine& e) { return helio_gpu_last_kernel_ms(e.eng->ctx()); })
+      .def_property(
+          "mode", [](const PyEngine& e) { return helio_gpu_get_mode(e.eng->ctx()) == HELIO_MODE_SCORE ? "score" : "parity"; },
+          [](PyEngine& e, const std::string& m) {
+            if (m != "parity" && m != "score") throw ValidationError("mode must be 'parity' or 'score'");
+            e.eng->check(helio_gpu_set_mode(e.eng->ctx(), m == "score" ? HELIO_MODE_SCORE : HELIO_MODE_PARITY),
+                         "helio_gpu_set_mode");
+          },
+          "'parity' (bit-exact FIFO replay, default) or 'score' (value-only Edmonds-Karp)")
       .def("score", &engine_score, py::arg("placements"), py::arg("allow_partial") = true,
            "Host arrays in, (values, status) out; copies inside.")
       .def(

@@ -212,3 +212,66 @@ def test_iwrr_weights_and_picker_bit_exact():
         p = h.IwrrPicker(w)
         got = [p.next(lambda j, m=int(m): bool((m >> j) & 1)) for m in masks]
         assert got == list(want), i
+
+
+# --- SCORE mode (value-only Edmonds-Karp) -------------------------------------
+# north_star: bit-exact values on integer capacities, within 1e-6 relative on
+# float capacities.  Statuses are identical in both modes.
+SCORE_REL_TOL = 1e-6
+
+
+@pytest.mark.parametrize("key", CAND_FIXTURES)
+def test_score_mode_against_reference(key):
+    z = golden(f"cand_{key}.npz")
+    c, e = engine(key)
+    e.mode = "score"
+    try:
+        for partial, vk, sk in ((True, "values_partial", "status_partial"),
+                                (False, "values_strict", "status_strict")):
+            v, s = e.score(z["rows"], partial)
+            assert np.array_equal(s, z[sk]), key
+            if key.endswith("_int"):
+                assert np.array_equal(bits(v), bits(z[vk])), key
+            else:
+                ref = z[vk]
+                assert np.all(np.abs(v - ref) <= SCORE_REL_TOL * np.maximum(1.0, np.abs(ref))), key
+    finally:
+        e.mode = "parity"
+
+
+@pytest.mark.parametrize("name", ["het42-70b", "single24-30b", "geo24", "single24-70b"])
+@pytest.mark.parametrize("cap", ["float", "int"])
+def test_score_mode_seeded_batches(name, cap):
+    d = clusters.CONFIGS[name](cap)
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    e.mode = "score"
+    o = Oracle(d)
+    rows = np.concatenate([h.generate_host(list(e.kmax), c.num_layers, 31, 0, 3000, 0),
+                           h.generate_host(list(e.kmax), c.num_layers, 31, 10**6, 1000, 150000)])
+    v, s = e.score(rows)
+    vo, so = o.score(rows)
+    assert np.array_equal(s, so)
+    if cap == "int":
+        assert np.array_equal(bits(v), bits(vo))
+    else:
+        assert np.all(np.abs(v - vo) <= SCORE_REL_TOL * np.maximum(1.0, np.abs(vo)))
+
+
+def test_score_mode_full_size_matches_parity_mode():
+    import torch
+    d = clusters.CONFIGS["het42-70b"]("int")
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    B = 1_000_000
+    pl = torch.empty((B, e.num_nodes, 2), dtype=torch.int16, device="cuda")
+    e.generate_device(77, 0, B, 50000, pl.data_ptr(), 0)
+    vp = torch.empty(B, dtype=torch.float64, device="cuda")
+    vs = torch.empty(B, dtype=torch.float64, device="cuda")
+    st = torch.empty(B, dtype=torch.int32, device="cuda")
+    e.score_device(pl.data_ptr(), B, vp.data_ptr(), st.data_ptr(), True, 0)
+    e.mode = "score"
+    e.score_device(pl.data_ptr(), B, vs.data_ptr(), st.data_ptr(), True, 0)
+    torch.cuda.synchronize()
+    # integer capacities: the two algorithms agree bit for bit at full size
+    assert torch.equal(vp.view(torch.int64), vs.view(torch.int64))

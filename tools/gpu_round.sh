@@ -1,6 +1,4 @@
 set -x
-timeout 900 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -15 gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests -q -m gpu --timeout 600 -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -15 gpurun_out/pytest_gpu.log
 timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1; echo bench=$?; tail -3 gpurun_out/bench_full.log
-timeout 300 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo ref=$?; tail -2 gpurun_out/bench_ref.log
-timeout 300 python tools/profile_score.py > gpurun_out/prof_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_kernel -c 1 -o gpurun_out/prof_score python tools/profile_score.py > gpurun_out/ncu_full.log 2>&1; echo ncu=$?; tail -3 gpurun_out/ncu_full.log
-timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/plain_launch.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu2=$?
+timeout 300 python tools/profile_score.py --mode score > gpurun_out/prof_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_kernel -c 1 -o gpurun_out/prof_score_ek python tools/profile_score.py --mode score > gpurun_out/ncu_full.log 2>&1; echo ncu=$?; tail -3 gpurun_out/ncu_full.log

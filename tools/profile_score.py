@@ -15,9 +15,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="het42-70b")
 ap.add_argument("--count", type=int, default=200_000)
 ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--mode", default="score", choices=["score", "parity"])
 a = ap.parse_args()
 c = h.Cluster.from_json(json.dumps(clusters.CONFIGS[a.config]("float")))
 e = h.Engine(c)
+e.mode = a.mode
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 pl = torch.empty((a.count, e.num_nodes, 2), dtype=torch.int16, device="cuda")
@@ -27,5 +29,5 @@ st = torch.empty(a.count, dtype=torch.int32, device="cuda")
 for _ in range(a.repeat):
     e.score_device(pl.data_ptr(), a.count, v.data_ptr(), st.data_ptr(), True, s.cuda_stream)
 torch.cuda.synchronize()
-print(json.dumps({"config": a.config, "count": a.count, "kernel_ms": e.last_kernel_ms(),
+print(json.dumps({"mode": a.mode, "config": a.config, "count": a.count, "kernel_ms": e.last_kernel_ms(),
                   "evals_per_s": a.count / (e.last_kernel_ms() / 1e3), "mean_value": float(v.mean())}))
