@@ -22,6 +22,13 @@ struct ClusterDev {
   const uint32_t* link_pack;  // [Mv] (src+1) | (dst+1) << 16, 0 = coordinator
   const double* link_cap;     // [Mv] link_token_capacity with the reference payload
   const double* cin_cap;      // [N] capacity of node -> coordinator edge (value sum)
+  // SCORE builder (arc order free): per-node link lists.
+  const int32_t* cout_link;   // [N] link index of coordinator -> node, -1 none
+  const int32_t* cin_link;    // [N] link index of node -> coordinator, -1 none
+  const int32_t* out_beg;     // [N+1] into out_list
+  const int32_t* in_beg;      // [N+1] into in_list
+  const int2* out_list;       // (dst node, link index) of node -> node links
+  const int2* in_list;        // (src node, link index)
 };
 
 // Shared-memory slot layout of one graph (byte offsets from the slot base).

@@ -302,76 +302,11 @@ __device__ void solve_fifo(const Gs& g, const int n, const int s, const int t, c
 
 // ---------------------------------------------------------------------------
 // SCORE mode: value-only Edmonds-Karp (shortest augmenting paths), one warp
-// per graph.  BFS dequeues one vertex at a time and tests all its arcs with
-// one ballot (built graphs have distinct targets per adjacency list); the
-// bottleneck to each discovered vertex rides along the BFS tree, so the path
-// is traced only once to apply the augmentation.  Exact on integer
-// capacities (every intermediate is an integer-valued double); on float
-// capacities the value differs from the reference's FIFO preflow-push only by
-// rounding (north_star tolerance 1e-6 relative; tests assert it).  Arc order
-// does not matter here.  Slot reuse: h = BFS parent arc, q = BFS queue,
-// ex = bottleneck capacity from the source.
-__device__ double solve_ek(const Gs& g, const int n, const int s, const int t, const int lane) {
-  double value = 0.0;
-  for (;;) {
-    for (int x = lane; x < n; x += 32) g.h[x] = -1;
-    __syncwarp();
-    if (lane == 0) {
-      g.h[s] = -2;
-      g.q[0] = (int16_t)s;
-      g.ex[s] = 1.0e300;
-    }
-    __syncwarp();
-    int qh = 0, qt = 1;
-    bool found = false;
-    while (qh < qt) {
-      const int u = g.q[qh++];
-      const double bu = g.ex[u];
-      const int b = g.abeg[u], e = g.abeg[u + 1];
-      for (int a0 = b; a0 < e; a0 += 32) {
-        const int a = a0 + lane;
-        bool ok = false;
-        int v = 0;
-        double c = 0.0;
-        if (a < e) {
-          c = g.cap[a];
-          if (c > FLOW_EPS) {
-            v = g.to[a];
-            ok = g.h[v] == -1;
-          }
-        }
-        const unsigned m = __ballot_sync(FULL, ok);
-        if (ok) {
-          g.h[v] = (int16_t)a;
-          g.q[qt + __popc(m & lanemask_lt())] = (int16_t)v;
-          g.ex[v] = ref_min(bu, c);
-        }
-        qt += __popc(m);
-        if (__any_sync(FULL, ok && v == t)) {
-          found = true;
-          break;
-        }
-      }
-      __syncwarp();
-      if (found) break;
-    }
-    if (!found) break;
-    const double f = g.ex[t];
-    if (lane == 0) {
-      int x = t;
-      while (x != s) {
-        const int a = g.h[x];
-        const int r = g.rv[a];
-        g.cap[a] -= f;
-        g.cap[r] += f;
-        x = g.to[r];
-      }
-    }
-    __syncwarp();
-    value += f;
-  }
-  return value;
-}
+// per graph — see solve_ek_batched below.  Exact on integer capacities (every
+// intermediate is an integer-valued double); on float capacities the value
+// differs from the reference's FIFO preflow-push only by rounding (north_star
+// tolerance 1e-6 relative; tests assert it).  Slot reuse: h = BFS parent arc,
+// q = BFS queue, ex = bottleneck capacity from the source.
 
 // ---------------------------------------------------------------------------
 // K1: build the reference's FlowGraph for one placement row into the slot.
@@ -560,6 +495,281 @@ __device__ int build_graph(const ClusterDev& cd, const Gs& g, const Layout& lay,
   return 0;
 }
 
+// SCORE-mode builder.  Same graph as build_graph up to vertex numbering and
+// arc order, which the value does not depend on: node k owns vertices
+// in = 2 + 2k, out = 3 + 2k (unused nodes keep no arcs), and each lane walks
+// its node's precomputed out-/in-link lists instead of scanning every link
+// of the cluster.  Validation and status codes are shared with build_graph.
+__device__ __forceinline__ bool edge_ok(int aend, int bs, int be, int partial) {
+  return partial ? (bs <= aend && aend < be) : (aend == bs);
+}
+
+__device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
+                                 int partial, int lane, int& V, int& E) {
+  const int N = cd.N, L = cd.L;
+  int bad = INT_MAX;
+  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = __ldg(row32 + k);
+    const int s = (int16_t)(w & 0xffff);
+    const int e = (int16_t)(w >> 16);
+    g.ps[k] = (int16_t)s;
+    g.pe[k] = (int16_t)e;
+    if (e > s) {
+      int code = 0;
+      if (s < 0 || e > L) code = 2;
+      else if (e - s > __ldg(cd.kmax + k)) code = 3;
+      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
+    }
+  }
+  bad = __reduce_min_sync(FULL, bad);
+  if (bad != INT_MAX) return bad & 3;
+  V = 2 + 2 * N;
+  if (V > lay.V) return ST_OVERFLOW;
+  __syncwarp();
+  // degrees: in_k = compute + valid in-links + source arc; out_k = compute +
+  // valid out-links + sink arc.
+  int nedges = 0, dsrc = 0, dsink = 0;
+  int* fill = reinterpret_cast<int*>(g.ex);  // int counters per vertex during the build
+  for (int k = lane; k < N; k += 32) {
+    const int s = g.ps[k], e = g.pe[k];
+    int din = 0, dout = 0;
+    if (e > s) {
+      din = 1;
+      dout = 1;
+      ++nedges;
+      for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
+        const int j = __ldg(&cd.out_list[p].x);
+        const int sj = g.ps[j], ej = g.pe[j];
+        if (ej > sj && edge_ok(e, sj, ej, partial)) ++dout;
+      }
+      for (int p = __ldg(cd.in_beg + k), pe_ = __ldg(cd.in_beg + k + 1); p < pe_; ++p) {
+        const int i = __ldg(&cd.in_list[p].x);
+        const int si = g.ps[i], ei = g.pe[i];
+        if (ei > si && edge_ok(ei, s, e, partial)) ++din;
+      }
+      nedges += dout - 1;  // each link edge counted once, at its source
+      if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
+        ++din;
+        ++dsrc;
+        ++nedges;
+      }
+      if (e == L && __ldg(cd.cin_link + k) >= 0) {
+        ++dout;
+        ++dsink;
+        ++nedges;
+      }
+    }
+    g.cur[2 + 2 * k] = (int16_t)din;
+    g.cur[3 + 2 * k] = (int16_t)dout;
+  }
+  nedges = __reduce_add_sync(FULL, nedges);
+  dsrc = __reduce_add_sync(FULL, dsrc);
+  dsink = __reduce_add_sync(FULL, dsink);
+  E = nedges;
+  if (2 * E > lay.A) return ST_OVERFLOW;
+  if (lane == 0) {
+    g.cur[0] = (int16_t)dsrc;
+    g.cur[1] = (int16_t)dsink;
+  }
+  __syncwarp();
+  int run = 0;
+  for (int x0 = 0; x0 < V; x0 += 32) {
+    const int x = x0 + lane;
+    const int d = x < V ? g.cur[x] : 0;
+    int incl = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (x < V) {
+      g.abeg[x] = (int16_t)(run + incl - d);
+      fill[x] = 0;
+    }
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) g.abeg[V] = (int16_t)run;
+  __syncwarp();
+  // arcs: each lane places its node's compute pair and every edge it
+  // sources; the paired reverse arc takes the next free slot at its head.
+  for (int k = lane; k < N; k += 32) {
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    const int vi = 2 + 2 * k, vo = vi + 1;
+    const int ai = g.abeg[vi] + atomicAdd(&fill[vi], 1);
+    const int ao = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+    g.to[ai] = (int16_t)vo;
+    g.rv[ai] = (int16_t)ao;
+    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
+    g.to[ao] = (int16_t)vi;
+    g.rv[ao] = (int16_t)ai;
+    g.cap[ao] = 0.0;
+    for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
+      const int2 jl = __ldg(&cd.out_list[p]);
+      const int sj = g.ps[jl.x], ej = g.pe[jl.x];
+      if (!(ej > sj && edge_ok(e, sj, ej, partial))) continue;
+      const int vj = 2 + 2 * jl.x;
+      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+      const int ra = g.abeg[vj] + atomicAdd(&fill[vj], 1);
+      g.to[fa] = (int16_t)vj;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + jl.y);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    const int lc = __ldg(cd.cout_link + k);
+    if (s == 0 && lc >= 0) {
+      const int fa = g.abeg[0] + atomicAdd(&fill[0], 1);
+      const int ra = g.abeg[vi] + atomicAdd(&fill[vi], 1);
+      g.to[fa] = (int16_t)vi;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lc);
+      g.to[ra] = 0;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    const int lk = __ldg(cd.cin_link + k);
+    if (e == L && lk >= 0) {
+      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+      const int ra = g.abeg[1] + atomicAdd(&fill[1], 1);
+      g.to[fa] = 1;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lk);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+  }
+  __syncwarp();
+  return 0;
+}
+
+// Edmonds-Karp with a batched BFS: each step takes as many queued vertices as
+// have <= 32 arcs between them and gives every lane one arc.  Lanes are in
+// queue order, and a vertex reached twice in one step keeps its lowest lane,
+// so the BFS tree — hence every augmenting path — is exactly that of the
+// one-vertex-at-a-time BFS.
+__device__ double solve_ek_batched(const Gs& g, const int n, const int s, const int t, const int lane) {
+  double value = 0.0;
+  const unsigned lt = lanemask_lt();
+  const unsigned le = lt | (1u << lane);
+  for (;;) {
+    for (int x = lane; x < n; x += 32) g.h[x] = -1;
+    __syncwarp();
+    if (lane == 0) {
+      g.h[s] = -2;
+      g.q[0] = (int16_t)s;
+      g.ex[s] = 1.0e300;
+    }
+    __syncwarp();
+    int qh = 0, qt = 1;
+    bool found = false;
+    while (qh < qt) {
+      const int avail = min(32, qt - qh);
+      int vi = 0, bi = 0, di = 0;
+      if (lane < avail) {
+        vi = g.q[qh + lane];
+        bi = g.abeg[vi];
+        di = g.abeg[vi + 1] - bi;
+      }
+      int incl = di;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int d0 = __shfl_sync(FULL, di, 0);
+      if (d0 > 32) {
+        // a wide vertex: scan it alone, 32 arcs at a time
+        const int u = vi, b = bi;
+        const double bu = g.ex[__shfl_sync(FULL, u, 0)];
+        const int ub = __shfl_sync(FULL, b, 0);
+        for (int a0 = ub; a0 < ub + d0; a0 += 32) {
+          const int a = a0 + lane;
+          bool ok = false;
+          int v = 0;
+          double c = 0.0;
+          if (a < ub + d0) {
+            c = g.cap[a];
+            if (c > FLOW_EPS) {
+              v = g.to[a];
+              ok = g.h[v] == -1;
+            }
+          }
+          const unsigned m = __ballot_sync(FULL, ok);
+          if (ok) {
+            g.h[v] = (int16_t)a;
+            g.q[qt + __popc(m & lt)] = (int16_t)v;
+            g.ex[v] = ref_min(bu, c);
+          }
+          qt += __popc(m);
+          if (__any_sync(FULL, ok && v == t)) {
+            found = true;
+            break;
+          }
+        }
+        qh += 1;
+      } else {
+        const unsigned fit = __ballot_sync(FULL, lane < avail && incl <= 32);
+        const int k = __popc(fit);  // >= 1: lane 0 fits (d0 <= 32)
+        const int start = incl - di;
+        const unsigned sm = __reduce_or_sync(FULL, (lane < k && di > 0) ? (1u << start) : 0u);
+        const int total = __shfl_sync(FULL, incl, k - 1);
+        const int slot = __popc(sm & le) - 1;
+        const int su = slot < 0 ? 0 : slot;
+        const int u_b = __shfl_sync(FULL, bi, su);
+        const int u_st = __shfl_sync(FULL, start, su);
+        const int u_v = __shfl_sync(FULL, vi, su);
+        bool ok = false;
+        int v = 0;
+        double c = 0.0;
+        if (lane < total) {
+          const int a = u_b + (lane - u_st);
+          c = g.cap[a];
+          if (c > FLOW_EPS) {
+            v = g.to[a];
+            ok = g.h[v] == -1;
+          }
+        }
+        const unsigned cand = __ballot_sync(FULL, ok);
+        if (ok) {
+          const unsigned peers = __match_any_sync(cand, v);
+          ok = (peers & lt) == 0u;
+        }
+        const unsigned m = __ballot_sync(FULL, ok);
+        if (ok) {
+          const int a = u_b + (lane - u_st);
+          g.h[v] = (int16_t)a;
+          g.q[qt + __popc(m & lt)] = (int16_t)v;
+          g.ex[v] = ref_min(g.ex[u_v], c);
+        }
+        qt += __popc(m);
+        qh += k;
+        if (__any_sync(FULL, ok && v == t)) found = true;
+      }
+      __syncwarp();
+      if (found) break;
+    }
+    if (!found) break;
+    const double f = g.ex[t];
+    if (lane == 0) {
+      int x = t;
+      while (x != s) {
+        const int a = g.h[x];
+        const int r = g.rv[a];
+        g.cap[a] -= f;
+        g.cap[r] += f;
+        x = g.to[r];
+      }
+    }
+    __syncwarp();
+    value += f;
+  }
+  return value;
+}
+
 // Net flow into the sink in edge order (:222-227).  In built graphs the only
 // edges touching the sink are node->coordinator links, whose order in
 // g.edges equals the order of the sink's arcs.
@@ -664,7 +874,8 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     if ((int64_t)w >= total) break;
     const int64_t b = big ? ovf[w] : (int64_t)w;
     int V = 0, E = 0;
-    int st = build_graph(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E);
+    int st = MODE == HELIO_MODE_SCORE ? build_graph_score(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
+                                      : build_graph(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E);
     if (st == ST_OVERFLOW) {
       if (!big) {
         if (lane == 0) ovf[atomicAdd(ovf_count, 1u)] = b;
@@ -674,7 +885,7 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     }
     double value = 0.0;
     if (st == 0 && MODE == HELIO_MODE_SCORE) {
-      value = solve_ek(g, V, 0, 1, lane);
+      value = solve_ek_batched(g, V, 0, 1, lane);
     } else if (st == 0) {
       solve_fifo(g, V, 0, 1, lane);
       value = built_value(cd, g, lane);
@@ -1150,6 +1361,35 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
     if (b == -1 && a >= 0) cin[a] = lcap[i];
   }
   const int Mv = (int)pack.size();
+  // SCORE builder tables: per-node out-/in-link lists (other endpoint, link
+  // index) over node<->node links, and each node's coordinator links.
+  std::vector<int32_t> cout(N, -1), cinl(N, -1), obeg(N + 1, 0), ibeg(N + 1, 0);
+  for (int i = 0; i < Mv; ++i) {
+    int a = (int)(pack[i] & 0xffffu) - 1, b = (int)(pack[i] >> 16) - 1;
+    if (a < 0) cout[b] = i;
+    else if (b < 0) cinl[a] = i;
+    else {
+      obeg[a + 1]++;
+      ibeg[b + 1]++;
+    }
+  }
+  for (int k = 0; k < N; ++k) {
+    obeg[k + 1] += obeg[k];
+    ibeg[k + 1] += ibeg[k];
+  }
+  std::vector<int32_t> olist(2 * std::max(obeg[N], 1)), ilist(2 * std::max(ibeg[N], 1));
+  {
+    std::vector<int32_t> fo(N, 0), fi(N, 0);
+    for (int i = 0; i < Mv; ++i) {
+      int a = (int)(pack[i] & 0xffffu) - 1, b = (int)(pack[i] >> 16) - 1;
+      if (a < 0 || b < 0) continue;
+      int po = obeg[a] + fo[a]++, pi = ibeg[b] + fi[b]++;
+      olist[2 * po] = b;
+      olist[2 * po + 1] = i;
+      ilist[2 * pi] = a;
+      ilist[2 * pi + 1] = i;
+    }
+  }
   // one device allocation for all constants
   auto al = [](size_t x) { return (x + 15) / 16 * 16; };
   size_t o_kmax = 0;
@@ -1160,7 +1400,13 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   size_t o_pack = o_captab + al(8 * cap_tab.size());
   size_t o_lcap = o_pack + al(4 * std::max(Mv, 1));
   size_t o_cin = o_lcap + al(8 * std::max(Mv, 1));
-  size_t total = o_cin + al(8 * N);
+  size_t o_cout = o_cin + al(8 * N);
+  size_t o_cinl = o_cout + al(4 * N);
+  size_t o_obeg = o_cinl + al(4 * N);
+  size_t o_ibeg = o_obeg + al(4 * (N + 1));
+  size_t o_olist = o_ibeg + al(4 * (N + 1));
+  size_t o_ilist = o_olist + al(4 * olist.size());
+  size_t total = o_ilist + al(4 * ilist.size());
   std::vector<char> hbuf(total, 0);
   std::memcpy(hbuf.data() + o_kmax, kmax16.data(), 2 * N);
   std::memcpy(hbuf.data() + o_lexrank, d->lex_rank, 4 * N);
@@ -1172,6 +1418,12 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
     std::memcpy(hbuf.data() + o_lcap, lcap.data(), 8 * Mv);
   }
   std::memcpy(hbuf.data() + o_cin, cin.data(), 8 * N);
+  std::memcpy(hbuf.data() + o_cout, cout.data(), 4 * N);
+  std::memcpy(hbuf.data() + o_cinl, cinl.data(), 4 * N);
+  std::memcpy(hbuf.data() + o_obeg, obeg.data(), 4 * (N + 1));
+  std::memcpy(hbuf.data() + o_ibeg, ibeg.data(), 4 * (N + 1));
+  std::memcpy(hbuf.data() + o_olist, olist.data(), 4 * olist.size());
+  std::memcpy(hbuf.data() + o_ilist, ilist.data(), 4 * ilist.size());
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->d_cluster) cudaFree(ctx->d_cluster);
   if (ctx->d_kmax32) cudaFree(ctx->d_kmax32);
@@ -1193,6 +1445,12 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   ctx->cd.link_pack = reinterpret_cast<const uint32_t*>(base + o_pack);
   ctx->cd.link_cap = reinterpret_cast<const double*>(base + o_lcap);
   ctx->cd.cin_cap = reinterpret_cast<const double*>(base + o_cin);
+  ctx->cd.cout_link = reinterpret_cast<const int32_t*>(base + o_cout);
+  ctx->cd.cin_link = reinterpret_cast<const int32_t*>(base + o_cinl);
+  ctx->cd.out_beg = reinterpret_cast<const int32_t*>(base + o_obeg);
+  ctx->cd.in_beg = reinterpret_cast<const int32_t*>(base + o_ibeg);
+  ctx->cd.out_list = reinterpret_cast<const int2*>(base + o_olist);
+  ctx->cd.in_list = reinterpret_cast<const int2*>(base + o_ilist);
   ctx->N = N;
   ctx->L = L;
   ctx->Mv = Mv;
