@@ -287,12 +287,9 @@ def main():
     rel = ((vals - other_vals).abs() / other_vals.abs().clamp(min=1.0)).max().item()
 
     # winner (deterministic: max value, then min global index)
-    if world > 1:
-        g = gathered.view(world, 2).cpu().numpy()
-        recs = [(float(g[r, 0:1].view(np.float64)[0]), int(g[r, 1])) for r in range(world)]
-    else:
-        recs = [(float(best.item()), int(bidx.item()))]
-    win = max([r for r in recs if r[1] >= 0], key=lambda r: (r[0], -r[1]), default=(0.0, -1))
+    from paper_2406_01566_b200.dist import reduce_best, unpack_records
+    recs = unpack_records(gathered) if world > 1 else [(float(best.item()), int(bidx.item()))]
+    win = reduce_best(recs)
     st_host = st.cpu().numpy()
     nonzero = float((vals.cpu().numpy() > 0).mean())
 

@@ -1,0 +1,79 @@
+"""CPU, world_size 2 (gloo): the multi-rank sharding + argmax reduction that
+bench.py runs over NCCL on GPUs."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2406_01566_b200.dist import gather_best, pack_record, reduce_best, shard_range
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, values, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    per = len(values) // world
+    lo, hi = shard_range(per, rank)
+    local = values[lo:hi]
+    ok = local > 0
+    if ok.any():
+        i = int(np.argmax(np.where(ok, local, -1.0)))
+        rec = pack_record(float(local[i]), lo + i)
+    else:
+        rec = pack_record(0.0, -1)
+    q.put((rank, gather_best(rec, world)))
+    dist.destroy_process_group()
+
+
+def _run(values, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, values, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return dict(res)
+
+
+def _first_max(values):
+    ok = values > 0
+    if not ok.any():
+        return 0.0, -1
+    i = int(np.argmax(np.where(ok, values, -1.0)))
+    return float(values[i]), i
+
+
+@pytest.mark.parametrize("case", ["random", "tie_across_ranks", "all_zero"])
+def test_two_rank_argmax_equals_global_first_max(case):
+    rng = np.random.default_rng(5)
+    v = rng.random(64) * 100
+    if case == "tie_across_ranks":
+        v[:] = 1.0
+        v[40] = 7.0
+        v[10] = 7.0  # rank 0 and rank 1 tie: min global index (10) must win
+    if case == "all_zero":
+        v[:] = 0.0
+    res = _run(v)
+    want = _first_max(v)
+    assert res[0] == want and res[1] == want
+
+
+def test_reduce_best_rules():
+    assert reduce_best([(3.0, 5), (3.0, 2), (1.0, 0)]) == (3.0, 2)
+    assert reduce_best([(0.0, -1), (0.0, -1)]) == (0.0, -1)
+    assert shard_range(1000, 3) == (3000, 4000)
