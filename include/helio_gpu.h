@@ -167,6 +167,16 @@ int helio_gpu_generate(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t
 void helio_generate_host(const int32_t* k, int32_t num_nodes, int32_t num_layers, uint64_t seed,
                          int64_t first, int64_t B, uint32_t p_uniform_ppm, int16_t* h_out);
 
+/* Exhaustive placement search (tests/oracles/enumerate.hpp:14-77) on the
+ * device: every combination of per-node choices {idle} + {[s, e): e - s <= k_i}
+ * that covers all L <= 32 layers is scored in PARITY mode in the reference's
+ * DFS order, and the first strict maximum over 0 wins (:59).  h_best_row is
+ * int16 [N][2] (all zero if nothing beats 0).  Fails with
+ * HELIO_ERR_TOO_LARGE when the leaf space exceeds max_leaves (> 0). */
+int helio_gpu_best_exhaustive(helio_gpu_ctx* ctx, int allow_partial, int64_t max_leaves,
+                              double* h_best_value, int16_t* h_best_row, int64_t* h_leaves_scored,
+                              int64_t* h_leaves_total);
+
 /* IWRR routing of R requests over a plan (scheduler.cpp:58-190) in the AC8
  * admit/complete order: request r is admitted with in_len[r] and completed at
  * once with out_len[r].  Plan edges in plan order; placement is the plan's

@@ -31,6 +31,8 @@
 #include "helio/rng.hpp"
 #include "helio/scheduler.hpp"
 #include "helio/workload.hpp"
+#include "oracles/enumerate.hpp"
+#include "oracles/random_cluster.hpp"
 
 using namespace helio;
 
@@ -323,6 +325,41 @@ int refh_trace(int count, double rate, int online, uint64_t seed, double mean_in
     out_len[i] = reqs[i].output_len;
   }
   return count;
+}
+
+// --- placement search oracles (proj/tests/oracles) ---------------------------
+
+// random_cluster (random_cluster.hpp:22-86) with AC2's parameters
+// (acceptance_main.cpp:306-310): returns the reference's serialize_cluster
+// JSON into buf; -needed size if buf is too small.
+int refh_random_cluster_json(uint64_t seed, int max_nodes, int min_layers, int max_layers, char* buf,
+                             int buflen) {
+  testutil::RandomClusterParams params;
+  params.max_nodes = max_nodes;
+  params.min_layers = min_layers;
+  params.max_layers = max_layers;
+  Rng rng(seed);
+  ClusterSpec c = testutil::random_cluster(rng, params);
+  std::string s = serialize_cluster(c);
+  if (static_cast<int>(s.size()) + 1 > buflen) return -static_cast<int>(s.size() + 1);
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
+}
+
+// best_placement_exhaustive (enumerate.hpp:14-77): best value, the winning
+// placement as an int16 [N][2] row, and the number of leaves scored.
+double refh_best_exhaustive(void* cp, int allow_partial, int16_t* best_row, int64_t* scored) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  Placement best;
+  long n = 0;
+  double v = testutil::best_placement_exhaustive(c, allow_partial != 0, &best, &n);
+  for (size_t k = 0; k < c.nodes.size(); ++k) {
+    auto it = best.find(c.nodes[k].id);
+    best_row[2 * k] = it == best.end() ? 0 : static_cast<int16_t>(it->second.start);
+    best_row[2 * k + 1] = it == best.end() ? 0 : static_cast<int16_t>(it->second.end);
+  }
+  *scored = n;
+  return v;
 }
 
 }  // extern "C"

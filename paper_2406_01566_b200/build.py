@@ -25,7 +25,7 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-f
               "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-sign-compare"]
 
-CU_SOURCES = ["helio_gpu.cu", "route.cu"]
+CU_SOURCES = ["helio_gpu.cu", "route.cu", "search.cu"]
 HEADERS = ["engine.h", "gen.h", "shim.hpp", "helio/cluster.hpp", "helio/errors.hpp",
            "helio/flow_graph.hpp", "helio/placement.hpp", "helio/scheduler.hpp"]
 

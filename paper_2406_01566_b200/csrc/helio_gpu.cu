@@ -1169,6 +1169,17 @@ int launch_score(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, in
   return HELIO_OK;
 }
 
+}  // namespace
+
+// PARITY scoring of device rows on `st` (used by search.cu).
+int helio_engine_score_parity(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int partial, double* d_val,
+                              int32_t* d_st, cudaStream_t st) {
+  FlowOut fo{nullptr, nullptr, nullptr, 0};
+  return launch_score(ctx, 0, d_pl, B, partial, d_val, d_st, st, fo, false, HELIO_MODE_PARITY);
+}
+
+namespace {
+
 int ensure_stage(helio_gpu_ctx* ctx, int64_t chunk) {
   if (ctx->stage_cap >= chunk) return HELIO_OK;
   for (int i = 0; i < 2; ++i) {

@@ -722,5 +722,23 @@ PYBIND11_MODULE(_helio, m) {
            "float64 [K,E,2] {cap,flow})")
       .def("route", &engine_route, py::arg("placement_row"), py::arg("plan_edges"), py::arg("plan_flows"),
            py::arg("input_lens"), py::arg("output_lens"), py::arg("max_hops") = 0)
+      .def(
+          "best_exhaustive",
+          [](PyEngine& e, bool allow_partial, int64_t max_leaves) {
+            const int N = e.eng->num_nodes();
+            py::array_t<int16_t> row({(py::ssize_t)N, (py::ssize_t)2});
+            double best = 0;
+            int64_t scored = 0, total = 0;
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = helio_gpu_best_exhaustive(e.eng->ctx(), allow_partial ? 1 : 0, max_leaves, &best,
+                                             row.mutable_data(), &scored, &total);
+            }
+            e.eng->check(rc, "helio_gpu_best_exhaustive");
+            return py::make_tuple(best, row, scored, total);
+          },
+          py::arg("allow_partial") = true, py::arg("max_leaves") = 2000000000LL,
+          "Exhaustive search in the reference's enumeration order: (best value, row, leaves scored, leaf space).")
       .def("sync", [](PyEngine& e) { e.eng->check(helio_gpu_sync(e.eng->ctx()), "helio_gpu_sync"); });
 }

@@ -1,0 +1,202 @@
+// search.cu — exhaustive placement search on the device.
+//
+// Reference: best_placement_exhaustive (tests/oracles/enumerate.hpp:14-77).
+// Node i's choices are {idle} followed by every [s, e) with e - s <= k_i in
+// (s, e) order (:21-28); the DFS visits nodes in declaration order, so leaf
+// order is mixed-radix order with node 0 as the most significant digit.  The
+// DFS prunes subtrees that can no longer cover all L layers (:37-51), i.e. it
+// scores exactly the covering leaves, in order, and keeps the first strict
+// maximum over best = 0 (:59).  Here: leaves are enumerated by index in
+// chunks, non-covering ones are dropped with an order-preserving select, the
+// survivors are materialised as placement rows and scored by the PARITY
+// kernel (bit-identical values), and K4's first-max argmax combines chunks.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "engine.h"
+
+using namespace helio_engine;
+
+namespace {
+
+struct Choices {
+  int N;
+  const int32_t* off;       // [N+1] into s/e/mask
+  const int64_t* radix;     // [N] product of choice counts of nodes after i
+  const int16_t* cs;        // start
+  const int16_t* ce;        // end
+  const uint64_t* cmask;    // coverage bits of the choice
+};
+
+__global__ void enum_flag(Choices ch, int64_t base, int64_t n, uint64_t full, uint8_t* flag) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t idx = base + t;
+    uint64_t cov = 0;
+    for (int i = 0; i < ch.N; ++i) {
+      const int64_t r = ch.radix[i];
+      const int64_t d = idx / r;
+      idx -= d * r;
+      cov |= ch.cmask[ch.off[i] + (int)d];
+    }
+    flag[t] = cov == full ? 1 : 0;
+  }
+}
+
+__global__ void enum_rows(Choices ch, int64_t base, const int64_t* sel, int64_t m, int16_t* rows) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t idx = base + sel[t];
+    for (int i = 0; i < ch.N; ++i) {
+      const int64_t r = ch.radix[i];
+      const int64_t d = idx / r;
+      idx -= d * r;
+      const int c = ch.off[i] + (int)d;
+      rows[(t * ch.N + i) * 2] = ch.cs[c];
+      rows[(t * ch.N + i) * 2 + 1] = ch.ce[c];
+    }
+  }
+}
+
+}  // namespace
+
+// defined in helio_gpu.cu
+int helio_engine_score_parity(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int partial, double* d_val,
+                              int32_t* d_st, cudaStream_t st);
+
+extern "C" int helio_gpu_best_exhaustive(helio_gpu_ctx* ctx, int allow_partial, int64_t max_leaves,
+                                         double* h_best_value, int16_t* h_best_row, int64_t* h_scored,
+                                         int64_t* h_total) {
+  if (!ctx) return HELIO_ERR_INVALID;
+  if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
+  if (!h_best_value || !h_best_row) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  const int N = ctx->N, L = ctx->L;
+  if (L > 32) return fail(ctx, HELIO_ERR_INVALID, "exhaustive search needs num_layers <= 32 (enumerate.hpp:30-35)");
+  CK(cudaSetDevice(ctx->device));
+  // choices per node, in the reference's order
+  std::vector<int32_t> off(N + 1, 0);
+  std::vector<int16_t> cs, ce;
+  std::vector<uint64_t> cm;
+  for (int i = 0; i < N; ++i) {
+    off[i] = (int32_t)cs.size();
+    cs.push_back(0);
+    ce.push_back(0);
+    cm.push_back(0);
+    const int k = ctx->h_kmax[i];
+    for (int s = 0; s < L; ++s)
+      for (int e = s + 1; e <= L && e - s <= k; ++e) {
+        cs.push_back((int16_t)s);
+        ce.push_back((int16_t)e);
+        uint64_t m = 0;
+        for (int l = s; l < e; ++l) m |= 1ull << l;
+        cm.push_back(m);
+      }
+  }
+  off[N] = (int32_t)cs.size();
+  std::vector<int64_t> radix(N, 1);
+  double total_d = 1.0;
+  int64_t total = 1;
+  for (int i = N - 1; i >= 0; --i) {
+    radix[i] = total;
+    const int64_t c = off[i + 1] - off[i];
+    total_d *= (double)c;
+    if (total_d > 9.0e18) return fail(ctx, HELIO_ERR_TOO_LARGE, "placement space exceeds 2^63 leaves");
+    total *= c;
+  }
+  if (max_leaves > 0 && total > max_leaves)
+    return fail(ctx, HELIO_ERR_TOO_LARGE, "placement space (" + std::to_string(total) + " leaves) exceeds max_leaves");
+  const uint64_t full = L >= 64 ? ~0ull : ((1ull << L) - 1);
+  cudaStream_t st = ctx->stream;
+  const int64_t chunk = std::min<int64_t>(total, 1 << 22);
+  int rc = HELIO_OK;
+  int32_t* d_off = nullptr;
+  int64_t *d_radix = nullptr, *d_sel = nullptr, *d_nsel = nullptr, *d_bidx = nullptr;
+  int16_t *d_cs = nullptr, *d_ce = nullptr, *d_rows = nullptr;
+  uint64_t* d_cm = nullptr;
+  uint8_t* d_flag = nullptr;
+  double *d_val = nullptr, *d_best = nullptr;
+  int32_t* d_st = nullptr;
+  void* d_tmp = nullptr;
+  size_t tmp = 0;
+  auto A = [&](void** p, size_t bytes) {
+    if (!rc && cudaMalloc(p, std::max<size_t>(bytes, 8)) != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "search alloc");
+  };
+  A((void**)&d_off, 4 * (N + 1));
+  A((void**)&d_radix, 8 * N);
+  A((void**)&d_cs, 2 * cs.size());
+  A((void**)&d_ce, 2 * ce.size());
+  A((void**)&d_cm, 8 * cm.size());
+  A((void**)&d_flag, chunk);
+  A((void**)&d_sel, 8 * chunk);
+  A((void**)&d_nsel, 8);
+  A((void**)&d_rows, 4 * (size_t)N * chunk);
+  A((void**)&d_val, 8 * chunk);
+  A((void**)&d_st, 4 * chunk);
+  A((void**)&d_best, 8);
+  A((void**)&d_bidx, 8);
+  if (!rc) {
+    cub::DeviceSelect::Flagged(nullptr, tmp, cub::CountingInputIterator<int64_t>(0), d_flag, d_sel, d_nsel,
+                               (int)chunk, st);
+    A(&d_tmp, tmp);
+  }
+  if (!rc) {
+    cudaMemcpyAsync(d_off, off.data(), 4 * (N + 1), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_radix, radix.data(), 8 * N, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_cs, cs.data(), 2 * cs.size(), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_ce, ce.data(), 2 * ce.size(), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_cm, cm.data(), 8 * cm.size(), cudaMemcpyHostToDevice, st);
+  }
+  Choices ch{N, d_off, d_radix, d_cs, d_ce, d_cm};
+  double best = 0.0;
+  int64_t best_leaf = -1, scored = 0;
+  std::vector<int16_t> best_row(2 * N, 0);
+  for (int64_t base = 0; !rc && base < total; base += chunk) {
+    const int64_t n = std::min(chunk, total - base);
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 16 * ctx->sm_count);
+    enum_flag<<<grid, 256, 0, st>>>(ch, base, n, full, d_flag);
+    cub::DeviceSelect::Flagged(d_tmp, tmp, cub::CountingInputIterator<int64_t>(0), d_flag, d_sel, d_nsel, (int)n, st);
+    ctx->launches += 2;
+    int64_t m = 0;
+    if (cudaMemcpyAsync(&m, d_nsel, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      rc = fail(ctx, HELIO_ERR_CUDA, std::string("search select: ") + cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    if (m == 0) continue;
+    const int g2 = (int)std::min<int64_t>((m + 255) / 256, 16 * ctx->sm_count);
+    enum_rows<<<g2, 256, 0, st>>>(ch, base, d_sel, m, d_rows);
+    ctx->launches++;
+    rc = helio_engine_score_parity(ctx, d_rows, m, allow_partial ? 1 : 0, d_val, d_st, st);
+    if (rc) break;
+    rc = helio_gpu_argmax(ctx, d_val, d_st, m, 0, d_best, d_bidx, st);
+    if (rc) break;
+    double cb = 0;
+    int64_t ci = -1;
+    if (cudaMemcpyAsync(&cb, d_best, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(&ci, d_bidx, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      rc = fail(ctx, HELIO_ERR_CUDA, "search argmax readback");
+      break;
+    }
+    scored += m;
+    if (ci >= 0 && cb > best) {  // strict: earlier chunks win ties (enumerate.hpp:59)
+      best = cb;
+      if (cudaMemcpyAsync(best_row.data(), d_rows + ci * 2 * N, 4 * N, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+          cudaStreamSynchronize(st) != cudaSuccess) {
+        rc = fail(ctx, HELIO_ERR_CUDA, "search row readback");
+        break;
+      }
+      best_leaf = ci;
+    }
+  }
+  (void)best_leaf;
+  cudaFree(d_off); cudaFree(d_radix); cudaFree(d_cs); cudaFree(d_ce); cudaFree(d_cm); cudaFree(d_flag);
+  cudaFree(d_sel); cudaFree(d_nsel); cudaFree(d_rows); cudaFree(d_val); cudaFree(d_st); cudaFree(d_best);
+  cudaFree(d_bidx); cudaFree(d_tmp);
+  if (rc) return rc;
+  *h_best_value = best;
+  std::copy(best_row.begin(), best_row.end(), h_best_row);
+  if (h_scored) *h_scored = scored;
+  if (h_total) *h_total = total;
+  return HELIO_OK;
+}

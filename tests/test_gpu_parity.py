@@ -275,3 +275,19 @@ def test_score_mode_full_size_matches_parity_mode():
     torch.cuda.synchronize()
     # integer capacities: the two algorithms agree bit for bit at full size
     assert torch.equal(vp.view(torch.int64), vs.view(torch.int64))
+
+
+# --- exhaustive placement search (enumerate.hpp:14-77; AC2) ------------------
+
+def test_exhaustive_search_matches_reference():
+    z = golden("search_exhaustive.npz")
+    for i, key in enumerate(z["keys"]):
+        d = golden_cluster(str(key))
+        c = h.Cluster.from_json(json.dumps(d))
+        e = h.Engine(c)
+        best, row, scored, total = e.best_exhaustive(bool(z["partial"][i]))
+        N = len(d["nodes"])
+        assert scored == z["scored"][i], key
+        assert bits([best])[0] == bits(z["values"][i : i + 1])[0], key
+        assert np.array_equal(row, z["rows"][i][:N]), key
+        assert total >= scored
