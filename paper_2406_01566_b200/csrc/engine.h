@@ -34,7 +34,7 @@ struct ClusterDev {
 // Shared-memory slot layout of one graph (byte offsets from the slot base).
 struct Layout {
   int V, A, N, M;  // vertex, arc, node, raw-edge capacities
-  int o_cap, o_ex, o_to, o_rv, o_abeg, o_h, o_cur, o_q, o_cnt, o_inq, o_ps, o_pe, o_vin, o_unode,
+  int o_vs, o_cap, o_ex, o_to, o_rv, o_abeg, o_h, o_cur, o_q, o_cnt, o_inq, o_ps, o_pe, o_vin, o_unode,
       o_efwd;
   int bytes;
 };
