@@ -29,6 +29,8 @@ struct ClusterDev {
   const int32_t* in_beg;      // [N+1] into in_list
   const int2* out_list;       // (dst node, link index) of node -> node links
   const int2* in_list;        // (src node, link index)
+  const unsigned long long* out_mask;  // [N] (N <= 64 only) node -> node link targets
+  const int32_t* pair_link;            // [N*N] (N <= 64 only) link index or -1
 };
 
 // Shared-memory slot layout of one graph (byte offsets from the slot base).

@@ -692,6 +692,159 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
   return 0;
 }
 
+// SCORE builder for N <= 64: node sets are 64-bit words.  cover[l] = nodes
+// whose interval contains layer l, start[l] = nodes starting at l.  Node i's
+// valid successors are (partial ? cover[e_i] : start[e_i]) & out_mask[i]
+// (flow_graph.cpp:121: s_j <= e_i < e_j, resp. e_i == s_j), so each node
+// visits only its ~2-3 actual edges instead of every link of the cluster.
+__device__ int build_graph_score_small(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
+                                       int partial, int lane, int& V, int& E) {
+  const int N = cd.N, L = cd.L;
+  unsigned long long* cover = reinterpret_cast<unsigned long long*>(g.cap);  // [L] then start[L]; scratch
+  unsigned long long* start = cover + L;
+  int bad = INT_MAX;
+  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = __ldg(row32 + k);
+    const int s = (int16_t)(w & 0xffff);
+    const int e = (int16_t)(w >> 16);
+    g.ps[k] = (int16_t)s;
+    g.pe[k] = (int16_t)e;
+    if (e > s) {
+      int code = 0;
+      if (s < 0 || e > L) code = 2;
+      else if (e - s > __ldg(cd.kmax + k)) code = 3;
+      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
+    }
+  }
+  bad = __reduce_min_sync(FULL, bad);
+  if (bad != INT_MAX) return bad & 3;
+  V = 2 + 2 * N;
+  if (V > lay.V || 2 * L > lay.A) return ST_OVERFLOW;  // cover/start scratch lives in cap[]
+  for (int l = lane; l < 2 * L; l += 32) cover[l] = 0ull;
+  __syncwarp();
+  for (int k = lane; k < N; k += 32) {
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    const unsigned long long bit = 1ull << k;
+    atomicOr(&start[s], bit);
+    for (int l = s; l < e; ++l) atomicOr(&cover[l], bit);
+  }
+  __syncwarp();
+  // successor sets (kept in registers; lanes own nodes lane, lane+32)
+  unsigned long long T[2] = {0ull, 0ull};
+  int* fill = reinterpret_cast<int*>(g.vs);
+  for (int x = lane; x < V; x += 32) fill[x] = 0;
+  __syncwarp();
+  int nedges = 0, dsrc = 0, dsink = 0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= N) continue;
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    unsigned long long t = 0ull;
+    if (e < L) t = (partial ? cover[e] : start[e]) & __ldg(cd.out_mask + k);
+    T[q] = t;
+    const int nt = __popcll(t);
+    nedges += 1 + nt;
+    int dout = 1 + nt, din = 1;
+    if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
+      ++din;
+      ++dsrc;
+      ++nedges;
+    }
+    if (e == L && __ldg(cd.cin_link + k) >= 0) {
+      ++dout;
+      ++dsink;
+      ++nedges;
+    }
+    atomicAdd(&fill[2 + 2 * k], din);
+    atomicAdd(&fill[3 + 2 * k], dout);
+    for (unsigned long long m = t; m; m &= m - 1) atomicAdd(&fill[2 + 2 * (__ffsll(m) - 1)], 1);  // in_j
+  }
+  nedges = __reduce_add_sync(FULL, nedges);
+  dsrc = __reduce_add_sync(FULL, dsrc);
+  dsink = __reduce_add_sync(FULL, dsink);
+  E = nedges;
+  if (2 * E > lay.A) return ST_OVERFLOW;
+  __syncwarp();
+  if (lane == 0) {
+    fill[0] = dsrc;
+    fill[1] = dsink;
+  }
+  __syncwarp();
+  int run = 0;
+  for (int x0 = 0; x0 < V; x0 += 32) {
+    const int x = x0 + lane;
+    const int d = x < V ? fill[x] : 0;
+    int incl = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (x < V) g.abeg[x] = (int16_t)(run + incl - d);
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) g.abeg[V] = (int16_t)run;
+  __syncwarp();
+  for (int x = lane; x < V; x += 32) fill[x] = 0;
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= N) continue;
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    const int vi = 2 + 2 * k, vo = vi + 1;
+    const int ai = g.abeg[vi] + atomicAdd(&fill[vi], 1);
+    const int ao = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+    g.to[ai] = (int16_t)vo;
+    g.rv[ai] = (int16_t)ao;
+    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
+    g.to[ao] = (int16_t)vi;
+    g.rv[ao] = (int16_t)ai;
+    g.cap[ao] = 0.0;
+    for (unsigned long long m = T[q]; m; m &= m - 1) {
+      const int j = __ffsll(m) - 1;
+      const int vj = 2 + 2 * j;
+      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+      const int ra = g.abeg[vj] + atomicAdd(&fill[vj], 1);
+      g.to[fa] = (int16_t)vj;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + __ldg(cd.pair_link + k * N + j));
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    const int lc = __ldg(cd.cout_link + k);
+    if (s == 0 && lc >= 0) {
+      const int fa = g.abeg[0] + atomicAdd(&fill[0], 1);
+      const int ra = g.abeg[vi] + atomicAdd(&fill[vi], 1);
+      g.to[fa] = (int16_t)vi;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lc);
+      g.to[ra] = 0;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    const int lk = __ldg(cd.cin_link + k);
+    if (e == L && lk >= 0) {
+      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+      const int ra = g.abeg[1] + atomicAdd(&fill[1], 1);
+      g.to[fa] = 1;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lk);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+  }
+  __syncwarp();
+  return 0;
+}
+
 // Edmonds-Karp with a batched BFS: each step takes as many queued vertices as
 // have <= 32 arcs between them and gives every lane one arc.  Lanes are in
 // queue order, and a vertex reached twice in one step keeps its lowest lane,
@@ -1047,7 +1200,9 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     if ((int64_t)w >= total) break;
     const int64_t b = big ? ovf[w] : (int64_t)w;
     int V = 0, E = 0;
-    int st = MODE == HELIO_MODE_SCORE ? build_graph_score(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
+    int st = MODE == HELIO_MODE_SCORE
+                 ? (cd.out_mask ? build_graph_score_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
+                                : build_graph_score(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E))
                                       : build_graph(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E);
     if (st == ST_OVERFLOW) {
       if (!big) {
@@ -1577,6 +1732,18 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
       ilist[2 * pi + 1] = i;
     }
   }
+  // N <= 64: node sets fit one 64-bit word; out-neighbour masks and a pair ->
+  // link-index matrix drive the cover-mask SCORE builder.
+  const bool small_n = N <= 64;
+  std::vector<unsigned long long> outmask(small_n ? N : 1, 0ull);
+  std::vector<int32_t> pairlink(small_n ? (size_t)N * N : 1, -1);
+  if (small_n)
+    for (int i = 0; i < Mv; ++i) {
+      int a = (int)(pack[i] & 0xffffu) - 1, b = (int)(pack[i] >> 16) - 1;
+      if (a < 0 || b < 0) continue;
+      outmask[a] |= 1ull << b;
+      pairlink[(size_t)a * N + b] = i;
+    }
   // one device allocation for all constants
   auto al = [](size_t x) { return (x + 15) / 16 * 16; };
   size_t o_kmax = 0;
@@ -1593,7 +1760,9 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   size_t o_ibeg = o_obeg + al(4 * (N + 1));
   size_t o_olist = o_ibeg + al(4 * (N + 1));
   size_t o_ilist = o_olist + al(4 * olist.size());
-  size_t total = o_ilist + al(4 * ilist.size());
+  size_t o_omask = o_ilist + al(4 * ilist.size());
+  size_t o_pair = o_omask + al(8 * outmask.size());
+  size_t total = o_pair + al(4 * pairlink.size());
   std::vector<char> hbuf(total, 0);
   std::memcpy(hbuf.data() + o_kmax, kmax16.data(), 2 * N);
   std::memcpy(hbuf.data() + o_lexrank, d->lex_rank, 4 * N);
@@ -1611,6 +1780,8 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   std::memcpy(hbuf.data() + o_ibeg, ibeg.data(), 4 * (N + 1));
   std::memcpy(hbuf.data() + o_olist, olist.data(), 4 * olist.size());
   std::memcpy(hbuf.data() + o_ilist, ilist.data(), 4 * ilist.size());
+  std::memcpy(hbuf.data() + o_omask, outmask.data(), 8 * outmask.size());
+  std::memcpy(hbuf.data() + o_pair, pairlink.data(), 4 * pairlink.size());
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->d_cluster) cudaFree(ctx->d_cluster);
   if (ctx->d_kmax32) cudaFree(ctx->d_kmax32);
@@ -1638,6 +1809,8 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   ctx->cd.in_beg = reinterpret_cast<const int32_t*>(base + o_ibeg);
   ctx->cd.out_list = reinterpret_cast<const int2*>(base + o_olist);
   ctx->cd.in_list = reinterpret_cast<const int2*>(base + o_ilist);
+  ctx->cd.out_mask = small_n ? reinterpret_cast<const unsigned long long*>(base + o_omask) : nullptr;
+  ctx->cd.pair_link = small_n ? reinterpret_cast<const int32_t*>(base + o_pair) : nullptr;
   ctx->N = N;
   ctx->L = L;
   ctx->Mv = Mv;
