@@ -132,6 +132,65 @@ def reference_rate(cluster_dict, kmax, L, budget_s, threads, first=0):
     return n / dt, n, dt
 
 
+def routing_leg(h, clusters, dev, sp, requests, with_reference):
+    """configs[3]: geo24 placement scoring + IWRR routing of 1M requests.
+    Score 100k candidates (SCORE), take the first-max plan, materialise its
+    flows (PARITY, plan_from_placement's filter), route `requests` requests of
+    generate_trace(seed 7) in the AC8 admit/complete order on the device, and
+    time the reference's sequential Scheduler on the same plan and requests."""
+    import numpy as np
+    import torch
+
+    d = clusters.CONFIGS["geo24"]("float")
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c, device=dev)
+    e.mode = "score"
+    B = 100_000
+    pl = torch.empty((B, e.num_nodes, 2), dtype=torch.int16, device=f"cuda:{dev}")
+    e.generate_device(SEED, 0, B, 0, pl.data_ptr(), sp)
+    v = torch.empty(B, dtype=torch.float64, device=pl.device)
+    st = torch.empty(B, dtype=torch.int32, device=pl.device)
+    bv = torch.empty(1, dtype=torch.float64, device=pl.device)
+    bi = torch.empty(1, dtype=torch.int64, device=pl.device)
+    e.score_device(pl.data_ptr(), B, v.data_ptr(), st.data_ptr(), True, sp)
+    e.argmax_device(v.data_ptr(), st.data_ptr(), B, 0, bv.data_ptr(), bi.data_ptr(), sp)
+    torch.cuda.synchronize(pl.device)
+    row = pl[int(bi.item())].cpu().numpy()
+    pe, pf, obj = e.plan_edges(row)
+    _, inl, outl = h.generate_trace(requests, 0.0, "offline", 7)
+    used = int((row[:, 1] > row[:, 0]).sum())
+    H = min(c.num_layers, used)
+    e.route(row, pe, pf, inl[:1000], outl[:1000], H, False)  # warm-up
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        nh, hn, _, _, den = e.route(row, pe, pf, inl, outl, H, False)
+        times.append(time.perf_counter() - t0)
+    rate = requests / min(times)
+    out = {"workload": f"geo24 (acceptance geo24(), 3 regions, 12 Mb/s WAN): best of {B} candidates "
+                       f"(value {float(bv.item()):.3f}), plan_from_placement, IWRR routes of "
+                       f"generate_trace({requests}, offline, seed 7) in AC8 order",
+           "requests": requests, "value": rate, "unit": "routes/s",
+           "timing": "host wall clock around helio_gpu_route_host (H2D lengths, kernels, D2H hop nodes)",
+           "hops_mean": float(nh[nh > 0].mean()), "deferred": int(den), "plan_edges": int(len(pf))}
+    if with_reference:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from _support import RefCluster  # test infrastructure: reference timing only
+            rc = RefCluster(d)
+            t0 = time.perf_counter()
+            rden, rnh, rhn, _, _ = rc.route(row, inl, outl, True, seed=7)
+            rt = time.perf_counter() - t0
+            m = np.arange(H)[None, :] < np.maximum(nh, 0)[:, None]
+            same = bool(rden == den and np.array_equal(rnh, nh) and np.array_equal(rhn[:, :H][m], hn[m]))
+            out["reference"] = {"value": requests / rt, "unit": "routes/s", "cores": 1,
+                                "kind": "reference", "sample": f"{requests} Scheduler::admit+complete, one thread"}
+            out["identical_to_reference"] = same
+        except Exception as ex:
+            out["reference"] = {"value": None, "sample": f"unavailable: {ex}"}
+    return out
+
+
 def run_reference(args):
     rank = env_int("RANK", 0)
     if rank != 0:
@@ -180,6 +239,8 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-routing", action="store_true")
+    ap.add_argument("--route-requests", type=int, default=1_000_000)
     ap.add_argument("--mode", default="score", choices=["score", "parity"],
                     help="headline scoring mode (the other mode is timed too and reported beside it)")
     args = ap.parse_args()
@@ -334,6 +395,14 @@ def main():
         e2e = {"value": e2e_rate, "unit": "evals/s", "h2d_bytes_per_step": B * world * 4 * N,
                "d2h_bytes_per_step": B * world * 12}
 
+    routing = None
+    if rank == 0 and not args.no_routing:
+        try:
+            routing = routing_leg(h, clusters, local, sp, args.route_requests,
+                                  with_reference=(world == 1 and not args.no_cpu_baseline))
+        except Exception as ex:  # reported, never fatal
+            routing = {"value": None, "error": str(ex)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -359,6 +428,7 @@ def main():
                        "nonzero_fraction": nonzero, "status_nonzero": int((st_host != 0).sum()),
                        "best": {"value": win[0], "index": win[1]}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "routing": routing,
             "clocks": clk.summary(),
         }
         print(json.dumps(out))

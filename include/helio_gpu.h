@@ -180,8 +180,9 @@ int helio_gpu_best_exhaustive(helio_gpu_ctx* ctx, int allow_partial, int64_t max
 /* IWRR routing of R requests over a plan (scheduler.cpp:58-190) in the AC8
  * admit/complete order: request r is admitted with in_len[r] and completed at
  * once with out_len[r].  Plan edges in plan order; placement is the plan's
- * int16 [N][2] row.  hop arrays are [R][max_hops]; h_num_hops[r] = -1 for a
- * deferred request.  *h_deferred receives the number of deferrals. */
+ * int16 [N][2] row.  hop arrays are [R][max_hops] (h_hop_start/h_hop_end may
+ * both be NULL to return node ids only); h_num_hops[r] = -1 for a deferred
+ * request.  *h_deferred receives the number of deferrals. */
 int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_placement,
                          const helio_plan_edge* h_plan_edges, int32_t num_plan_edges, int64_t R,
                          const int32_t* h_in_len, const int32_t* h_out_len, int32_t max_hops,

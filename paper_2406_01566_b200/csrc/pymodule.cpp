@@ -424,7 +424,7 @@ py::tuple engine_flows(PyEngine& pe, const py::array& pl, bool allow_partial, in
 
 py::tuple engine_route(PyEngine& pe, const py::array& placement_row, const py::array& plan_edges_i,
                        const py::array& plan_flows, const py::array& in_len, const py::array& out_len,
-                       int max_hops) {
+                       int max_hops, bool exec_ranges) {
   const int N = pe.eng->num_nodes();
   auto row = as_rows(placement_row, N);
   auto ei = py::array_t<int32_t, py::array::c_style | py::array::forcecast>::ensure(plan_edges_i);
@@ -445,14 +445,16 @@ py::tuple engine_route(PyEngine& pe, const py::array& placement_row, const py::a
   const int64_t R = iin.size();
   if (iout.size() != R) throw ValidationError("input/output length arrays differ in size");
   if (max_hops <= 0) max_hops = pe.eng->num_layers();
-  py::array_t<int32_t> nh(R), hn({(py::ssize_t)R, (py::ssize_t)max_hops}), hs({(py::ssize_t)R, (py::ssize_t)max_hops}),
-      he({(py::ssize_t)R, (py::ssize_t)max_hops});
+  const py::ssize_t HS = exec_ranges ? R : 0;
+  py::array_t<int32_t> nh(R), hn({(py::ssize_t)R, (py::ssize_t)max_hops}), hs({HS, (py::ssize_t)max_hops}),
+      he({HS, (py::ssize_t)max_hops});
   int64_t deferred = 0;
   int rc;
   {
     py::gil_scoped_release rel;
     rc = helio_gpu_route_host(pe.eng->ctx(), row.data(), pe_.data(), E, R, iin.data(), iout.data(), max_hops,
-                              nh.mutable_data(), hn.mutable_data(), hs.mutable_data(), he.mutable_data(), &deferred);
+                              nh.mutable_data(), hn.mutable_data(), exec_ranges ? hs.mutable_data() : nullptr,
+                              exec_ranges ? he.mutable_data() : nullptr, &deferred);
   }
   pe.eng->check(rc, "helio_gpu_route_host");
   return py::make_tuple(nh, hn, hs, he, deferred);
@@ -721,7 +723,41 @@ PYBIND11_MODULE(_helio, m) {
            "(values, status, num_vertices, num_edges, int32 [K,E,8] {u,v,kind,exec_start,exec_end,src,dst,0}, "
            "float64 [K,E,2] {cap,flow})")
       .def("route", &engine_route, py::arg("placement_row"), py::arg("plan_edges"), py::arg("plan_flows"),
-           py::arg("input_lens"), py::arg("output_lens"), py::arg("max_hops") = 0)
+           py::arg("input_lens"), py::arg("output_lens"), py::arg("max_hops") = 0, py::arg("exec_ranges") = true)
+      .def(
+          "plan_edges",
+          [](PyEngine& e, const py::array& placement_row, bool allow_partial) {
+            // plan_from_placement's edge filter (placement.cpp:440-455) over the
+            // device's PARITY flows: non-compute edges with flow > 1e-9, the
+            // coordinator as -1.  Returns (int32 [E,4] src,dst,exec_start,exec_end;
+            // float64 [E] flow; objective).
+            const int N = e.eng->num_nodes();
+            auto row = as_rows(placement_row, N);
+            if (row.shape(0) != 1) throw ValidationError("plan_edges takes one placement row");
+            const int max_e = N + e.eng->num_links() + 1;
+            std::vector<helio_edge> ed(max_e);
+            int32_t nv = 0, ne = 0, st = 0;
+            double val = 0;
+            e.eng->check(helio_gpu_flows_host(e.eng->ctx(), row.data(), 1, allow_partial ? 1 : 0, max_e, &nv, &ne,
+                                              ed.data(), &val, &st),
+                         "helio_gpu_flows_host");
+            if (st != HELIO_CAND_OK) throw ValidationError("placement rejected (status " + std::to_string(st) + ")");
+            std::vector<const helio_edge*> keep;
+            for (int i = 0; i < ne; ++i)
+              if (ed[i].kind != HELIO_EDGE_COMPUTE && ed[i].flow > 1e-9) keep.push_back(&ed[i]);
+            py::array_t<int32_t> ints({(py::ssize_t)keep.size(), (py::ssize_t)4});
+            py::array_t<double> fl((py::ssize_t)keep.size());
+            for (size_t i = 0; i < keep.size(); ++i) {
+              const helio_edge& x = *keep[i];
+              ints.mutable_at(i, 0) = x.kind == HELIO_EDGE_COORD_OUT ? -1 : x.src_node;
+              ints.mutable_at(i, 1) = x.kind == HELIO_EDGE_COORD_IN ? -1 : x.dst_node;
+              ints.mutable_at(i, 2) = x.exec_start;
+              ints.mutable_at(i, 3) = x.exec_end;
+              fl.mutable_at(i) = x.flow;
+            }
+            return py::make_tuple(ints, fl, val);
+          },
+          py::arg("placement_row"), py::arg("allow_partial") = true)
       .def(
           "best_exhaustive",
           [](PyEngine& e, bool allow_partial, int64_t max_leaves) {

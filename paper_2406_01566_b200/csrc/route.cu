@@ -104,8 +104,10 @@ __global__ void route_apply(int64_t R, int x, int L, int max_hops, const int32_t
     const int h = nh[r];
     if (h < max_hops) {
       hop_node[r * max_hops + h] = node_of[d];
-      hop_s[r * max_hops + h] = oes[e];
-      hop_e[r * max_hops + h] = oee[e];
+      if (hop_s) {
+        hop_s[r * max_hops + h] = oes[e];
+        hop_e[r * max_hops + h] = oee[e];
+      }
     }
     nh[r] = h + 1;
     cov[r] = (int16_t)oee[e];
@@ -178,8 +180,10 @@ __global__ void route_sequential(int64_t R, int nv, int L, int max_hops, double 
       ch_b[n] = bytes;
       if (n < max_hops) {
         hop_node[r * max_hops + n] = node_of[d];
-        hop_s[r * max_hops + n] = oes[e];
-        hop_e[r * max_hops + n] = oee[e];
+        if (hop_s) {
+          hop_s[r * max_hops + n] = oes[e];
+          hop_e[r * max_hops + n] = oee[e];
+        }
       }
       ++n;
       covered = oee[e];
@@ -214,7 +218,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   if (!ctx) return HELIO_ERR_INVALID;
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (!h_pl || (ne > 0 && !pe) || R < 0 || max_hops < 0 || (R > 0 && (!h_in || !h_out || !h_nh)) ||
-      (R > 0 && max_hops > 0 && (!h_hn || !h_hs || !h_he)))
+      (R > 0 && max_hops > 0 && (!h_hn || (!h_hs) != (!h_he))))
     return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   CK(cudaSetDevice(ctx->device));
   const int N = ctx->N, L = ctx->L;
@@ -319,8 +323,9 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   TRY(dalloc(ctx, &d_out, R));
   TRY(dalloc(ctx, &d_nh, R));
   TRY(dalloc(ctx, &d_hn, HR));
-  TRY(dalloc(ctx, &d_hs, HR));
-  TRY(dalloc(ctx, &d_he, HR));
+  const bool want_se = h_hs != nullptr;
+  TRY(dalloc(ctx, &d_hs, want_se ? HR : 1));
+  TRY(dalloc(ctx, &d_he, want_se ? HR : 1));
   TRY(dalloc(ctx, &d_err, 1));
   TRY(dalloc(ctx, &d_den, 1));
   if (!rc) {
@@ -372,7 +377,8 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
         route_flag<<<grid, 256, 0, st>>>(R, x, d_cur, d_flag);
         cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_flag, d_rank, (int)R, st);
         route_apply<<<grid, 256, 0, st>>>(R, x, L, max_hops, d_obeg, d_odst, d_oes, d_oee, d_node,
-                                           d_cycoff, d_cyclen, d_cyc, d_rank, d_cur, d_nh, d_cov, d_hn, d_hs, d_he,
+                                           d_cycoff, d_cyclen, d_cyc, d_rank, d_cur, d_nh, d_cov, d_hn,
+                                           want_se ? d_hs : nullptr, want_se ? d_he : nullptr,
                                            d_err);
         ctx->launches += 3;
       }
@@ -387,7 +393,8 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
     if (!rc) {
       route_sequential<<<1, 1, 0, st>>>(R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst, d_oes,
                                         d_oee, d_w, d_wmax, d_node, d_kvcap, d_kvest, d_pround, d_pidx,
-                                        d_in, d_out, d_nh, d_hn, d_hs, d_he, d_chv, d_chb, d_den, d_err);
+                                        d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr, want_se ? d_he : nullptr,
+                                        d_chv, d_chb, d_den, d_err);
       ctx->launches++;
       if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route_sequential failed");
     }
@@ -396,9 +403,9 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   if (!rc && R > 0) {
     bool ok = cudaMemcpyAsync(h_nh, d_nh, 4 * R, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
               cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, st) == cudaSuccess;
-    if (ok && max_hops > 0)
-      ok = cudaMemcpyAsync(h_hn, d_hn, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-           cudaMemcpyAsync(h_hs, d_hs, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+    if (ok && max_hops > 0) ok = cudaMemcpyAsync(h_hn, d_hn, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+    if (ok && max_hops > 0 && want_se)
+      ok = cudaMemcpyAsync(h_hs, d_hs, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
            cudaMemcpyAsync(h_he, d_he, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess;
     long long dd = 0;
     if (ok && !closed) ok = cudaMemcpyAsync(&dd, d_den, sizeof(long long), cudaMemcpyDeviceToHost, st) == cudaSuccess;
