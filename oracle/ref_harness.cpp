@@ -363,3 +363,6 @@ double refh_best_exhaustive(void* cp, int allow_partial, int16_t* best_row, int6
 }
 
 }  // extern "C"
+
+#define HARNESS_FN(x) refh_##x
+#include "milp_harness.inc"

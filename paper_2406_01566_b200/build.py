@@ -26,7 +26,8 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-f
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-sign-compare"]
 
 CU_SOURCES = ["helio_gpu.cu", "route.cu", "search.cu"]
-HEADERS = ["engine.h", "gen.h", "shim.hpp", "helio/cluster.hpp", "helio/errors.hpp",
+SHIM_SOURCES = ["shim_cluster.cpp", "shim_flow.cpp", "shim_plan.cpp", "shim_sched.cpp"]
+HEADERS = ["engine.h", "gen.h", "shim.hpp", "shim_engine.hpp", "helio/cluster.hpp", "helio/errors.hpp",
            "helio/flow_graph.hpp", "helio/placement.hpp", "helio/scheduler.hpp"]
 
 
@@ -74,9 +75,9 @@ def build(force: bool = False, verbose: bool = False) -> None:
 
     inc = ["-I" + CSRC, "-I" + os.path.join(ROOT, "include")]
     libshim = os.path.join(LIB, "libhelio.so")
-    shim_src = os.path.join(CSRC, "shim.cpp")
-    if force or _newer(libshim, [shim_src, libgpu] + hdrs):
-        _run(["g++", *CXX_FLAGS, *inc, "-shared", shim_src, "-o", libshim,
+    shim_srcs = [os.path.join(CSRC, f) for f in SHIM_SOURCES]
+    if force or _newer(libshim, shim_srcs + [libgpu] + hdrs):
+        _run(["g++", *CXX_FLAGS, *inc, "-shared", *shim_srcs, "-o", libshim,
               "-L" + LIB, "-lhelio_gpu", "-Wl,-rpath,$ORIGIN"], quiet=not verbose)
     pyext = os.path.join(PKG, "_helio" + ext_suffix())
     py_src = os.path.join(CSRC, "pymodule.cpp")

@@ -1,11 +1,8 @@
-// shim.cpp — the reference's C++ API (namespace helio) over the C ABI.
-//
-// Same names, argument meaning and error behaviour as the reference
-// (proj/include/helio/*.hpp); every graph is built and solved by the B200
-// engine (include/helio_gpu.h).  There is no host implementation of
-// build_flow_graph, max_flow, plan_from_placement or routing here: if the
-// engine cannot be created (no B200) every call throws InternalError.
-#include "shim.hpp"
+// shim_flow.cpp — engine cache, placement validation and the flow-graph API
+// (flow_graph.hpp:43-55) over the C ABI.  No host implementation of
+// build_flow_graph or max_flow exists: every graph is built and solved by the
+// B200 engine, and without one every call throws InternalError.
+#include "shim_engine.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -21,105 +18,6 @@
 #include "helio/errors.hpp"
 
 namespace helio {
-
-// --- cluster model (cluster.cpp:56-100, 237-300) ----------------------------
-
-int ClusterSpec::node_index(const std::string& id) const {
-  for (size_t i = 0; i < nodes.size(); ++i)
-    if (nodes[i].id == id) return static_cast<int>(i);
-  return -1;
-}
-
-int ClusterSpec::max_layers(const NodeSpec& n) const {
-  const double usable = n.vram_bytes * (1.0 - n.kv_reserve);
-  int k = static_cast<int>(std::floor(usable / model.bytes_per_layer()));
-  if (!n.throughput_table.empty()) k = std::min(k, n.throughput_table.rbegin()->first);
-  return std::min(k, model.num_layers);
-}
-
-double ClusterSpec::throughput(const NodeSpec& n, int j) const {
-  if (j < 1 || j > max_layers(n))
-    throw ValidationError("throughput request for node '" + n.id + "' outside profile range: j=" +
-                          std::to_string(j));
-  if (!n.throughput_table.empty()) return n.throughput_table.at(j);
-  return n.peak_layer_tokens / j;
-}
-
-double ClusterSpec::layer_token_rate(const NodeSpec& n, int j) const { return j * throughput(n, j); }
-
-static double incident_bw(const ClusterSpec& c, const NodeSpec& n) {
-  double best = 0;
-  for (const auto& l : c.links)
-    if (l.src == n.id || l.dst == n.id) best = std::max(best, l.bandwidth_bps);
-  return best;
-}
-
-double ClusterSpec::nic_in(const NodeSpec& n) const {
-  return n.nic_in_bps > 0 ? n.nic_in_bps : incident_bw(*this, n);
-}
-
-double ClusterSpec::nic_out(const NodeSpec& n) const {
-  return n.nic_out_bps > 0 ? n.nic_out_bps : incident_bw(*this, n);
-}
-
-double link_token_capacity(const LinkSpec& link, double payload_bytes) {
-  return link.bandwidth_bps / (8.0 * payload_bytes);
-}
-
-void validate_cluster(const ClusterSpec& c) {
-  auto fail = [](const std::string& msg) { throw ValidationError(msg); };
-  if (c.model.num_layers < 1) fail("model.num_layers must be >= 1");
-  if (c.model.param_bytes <= 0) fail("model.param_gb must be > 0");
-  if (c.model.token_bytes <= 0) fail("model.token_bytes must be > 0");
-  if (c.model.activation_bytes <= 0) fail("model.activation_bytes must be > 0");
-  if (c.model.kv_bytes_per_token_layer < 0) fail("model.kv_bytes_per_token_layer must be >= 0");
-  if (c.coordinator_id.empty()) fail("coordinator.id must be non-empty");
-  if (c.nodes.empty()) fail("cluster needs at least one compute node");
-  std::set<std::string> ids;
-  for (const auto& n : c.nodes) {
-    if (n.id.empty()) fail("node id must be non-empty");
-    if (n.id == c.coordinator_id) fail("node id '" + n.id + "' collides with the coordinator");
-    if (!ids.insert(n.id).second) fail("duplicate node id '" + n.id + "'");
-    if (n.vram_bytes <= 0) fail("node '" + n.id + "': vram_gb must be > 0");
-    if (n.kv_reserve < 0 || n.kv_reserve >= 1) fail("node '" + n.id + "': kv_reserve must be in [0, 1)");
-    const bool has_peak = n.peak_layer_tokens > 0;
-    const bool has_table = !n.throughput_table.empty();
-    if (has_peak == has_table)
-      fail("node '" + n.id + "': exactly one of peak_layer_tokens_per_s or throughput_table required");
-    if (has_table) {
-      int expect = 1;
-      double prev = 0;
-      for (const auto& [j, v] : n.throughput_table) {
-        if (j != expect) fail("node '" + n.id + "': throughput_table keys must be contiguous from 1");
-        if (v <= 0) fail("node '" + n.id + "': throughput_table values must be > 0");
-        if (expect > 1 && v >= prev) fail("node '" + n.id + "': throughput_table must be strictly decreasing");
-        prev = v;
-        ++expect;
-      }
-    }
-    if (n.nic_in_bps < 0 || n.nic_out_bps < 0) fail("node '" + n.id + "': NIC rates must be >= 0");
-  }
-  std::set<std::pair<std::string, std::string>> pairs;
-  bool coord_out = false, coord_in = false;
-  for (const auto& l : c.links) {
-    auto known = [&](const std::string& e) { return e == c.coordinator_id || c.node_index(e) >= 0; };
-    if (!known(l.src)) fail("link endpoint '" + l.src + "' is not a declared node");
-    if (!known(l.dst)) fail("link endpoint '" + l.dst + "' is not a declared node");
-    if (l.src == l.dst) fail("self-link on '" + l.src + "'");
-    if (!pairs.insert({l.src, l.dst}).second) fail("duplicate link " + l.src + " -> " + l.dst);
-    if (l.bandwidth_bps <= 0) fail("link " + l.src + " -> " + l.dst + ": bandwidth must be > 0");
-    if (l.latency_s < 0) fail("link " + l.src + " -> " + l.dst + ": latency must be >= 0");
-    if (l.src == c.coordinator_id) coord_out = true;
-    if (l.dst == c.coordinator_id) coord_in = true;
-  }
-  if (!coord_out) fail("coordinator has no outgoing link");
-  if (!coord_in) fail("coordinator has no incoming link");
-  long total = 0;
-  for (const auto& n : c.nodes) total += c.max_layers(n);
-  if (total < c.model.num_layers)
-    fail("insufficient VRAM: total layer capacity " + std::to_string(total) + " < model layers " +
-         std::to_string(c.model.num_layers));
-}
 
 // --- engine cache -----------------------------------------------------------
 
@@ -314,13 +212,7 @@ std::vector<int16_t> placement_row(const ClusterSpec& c, const Placement& p) {
   return row;
 }
 
-namespace {
-
-struct Solved {
-  int nv = 0;
-  double value = 0;
-  std::vector<helio_edge> edges;
-};
+namespace detail {
 
 Solved solve_one(const ClusterSpec& c, const Placement& p, bool allow_partial) {
   std::vector<int16_t> row = placement_row(c, p);
@@ -344,7 +236,11 @@ const std::string& node_name(const ClusterSpec& c, int idx) {
   return idx < 0 ? c.coordinator_id : c.nodes[idx].id;
 }
 
-}  // namespace
+}  // namespace detail
+
+using detail::node_name;
+using detail::solve_one;
+using detail::Solved;
 
 // --- flow graph API ---------------------------------------------------------
 
@@ -462,131 +358,6 @@ double compute_edge_capacity(const ClusterSpec& c, const NodeSpec& n, int j) {
   double out = 0;
   eng->check(helio_gpu_compute_edge_capacity(eng->ctx(), idx, j, &out), "helio_gpu_compute_edge_capacity");
   return out;
-}
-
-// --- plans (placement.cpp:440-469) -------------------------------------------
-
-PlacementPlan plan_from_placement(const ClusterSpec& c, const Placement& p, bool allow_partial,
-                                  const std::string& method) {
-  PlacementPlan plan;
-  plan.method = method;
-  plan.placement = p;
-  plan.allow_partial = allow_partial;
-  plan.status = MilpStatus::kFeasible;
-  Solved s = solve_one(c, p, allow_partial);
-  for (const helio_edge& e : s.edges) {
-    if (e.kind == HELIO_EDGE_COMPUTE || e.flow <= 1e-9) continue;
-    PlanEdge pe;
-    pe.src = node_name(c, e.kind == HELIO_EDGE_COORD_OUT ? -1 : e.src_node);
-    pe.dst = node_name(c, e.kind == HELIO_EDGE_COORD_IN ? -1 : e.dst_node);
-    pe.flow = e.flow;
-    pe.exec_start = e.exec_start;
-    pe.exec_end = e.exec_end;
-    plan.edges.push_back(pe);
-  }
-  plan.objective = s.value;
-  plan.best_bound = plan.objective;
-  return plan;
-}
-
-// --- IWRR (scheduler.cpp:28-190) ----------------------------------------------
-
-std::vector<long> iwrr_weights(const std::vector<double>& flows) {
-  std::vector<int64_t> w(flows.size());
-  if (!flows.empty()) {
-    auto eng = gpu::raw_engine();
-    eng->check(helio_gpu_iwrr_weights(eng->ctx(), flows.data(), static_cast<int32_t>(flows.size()), w.data()),
-               "helio_gpu_iwrr_weights");
-  }
-  return std::vector<long>(w.begin(), w.end());
-}
-
-IwrrPicker::IwrrPicker(std::vector<long> weights) : weights_(std::move(weights)) {}
-
-std::vector<int> IwrrPicker::next_batch(const std::vector<uint64_t>& masks) {
-  const int n = static_cast<int>(weights_.size());
-  const int words = (n + 63) / 64;
-  const int calls = words ? static_cast<int>(masks.size()) / words : static_cast<int>(masks.size());
-  std::vector<int32_t> out(calls, -1);
-  if (calls == 0) return {};
-  std::vector<int64_t> w(weights_.begin(), weights_.end());
-  int64_t round = round_, idx = idx_;
-  auto eng = gpu::raw_engine();
-  eng->check(helio_gpu_iwrr_picks(eng->ctx(), w.data(), n, &round, &idx, calls, masks.data(), out.data()),
-             "helio_gpu_iwrr_picks");
-  round_ = static_cast<long>(round);
-  idx_ = static_cast<long>(idx);
-  return std::vector<int>(out.begin(), out.end());
-}
-
-int IwrrPicker::next(const std::function<bool(int)>& eligible) {
-  const int n = static_cast<int>(weights_.size());
-  if (n == 0) return -1;
-  std::vector<uint64_t> mask((n + 63) / 64, 0);
-  for (int i = 0; i < n; ++i)
-    if (eligible(i)) mask[i >> 6] |= 1ull << (i & 63);
-  return next_batch(mask)[0];
-}
-
-Scheduler::Scheduler(const ClusterSpec& c, const PlacementPlan& plan) : cluster_(c), plan_(plan) {
-  if (plan.edges.empty()) throw ValidationError("plan has no flow edges to schedule on");
-  for (const auto& [id, iv] : plan.placement)
-    if (!iv.empty() && c.node_index(id) < 0) throw ValidationError("plan references unknown node '" + id + "'");
-  bool coord_out = false;
-  for (const PlanEdge& e : plan.edges) {
-    auto placed = [&](const std::string& id) {
-      if (id == c.coordinator_id) return true;
-      auto it = plan.placement.find(id);
-      return it != plan.placement.end() && !it->second.empty();
-    };
-    if (!placed(e.src) || !placed(e.dst))
-      throw ValidationError("plan edge " + e.src + "->" + e.dst + " references an unplaced node");
-    if (e.src == c.coordinator_id) coord_out = true;
-  }
-  if (!coord_out) throw ValidationError("plan has no edge leaving the coordinator");
-}
-
-std::vector<std::optional<std::vector<RouteHop>>> Scheduler::route(const std::vector<int>& in,
-                                                                    const std::vector<int>& out) {
-  if (in.size() != out.size()) throw ValidationError("input/output length arrays differ in size");
-  const ClusterSpec& c = cluster_;
-  auto eng = gpu::engine_for(c);
-  std::vector<int16_t> row(2 * c.nodes.size(), 0);
-  for (const auto& [id, iv] : plan_.placement) {
-    if (iv.empty()) continue;
-    int idx = c.node_index(id);
-    row[2 * idx] = static_cast<int16_t>(iv.start);
-    row[2 * idx + 1] = static_cast<int16_t>(iv.end);
-  }
-  std::vector<helio_plan_edge> pe;
-  for (const PlanEdge& e : plan_.edges) {
-    helio_plan_edge x{};
-    x.src_node = e.src == c.coordinator_id ? -1 : c.node_index(e.src);
-    x.dst_node = e.dst == c.coordinator_id ? -1 : c.node_index(e.dst);
-    x.exec_start = e.exec_start;
-    x.exec_end = e.exec_end;
-    x.flow = e.flow;
-    pe.push_back(x);
-  }
-  const int64_t R = static_cast<int64_t>(in.size());
-  const int max_hops = c.model.num_layers;
-  std::vector<int32_t> nh(R), hn((size_t)R * max_hops), hs((size_t)R * max_hops), he((size_t)R * max_hops);
-  int64_t deferred = 0;
-  int rc = helio_gpu_route_host(eng->ctx(), row.data(), pe.data(), static_cast<int32_t>(pe.size()), R, in.data(),
-                                out.data(), max_hops, nh.data(), hn.data(), hs.data(), he.data(), &deferred);
-  if (rc == HELIO_ERR_INVALID) throw InternalError(helio_gpu_last_error(eng->ctx()));
-  eng->check(rc, "helio_gpu_route_host");
-  std::vector<std::optional<std::vector<RouteHop>>> routes(R);
-  for (int64_t r = 0; r < R; ++r) {
-    if (nh[r] < 0) continue;
-    std::vector<RouteHop> hops;
-    for (int k = 0; k < nh[r]; ++k) {
-      size_t at = (size_t)r * max_hops + k;
-      hops.push_back({c.nodes[hn[at]].id, hs[at], he[at]});
-    }
-    routes[r] = std::move(hops);
-  }
-  return routes;
 }
 
 }  // namespace helio

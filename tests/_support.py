@@ -252,6 +252,9 @@ def ref():
         lib.refh_trace.argtypes = [C.c_int, C.c_double, C.c_int, C.c_uint64, C.c_double, C.c_double,
                                    C.c_int, C.c_int, _f64p, _i32p, _i32p]
         lib.refh_trace.restype = C.c_int
+        lib.refh_plan_milp.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_long, C.c_double,
+                                       C.c_int, _i16p, _i32p, _f64p, _i64p]
+        lib.refh_plan_milp.restype = C.c_double
         _ref = lib
     return _ref
 
@@ -327,6 +330,33 @@ class RefCluster:
                                   np.ascontiguousarray(in_len, np.int32),
                                   np.ascontiguousarray(out_len, np.int32), H, nh, hn, hs, he)
         return den, nh, hn.reshape(R, H), hs.reshape(R, H), he.reshape(R, H)
+
+
+HYB_SO = os.path.join(ROOT, "oracle", "_ref", "libhelio_hybrid.so")
+
+
+def plan_milp(lib, prefix, handle, N, partial, gap=0.0, lex=False, node_budget=-1, prune=0.0, warm=True):
+    """plan_placement through a harness (refh_ = pure reference, hyb_ = the
+    reference planner over the B200 drop-in).  -> (objective, row, status,
+    best_bound, nodes_explored)."""
+    fn = getattr(lib, prefix + "plan_milp")
+    row = np.zeros((N, 2), np.int16)
+    st = np.zeros(1, np.int32)
+    bb = np.zeros(1, np.float64)
+    ne = np.zeros(1, np.int64)
+    obj = fn(handle, int(partial), gap, int(lex), node_budget, prune, int(warm), row, st, bb, ne)
+    return obj, row, int(st[0]), float(bb[0]), int(ne[0])
+
+
+def hybrid():
+    lib = C.CDLL(HYB_SO)
+    lib.hyb_cluster_from_json.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+    lib.hyb_cluster_from_json.restype = C.c_void_p
+    lib.hyb_cluster_free.argtypes = [C.c_void_p]
+    lib.hyb_plan_milp.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_long, C.c_double,
+                                  C.c_int, _i16p, _i32p, _f64p, _i64p]
+    lib.hyb_plan_milp.restype = C.c_double
+    return lib
 
 
 def ref_trace(count, seed, mean_in=763.0, mean_out=232.0, max_in=2048, max_out=1024, rate=0.0,
