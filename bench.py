@@ -376,24 +376,25 @@ def main():
         hv = torch.empty(B, dtype=torch.float64).pin_memory()
         hs = torch.empty(B, dtype=torch.int32).pin_memory()
         for _ in range(2):
-            eng.score_host_ptr(host.data_ptr(), B, hv.data_ptr(), hs.data_ptr(), True)
+            eng.score_best_host_ptr(host.data_ptr(), B, hv.data_ptr(), hs.data_ptr(), True)
         times = []
         for _ in range(args.steps):
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            eng.score_host_ptr(host.data_ptr(), B, hv.data_ptr(), hs.data_ptr(), True)
-            v = hv.numpy()
-            ok = (hs.numpy() == 0) & (v > 0)
-            _ = int(np.argmax(np.where(ok, v, -1.0)))
+            e2e_best = eng.score_best_host_ptr(host.data_ptr(), B, hv.data_ptr(), hs.data_ptr(), True)
             times.append(time.perf_counter() - t0)
+        if world == 1:
+            assert int(e2e_best[1]) == recs[0][1], "e2e winner differs from the device path"
         tt = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_rate = B * world * args.steps / float(tt.item())
         assert torch.equal(hv.view(torch.int64), vals.cpu().view(torch.int64)), "e2e values differ from device path"
         e2e = {"value": e2e_rate, "unit": "evals/s", "h2d_bytes_per_step": B * world * 4 * N,
-               "d2h_bytes_per_step": B * world * 12}
+               "d2h_bytes_per_step": B * world * 12 + 16 * world,
+               "call": "helio_gpu_score_best_host (pinned host placements in; every value + status and the "
+                       "first-max winner out)"}
 
     routing = None
     if rank == 0 and not args.no_routing:

@@ -137,6 +137,13 @@ int helio_gpu_score(helio_gpu_ctx* ctx, const int16_t* d_placements, int64_t B, 
 int helio_gpu_score_host(helio_gpu_ctx* ctx, const int16_t* h_placements, int64_t B,
                          int allow_partial, double* h_values, int32_t* h_status);
 
+/* Same, plus the first maximum over status==0 candidates with value > 0
+ * (enumerate.hpp:59), reduced on the device; h_values/h_status may both be
+ * NULL when only the winner is wanted.  *h_index = -1 if nothing beats 0. */
+int helio_gpu_score_best_host(helio_gpu_ctx* ctx, const int16_t* h_placements, int64_t B,
+                              int allow_partial, double* h_values, int32_t* h_status,
+                              double* h_best, int64_t* h_index);
+
 /* Full FlowGraph (edges in reference order, with max_flow's per-edge flows)
  * for K candidates; synchronous, host buffers.  h_edges is [K][max_edges]. */
 int helio_gpu_flows_host(helio_gpu_ctx* ctx, const int16_t* h_placements, int64_t K,

@@ -76,6 +76,8 @@ struct helio_gpu_ctx {
   int64_t ovf_cap[2] = {0, 0};
   double* d_pv = nullptr;
   long long* d_pi = nullptr;
+  double* d_best = nullptr;   // per-chunk best of score_best_host
+  int64_t* d_bidx = nullptr;
 
   // host-call staging
   int16_t* d_pl[2] = {nullptr, nullptr};

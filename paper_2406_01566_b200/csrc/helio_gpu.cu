@@ -1569,8 +1569,10 @@ int helio_gpu_create(int device, helio_gpu_ctx** out) {
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
       cudaMalloc(&ctx->d_work, 4 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMalloc(&ctx->d_ovf_count, 2 * sizeof(unsigned int)) != cudaSuccess ||
-      cudaMalloc(&ctx->d_pv, 4096 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&ctx->d_pi, 4096 * sizeof(long long)) != cudaSuccess) {
+      cudaMalloc(&ctx->d_pv, 3 * 4096 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_pi, 3 * 4096 * sizeof(long long)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_best, 2 * 4096 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_bidx, 2 * 4096 * sizeof(int64_t)) != cudaSuccess) {
     helio_gpu_destroy(ctx);
     return HELIO_ERR_CUDA;
   }
@@ -1601,6 +1603,8 @@ void helio_gpu_destroy(helio_gpu_ctx* ctx) {
   cudaFree(ctx->d_ovf_count);
   cudaFree(ctx->d_pv);
   cudaFree(ctx->d_pi);
+  cudaFree(ctx->d_best);
+  cudaFree(ctx->d_bidx);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1859,29 +1863,47 @@ int helio_gpu_score(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int allo
   return launch_score(ctx, 0, d_pl, B, allow_partial ? 1 : 0, d_values, d_status, st, fo, true, ctx->mode);
 }
 
-int helio_gpu_score_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allow_partial,
-                         double* h_values, int32_t* h_status) {
+}  // extern "C"
+
+namespace {
+int argmax_on(helio_gpu_ctx* ctx, int scratch, const double* d_values, const int32_t* d_status, int64_t B,
+              int64_t index_base, double* d_best, int64_t* d_index, cudaStream_t st);
+
+// Host-buffer scoring, pipelined over two streams in chunks: H2D of chunk c+1
+// and D2H of chunk c-1 overlap the kernels of chunk c.  With pinned caller
+// buffers everything is enqueued up front (no host waits until the end);
+// pageable buffers go through pinned staging.  Optionally reduces the first
+// maximum on the device per chunk (best/index).
+int score_host_impl(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allow_partial, double* h_values,
+                    int32_t* h_status, double* h_best, int64_t* h_index) {
   if (!ctx) return HELIO_ERR_INVALID;
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
-  if (B < 0 || (B > 0 && (!h_pl || !h_values || !h_status))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
-  if (B == 0) return HELIO_OK;
+  if (B < 0 || (B > 0 && (!h_pl || (!h_values) != (!h_status) || (!h_values && !h_best))))
+    return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  if (B == 0) {
+    if (h_best) *h_best = 0.0;
+    if (h_index) *h_index = -1;
+    return HELIO_OK;
+  }
   CK(cudaSetDevice(ctx->device));
-  const int64_t chunk = std::min<int64_t>(B, 1 << 17);
+  const int64_t chunk = std::min<int64_t>(B, 1 << 18);
+  const int64_t nchunks = (B + chunk - 1) / chunk;
+  if (h_best && nchunks > 2 * 4096) return fail(ctx, HELIO_ERR_TOO_LARGE, "batch too large for the best reduction");
   int rc = ensure_stage(ctx, chunk);
   if (rc) return rc;
   const bool pin_in = is_pinned(h_pl);
-  const bool pin_out = is_pinned(h_values) && is_pinned(h_status);
+  const bool want_vals = h_values != nullptr;
+  const bool pin_out = want_vals && is_pinned(h_values) && is_pinned(h_status);
   const size_t row = sizeof(int16_t) * 2 * ctx->N;
-  const int64_t nchunks = (B + chunk - 1) / chunk;
   FlowOut fo{nullptr, nullptr, nullptr, 0};
   for (int64_t c = 0; c < nchunks; ++c) {
     const int s = (int)(c & 1);
     cudaStream_t st = ctx->pipe[s];
     const int64_t lo = c * chunk, n = std::min(chunk, B - lo);
-    if (c >= 2) {
-      // retire chunk c-2 of this stage before reusing its buffers
+    if (c >= 2 && (!pin_in || (want_vals && !pin_out))) {
+      // staging buffers of chunk c-2 are reused: retire it first
       CK(cudaStreamSynchronize(st));
-      if (!pin_out) {
+      if (want_vals && !pin_out) {
         const int64_t plo = (c - 2) * chunk, pn = std::min(chunk, B - plo);
         std::memcpy(h_values + plo, ctx->h_val_pin[s], sizeof(double) * pn);
         std::memcpy(h_status + plo, ctx->h_st_pin[s], sizeof(int32_t) * pn);
@@ -1896,21 +1918,58 @@ int helio_gpu_score_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int
     rc = launch_score(ctx, s, ctx->d_pl[s], n, allow_partial ? 1 : 0, ctx->d_val[s], ctx->d_st[s], st, fo,
                       false, ctx->mode);
     if (rc) return rc;
-    double* vdst = pin_out ? h_values + lo : ctx->h_val_pin[s];
-    int32_t* sdst = pin_out ? h_status + lo : ctx->h_st_pin[s];
-    CK(cudaMemcpyAsync(vdst, ctx->d_val[s], sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(sdst, ctx->d_st[s], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    if (h_best) {
+      rc = argmax_on(ctx, s, ctx->d_val[s], ctx->d_st[s], n, lo, ctx->d_best + c, ctx->d_bidx + c, st);
+      if (rc) return rc;
+    }
+    if (want_vals) {
+      double* vdst = pin_out ? h_values + lo : ctx->h_val_pin[s];
+      int32_t* sdst = pin_out ? h_status + lo : ctx->h_st_pin[s];
+      CK(cudaMemcpyAsync(vdst, ctx->d_val[s], sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(sdst, ctx->d_st[s], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    }
   }
-  for (int64_t c = std::max<int64_t>(0, nchunks - 2); c < nchunks; ++c) {
+  const int64_t first_tail = (pin_in && (!want_vals || pin_out)) ? 0 : std::max<int64_t>(0, nchunks - 2);
+  for (int64_t c = first_tail; c < nchunks; ++c) {
     const int s = (int)(c & 1);
     CK(cudaStreamSynchronize(ctx->pipe[s]));
-    if (!pin_out) {
+    if (want_vals && !pin_out) {
       const int64_t lo = c * chunk, n = std::min(chunk, B - lo);
       std::memcpy(h_values + lo, ctx->h_val_pin[s], sizeof(double) * n);
       std::memcpy(h_status + lo, ctx->h_st_pin[s], sizeof(int32_t) * n);
     }
   }
+  if (h_best) {
+    std::vector<double> bv(nchunks);
+    std::vector<int64_t> bi(nchunks);
+    CK(cudaMemcpy(bv.data(), ctx->d_best, sizeof(double) * nchunks, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(bi.data(), ctx->d_bidx, sizeof(int64_t) * nchunks, cudaMemcpyDeviceToHost));
+    double best = 0.0;
+    int64_t idx = -1;
+    for (int64_t c = 0; c < nchunks; ++c)  // chunks in index order: strict '>' keeps the first max
+      if (bi[c] >= 0 && (idx < 0 || bv[c] > best)) {
+        best = bv[c];
+        idx = bi[c];
+      }
+    *h_best = best;
+    if (h_index) *h_index = idx;
+  }
   return HELIO_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int helio_gpu_score_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allow_partial,
+                         double* h_values, int32_t* h_status) {
+  if (!h_values || !h_status) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  return score_host_impl(ctx, h_pl, B, allow_partial, h_values, h_status, nullptr, nullptr);
+}
+
+int helio_gpu_score_best_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allow_partial,
+                              double* h_values, int32_t* h_status, double* h_best, int64_t* h_index) {
+  if (!h_best || !h_index) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  return score_host_impl(ctx, h_pl, B, allow_partial, h_values, h_status, h_best, h_index);
 }
 
 int helio_gpu_flows_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t K, int allow_partial,
@@ -2027,19 +2086,31 @@ int helio_gpu_maxflow_raw_host(helio_gpu_ctx* ctx, int64_t G, const int32_t* h_n
   return HELIO_OK;
 }
 
+}  // extern "C"
+
+namespace {
+int argmax_on(helio_gpu_ctx* ctx, int scratch, const double* d_values, const int32_t* d_status, int64_t B,
+              int64_t index_base, double* d_best, int64_t* d_index, cudaStream_t st) {
+  const int P = (int)std::min<int64_t>(std::max<int64_t>((B + 255) / 256, 1), 2 * ctx->sm_count);
+  double* pv = ctx->d_pv + 4096 * scratch;
+  long long* pi = ctx->d_pi + 4096 * scratch;
+  argmax_partial<<<P, 256, 0, st>>>(d_values, d_status, B, pv, pi);
+  argmax_final<<<1, 32, 0, st>>>(pv, pi, P, index_base, d_best, d_index);
+  CK(cudaGetLastError());
+  ctx->launches += 2;
+  return HELIO_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int helio_gpu_argmax(helio_gpu_ctx* ctx, const double* d_values, const int32_t* d_status, int64_t B,
                      int64_t index_base, double* d_best, int64_t* d_index, void* stream) {
   if (!ctx) return HELIO_ERR_INVALID;
   if (!d_best || !d_index || (B > 0 && (!d_values || !d_status))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-  int P = (int)std::min<int64_t>(std::max<int64_t>((B + 255) / 256, 1), 2 * ctx->sm_count);
-  argmax_partial<<<P, 256, 0, st>>>(d_values, d_status, B, ctx->d_pv, ctx->d_pi);
-  CK(cudaGetLastError());
-  argmax_final<<<1, 32, 0, st>>>(ctx->d_pv, ctx->d_pi, P, index_base, d_best, d_index);
-  CK(cudaGetLastError());
-  ctx->launches += 2;
-  return HELIO_OK;
+  return argmax_on(ctx, 2, d_values, d_status, B, index_base, d_best, d_index, st);
 }
 
 int helio_gpu_generate(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B, uint32_t ppm,

@@ -699,6 +699,23 @@ PYBIND11_MODULE(_helio, m) {
           py::arg("placements_ptr"), py::arg("count"), py::arg("values_ptr"), py::arg("status_ptr"),
           py::arg("allow_partial") = true)
       .def(
+          "score_best_host_ptr",
+          [](PyEngine& e, uintptr_t pl, int64_t B, uintptr_t values, uintptr_t status, bool allow_partial) {
+            double best = 0;
+            int64_t idx = -1;
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = helio_gpu_score_best_host(e.eng->ctx(), reinterpret_cast<const int16_t*>(pl), B,
+                                             allow_partial ? 1 : 0, reinterpret_cast<double*>(values),
+                                             reinterpret_cast<int32_t*>(status), &best, &idx);
+            }
+            e.eng->check(rc, "helio_gpu_score_best_host");
+            return py::make_tuple(best, idx);
+          },
+          py::arg("placements_ptr"), py::arg("count"), py::arg("values_ptr"), py::arg("status_ptr"),
+          py::arg("allow_partial") = true, "Host buffers: every value + status, and the first maximum.")
+      .def(
           "generate_device",
           [](PyEngine& e, uint64_t seed, int64_t first, int64_t B, uint32_t ppm, uintptr_t out, uintptr_t stream) {
             e.eng->check(helio_gpu_generate(e.eng->ctx(), seed, first, B, ppm, reinterpret_cast<int16_t*>(out),

@@ -291,3 +291,26 @@ def test_exhaustive_search_matches_reference():
         assert bits([best])[0] == bits(z["values"][i : i + 1])[0], key
         assert np.array_equal(row, z["rows"][i][:N]), key
         assert total >= scored
+
+
+def test_score_best_host_matches_first_max():
+    import torch
+    c, e = engine("het42-70b_float")
+    rows = h.generate_host(list(e.kmax), c.num_layers, 99, 0, 700_000, 80000)
+    rows[::97, 0] = (0, 99)  # invalid rows (status 2) must be skipped
+    pin = torch.from_numpy(rows).pin_memory()
+    for mode in ("parity", "score"):
+        e.mode = mode
+        try:
+            v = torch.empty(len(rows), dtype=torch.float64).pin_memory()
+            s = torch.empty(len(rows), dtype=torch.int32).pin_memory()
+            best, idx = e.score_best_host_ptr(pin.data_ptr(), len(rows), v.data_ptr(), s.data_ptr(), True)
+            vv, ss = v.numpy(), s.numpy()
+            ok = (ss == 0) & (vv > 0)
+            want = int(np.argmax(np.where(ok, vv, -1.0)))
+            assert idx == want and best == vv[want]
+            # pageable buffers take the staged path and agree
+            v2, s2 = e.score(rows)
+            assert np.array_equal(bits(v2), bits(vv)) and np.array_equal(s2, ss)
+        finally:
+            e.mode = "parity"
