@@ -167,7 +167,6 @@ __device__ __forceinline__ double ref_min(double a, double b) { return b < a ? b
 // (every lane holds the same two 64-bit words, so the enqueue test is a
 // uniform register test), and a failed scan of the last arc chunk falls
 // straight into the relabel instead of taking another loop trip.
-template <bool SMALLV>
 __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, const int lane) {
   VState* vs = g.vs;
   for (int x = lane; x < n; x += 32) {
@@ -178,7 +177,7 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
     v.b = g.abeg[x];
     v.deg = (int16_t)(g.abeg[x + 1] - g.abeg[x]);
     vs[x] = v;
-    if (!SMALLV) g.inq[x] = 0;
+    g.inq[x] = 0;
   }
   for (int x = lane; x <= 2 * n; x += 32) g.cnt[x] = 0;
   __syncwarp();
@@ -186,20 +185,11 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
     g.cnt[0] = (int16_t)(n - 1);
     g.cnt[n] += 1;
   }
-  unsigned long long iq0 = 0ull, iq1 = 0ull;
-  auto in_queue = [&](int x) -> bool {
-    if (SMALLV) return (((x < 64) ? iq0 : iq1) >> (x & 63)) & 1ull;
-    return g.inq[x] != 0;
-  };
-  auto mark = [&](int x, bool on) {
-    if (SMALLV) {
-      const unsigned long long bit = 1ull << (x & 63);
-      if (x < 64) iq0 = on ? (iq0 | bit) : (iq0 & ~bit);
-      else iq1 = on ? (iq1 | bit) : (iq1 & ~bit);
-    } else {
-      g.inq[x] = on ? 1 : 0;  // every lane writes, every lane reads its own write
-    }
-  };
+  // in-queue flags: every lane writes them and every lane reads its own
+  // write, so no cross-lane ordering is needed (a byte test beat a register
+  // bitmask on issue slots)
+  auto in_queue = [&](int x) -> bool { return g.inq[x] != 0; };
+  auto mark = [&](int x, bool on) { g.inq[x] = on ? 1 : 0; };
   int tail = 0, qcount = 0;
   // saturate source arcs in adjacency order (:168-173): uniform loop, lane 0 stores
   __syncwarp();
@@ -1215,8 +1205,7 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     if (st == 0 && MODE == HELIO_MODE_SCORE) {
       value = V <= 128 ? solve_ek_bits(g, V, 0, 1, lane) : solve_ek_batched(g, V, 0, 1, lane);
     } else if (st == 0) {
-      if (V <= 128) solve_fifo2<true>(g, V, 0, 1, lane);
-      else solve_fifo2<false>(g, V, 0, 1, lane);
+      solve_fifo2(g, V, 0, 1, lane);
       value = built_value(cd, g, lane);
       if (fo.edges) {
         if (E <= fo.max_e) emit_edges(cd, g, (V - 2) / 2, partial, lane, fo.edges + b * fo.max_e);
@@ -1290,8 +1279,7 @@ __global__ void raw_kernel(Layout lay, int64_t G, const int32_t* __restrict__ gn
       }
     }
     __syncwarp();
-    if (n <= 128) solve_fifo2<true>(g, n, s, t, lane);
-    else solve_fifo2<false>(g, n, s, t, lane);
+    solve_fifo2(g, n, s, t, lane);
     if (flows) {
       for (int i = lane; i < m; i += 32) {
         double f = ecap[e0 + i] - g.cap[g.efwd[i]];

@@ -1,2 +1,3 @@
 set -x
-timeout 900 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -15 gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests -q -m gpu --timeout 600 -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -4 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1; echo bench=$?; tail -1 gpurun_out/bench_full.log | cut -c1-250; grep -o '"other_mode": {[^}]*}' gpurun_out/bench_full.log; grep -o '"e2e": {[^}]*}' gpurun_out/bench_full.log
