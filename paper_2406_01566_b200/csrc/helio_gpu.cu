@@ -978,10 +978,21 @@ __device__ __forceinline__ unsigned long long warp_or64(unsigned long long v) {
   return ((unsigned long long)hi << 32) | lo;
 }
 
+// Pair closure: in this numbering a node's vertices are v and v^1 (in = 2+2k,
+// out = 3+2k), joined by its compute arc.  When a BFS level reaches one half
+// of a node whose pair arc has residual capacity, the other half joins the
+// same level (a shift on the 128-bit frontier), so the BFS walks nodes rather
+// than split vertices and needs about half the levels.  Paths remain valid
+// augmenting paths and the choice stays deterministic.
+__device__ __forceinline__ unsigned long long swap_pairs(unsigned long long x) {
+  return ((x & 0x5555555555555555ull) << 1) | ((x & 0xAAAAAAAAAAAAAAAAull) >> 1);
+}
+
 __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int t, const int lane) {
   // rows R[x] (residual out-neighbours of x, 128 bits) in the VState region;
-  // BFS level per vertex in the count region; canonical parent arc per vertex
-  // in `cur`; the augmenting path in the queue region.
+  // per-vertex BFS code (2*level, +1 if added by the pair closure) in the
+  // count region; canonical parent arc per vertex in `cur`; the augmenting
+  // path in the queue region.
   ulonglong2* R = reinterpret_cast<ulonglong2*>(g.vs);
   int16_t* dist = g.cnt;
   int16_t* par = g.cur;
@@ -1000,6 +1011,24 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
   __syncwarp();
   double value = 0.0;
   for (;;) {
+    // pair arcs with residual capacity: bit v set iff R[v] holds v^1 (v >= 2)
+    unsigned long long P0, P1;
+    {
+      unsigned b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int v = lane + 32 * i;
+        bool pr = false;
+        if (v >= 2 && v < n) {
+          const ulonglong2 r = R[v];
+          const int w = v ^ 1;
+          pr = ((w < 64 ? r.x : r.y) >> (w & 63)) & 1ull;
+        }
+        b[i] = __ballot_sync(FULL, pr);
+      }
+      P0 = ((unsigned long long)b[1] << 32) | b[0];
+      P1 = ((unsigned long long)b[3] << 32) | b[2];
+    }
     for (int x = lane; x < n; x += 32) dist[x] = (int16_t)(x == s ? 0 : -1);
     unsigned long long F0 = s < 64 ? (1ull << s) : 0ull, F1 = s < 64 ? 0ull : (1ull << (s - 64));
     unsigned long long V0 = F0, V1 = F1;
@@ -1016,16 +1045,22 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
           a1 |= r.y;
         }
       }
-      const unsigned long long n0 = warp_or64(a0) & ~V0;
-      const unsigned long long n1 = warp_or64(a1) & ~V1;
+      unsigned long long n0 = warp_or64(a0) & ~V0;
+      unsigned long long n1 = warp_or64(a1) & ~V1;
       if ((n0 | n1) == 0ull) break;
       ++d;
+      const unsigned long long c0 = swap_pairs(n0 & P0) & ~V0 & ~n0;
+      const unsigned long long c1 = swap_pairs(n1 & P1) & ~V1 & ~n1;
+      n0 |= c0;
+      n1 |= c1;
       V0 |= n0;
       V1 |= n1;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
+        const int sh = lane + 32 * (i & 1);
         const unsigned long long w = (i < 2) ? n0 : n1;
-        if ((w >> (lane + 32 * (i & 1))) & 1ull) dist[lane + 32 * i] = (int16_t)d;
+        const unsigned long long cw = (i < 2) ? c0 : c1;
+        if ((w >> sh) & 1ull) dist[lane + 32 * i] = (int16_t)(2 * d + (int)((cw >> sh) & 1ull));
       }
       F0 = n0;
       F1 = n1;
@@ -1036,14 +1071,18 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
     }
     if (!found) break;
     __syncwarp();
-    // canonical parent of every visited vertex: its first arc, in adjacency
-    // order, back to a vertex one level closer with residual capacity
+    // canonical parent of every visited vertex: a closure vertex takes its
+    // pair arc; otherwise the first arc, in adjacency order, back to a vertex
+    // of the previous level with residual capacity
     for (int x = lane; x < n; x += 32) {
-      const int dx = dist[x];
-      if (dx <= 0) continue;
+      const int cx = dist[x];
+      if (cx <= 0) continue;
+      const int want = (cx >> 1) - 1;
       for (int a = g.abeg[x], e = g.abeg[x + 1]; a < e; ++a) {
+        const int u = g.to[a];
         const int r = g.rv[a];
-        if (dist[g.to[a]] == dx - 1 && g.cap[r] > FLOW_EPS) {
+        const bool ok = (cx & 1) ? (u == (x ^ 1)) : (dist[u] >= 0 && (dist[u] >> 1) == want && g.cap[r] > FLOW_EPS);
+        if (ok) {
           par[x] = (int16_t)r;
           break;
         }
