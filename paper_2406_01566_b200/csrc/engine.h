@@ -88,6 +88,10 @@ struct helio_gpu_ctx {
   int32_t* h_st_pin[2] = {nullptr, nullptr};
   int64_t stage_cap = 0;
   cudaStream_t pipe[2] = {nullptr, nullptr};
+
+  // routing arena (route.cu), grows only
+  void* d_route = nullptr;
+  size_t route_cap = 0;
 };
 
 

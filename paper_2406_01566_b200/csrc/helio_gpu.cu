@@ -1632,6 +1632,7 @@ void helio_gpu_destroy(helio_gpu_ctx* ctx) {
   cudaFree(ctx->d_pi);
   cudaFree(ctx->d_best);
   cudaFree(ctx->d_bidx);
+  cudaFree(ctx->d_route);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);

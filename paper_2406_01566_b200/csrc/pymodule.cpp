@@ -444,7 +444,22 @@ py::tuple engine_route(PyEngine& pe, const py::array& placement_row, const py::a
   }
   const int64_t R = iin.size();
   if (iout.size() != R) throw ValidationError("input/output length arrays differ in size");
-  if (max_hops <= 0) max_hops = pe.eng->num_layers();
+  if (max_hops <= 0) {
+    // longest route the plan allows: hops along node -> node edges from the
+    // coordinator (every hop covers >= 1 layer, so at most L)
+    std::vector<std::vector<int>> succ(N + 1);
+    for (const auto& x : pe_)
+      if (x.dst_node >= 0 && x.src_node >= -1 && x.src_node < N) succ[x.src_node + 1].push_back(x.dst_node + 1);
+    std::vector<int> memo(N + 1, -1);
+    std::function<int(int, int)> longest = [&](int v, int depth) -> int {
+      if (depth > pe.eng->num_layers()) return 0;
+      if (memo[v] >= 0) return memo[v];
+      int best = 0;
+      for (int w : succ[v]) best = std::max(best, 1 + longest(w, depth + 1));
+      return memo[v] = best;
+    };
+    max_hops = std::max(1, std::min(pe.eng->num_layers(), longest(0, 0)));
+  }
   const py::ssize_t HS = exec_ranges ? R : 0;
   py::array_t<int32_t> nh(R), hn({(py::ssize_t)R, (py::ssize_t)max_hops}), hs({HS, (py::ssize_t)max_hops}),
       he({HS, (py::ssize_t)max_hops});

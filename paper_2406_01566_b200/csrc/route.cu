@@ -202,11 +202,20 @@ __global__ void route_sequential(int64_t R, int nv, int L, int max_hops, double 
   *deferred = den;
 }
 
-template <typename T>
-int dalloc(helio_gpu_ctx* ctx, T** p, size_t n) {
-  CK(cudaMalloc(p, sizeof(T) * std::max<size_t>(n, 1)));
-  return HELIO_OK;
-}
+// Route buffers are carved from one context-owned device arena that only
+// grows, so steady-state calls make no cudaMalloc/cudaFree.
+struct Arena {
+  helio_gpu_ctx* ctx;
+  size_t off = 0;
+  bool sizing = true;
+  template <typename T>
+  int take(T** p, size_t n) {
+    const size_t bytes = (sizeof(T) * std::max<size_t>(n, 1) + 255) / 256 * 256;
+    if (!sizing) *p = reinterpret_cast<T*>(static_cast<char*>(ctx->d_route) + off);
+    off += bytes;
+    return HELIO_OK;
+  }
+};
 
 }  // namespace
 
@@ -307,27 +316,56 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   do {                       \
     if (!rc) rc = (x);       \
   } while (0)
-  TRY(dalloc(ctx, &d_obeg, nv + 1));
-  TRY(dalloc(ctx, &d_odst, ne));
-  TRY(dalloc(ctx, &d_oes, ne));
-  TRY(dalloc(ctx, &d_oee, ne));
-  TRY(dalloc(ctx, &d_flow, ne));
-  TRY(dalloc(ctx, &d_node, nv));
-  TRY(dalloc(ctx, &d_kvcap, nv));
-  TRY(dalloc(ctx, &d_w, ne));
-  TRY(dalloc(ctx, &d_wmax, nv));
-  TRY(dalloc(ctx, &d_cycoff, nv + 1));
-  TRY(dalloc(ctx, &d_cyc, cyc_off[nv]));
-  TRY(dalloc(ctx, &d_cyclen, nv));
-  TRY(dalloc(ctx, &d_in, R));
-  TRY(dalloc(ctx, &d_out, R));
-  TRY(dalloc(ctx, &d_nh, R));
-  TRY(dalloc(ctx, &d_hn, HR));
   const bool want_se = h_hs != nullptr;
-  TRY(dalloc(ctx, &d_hs, want_se ? HR : 1));
-  TRY(dalloc(ctx, &d_he, want_se ? HR : 1));
-  TRY(dalloc(ctx, &d_err, 1));
-  TRY(dalloc(ctx, &d_den, 1));
+  const bool closed_path = closed && R > 0;
+  if (closed_path) {
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (int32_t*)nullptr, (int32_t*)nullptr, (int)R, st);
+  }
+  Arena ar{ctx};
+  for (int pass = 0; pass < 2 && !rc; ++pass) {
+    ar.off = 0;
+    ar.sizing = pass == 0;
+    TRY(ar.take(&d_obeg, nv + 1));
+    TRY(ar.take(&d_odst, ne));
+    TRY(ar.take(&d_oes, ne));
+    TRY(ar.take(&d_oee, ne));
+    TRY(ar.take(&d_flow, ne));
+    TRY(ar.take(&d_node, nv));
+    TRY(ar.take(&d_kvcap, nv));
+    TRY(ar.take(&d_w, ne));
+    TRY(ar.take(&d_wmax, nv));
+    TRY(ar.take(&d_cycoff, nv + 1));
+    TRY(ar.take(&d_cyc, cyc_off[nv]));
+    TRY(ar.take(&d_cyclen, nv));
+    TRY(ar.take(&d_in, R));
+    TRY(ar.take(&d_out, R));
+    TRY(ar.take(&d_nh, R));
+    TRY(ar.take(&d_hn, HR));
+    TRY(ar.take(&d_hs, want_se ? HR : 1));
+    TRY(ar.take(&d_he, want_se ? HR : 1));
+    TRY(ar.take(&d_err, 1));
+    TRY(ar.take(&d_den, 1));
+    if (closed_path) {
+      TRY(ar.take(&d_cur, R));
+      TRY(ar.take(&d_cov, R));
+      TRY(ar.take(&d_flag, R));
+      TRY(ar.take(&d_rank, R));
+      TRY(ar.take(reinterpret_cast<char**>(&d_tmp), tmp_bytes));
+    } else {
+      TRY(ar.take(&d_kvest, nv));
+      TRY(ar.take(&d_pround, nv));
+      TRY(ar.take(&d_pidx, nv));
+      TRY(ar.take(&d_chv, L + 1));
+      TRY(ar.take(&d_chb, L + 1));
+    }
+    if (pass == 0 && ar.off > ctx->route_cap) {
+      cudaFree(ctx->d_route);
+      ctx->d_route = nullptr;
+      ctx->route_cap = 0;
+      if (cudaMalloc(&ctx->d_route, ar.off) != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route arena alloc");
+      else ctx->route_cap = ar.off;
+    }
+  }
   if (!rc) {
     auto H2D = [&](void* d, const void* h, size_t bytes) {
       if (bytes && !rc && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
@@ -354,16 +392,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   }
   int64_t den = 0;
   if (!rc && closed && R > 0) {
-    TRY(dalloc(ctx, &d_cur, R));
-    TRY(dalloc(ctx, &d_cov, R));
-    TRY(dalloc(ctx, &d_flag, R));
-    TRY(dalloc(ctx, &d_rank, R));
-    if (!rc) {
-      cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_flag, d_rank, (int)R, st);
-      if (cudaMalloc(&d_tmp, std::max<size_t>(tmp_bytes, 1)) != cudaSuccess)
-        rc = fail(ctx, HELIO_ERR_CUDA, "route scan alloc failed");
-    }
-    if (!rc) {
+    {
       const int grid = (int)std::min<int64_t>((R + 255) / 256, 8 * ctx->sm_count);
       route_init<<<grid, 256, 0, st>>>(R, d_cur, d_nh, d_cov);
       ctx->launches++;
@@ -385,12 +414,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
       if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route kernels failed");
     }
   } else if (!rc && R > 0) {
-    TRY(dalloc(ctx, &d_kvest, nv));
-    TRY(dalloc(ctx, &d_pround, nv));
-    TRY(dalloc(ctx, &d_pidx, nv));
-    TRY(dalloc(ctx, &d_chv, L + 1));
-    TRY(dalloc(ctx, &d_chb, L + 1));
-    if (!rc) {
+    {
       route_sequential<<<1, 1, 0, st>>>(R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst, d_oes,
                                         d_oee, d_w, d_wmax, d_node, d_kvcap, d_kvest, d_pround, d_pidx,
                                         d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr, want_se ? d_he : nullptr,
@@ -418,11 +442,6 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   }
   if (!rc && herr) rc = fail(ctx, HELIO_ERR_INVALID, "plan edges do not tile the layer range");
   if (!rc && h_deferred) *h_deferred = den;
-  cudaFree(d_obeg); cudaFree(d_odst); cudaFree(d_oes); cudaFree(d_oee); cudaFree(d_flow); cudaFree(d_node);
-  cudaFree(d_kvcap); cudaFree(d_w); cudaFree(d_wmax); cudaFree(d_cycoff); cudaFree(d_cyc); cudaFree(d_in);
-  cudaFree(d_out); cudaFree(d_nh); cudaFree(d_hn); cudaFree(d_hs); cudaFree(d_he); cudaFree(d_err);
-  cudaFree(d_den); cudaFree(d_cur); cudaFree(d_cov); cudaFree(d_flag); cudaFree(d_rank); cudaFree(d_tmp);
-  cudaFree(d_cyclen); cudaFree(d_kvest); cudaFree(d_pround); cudaFree(d_pidx); cudaFree(d_chv); cudaFree(d_chb);
 #undef TRY
   return rc;
 }
