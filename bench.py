@@ -191,6 +191,75 @@ def routing_leg(h, clusters, dev, sp, requests, with_reference):
     return out
 
 
+OTHER_CONFIGS = [
+    # (config, capacity, generator, candidates) — BASELINE.json configs[0,1,3,4]; het42 int-capacity
+    ("single24-70b", "float", "chain", 100_000),
+    ("single24-30b", "float", "chain", 100_000),
+    ("geo24", "float", "chain", 100_000),
+    ("het42-70b", "int", "chain", 100_000),
+    ("syn256-120l", "float", "walk", 20_000),
+]
+
+
+def config_table(h, clusters, dev, sp, with_reference):
+    """Throughput of both modes on the other BASELINE configs (parity-test
+    cases of the tier; reported for coverage, not the headline)."""
+    import numpy as np
+    import torch
+
+    rows = []
+    for name, cap, gen, B in OTHER_CONFIGS:
+        d = clusters.CONFIGS[name](cap)
+        c = h.Cluster.from_json(json.dumps(d))
+        e = h.Engine(c, device=dev)
+        pl = torch.empty((B, e.num_nodes, 2), dtype=torch.int16, device=f"cuda:{dev}")
+        if gen == "walk":
+            e.generate_walk_device(SEED, 0, B, pl.data_ptr(), sp)
+        else:
+            e.generate_device(SEED, 0, B, 0, pl.data_ptr(), sp)
+        v = torch.empty(B, dtype=torch.float64, device=pl.device)
+        st = torch.empty(B, dtype=torch.int32, device=pl.device)
+        rec = {"config": name, "capacity": cap, "generator": gen, "candidates": B,
+               "nodes": e.num_nodes, "links": c.num_links, "layers": c.num_layers}
+        out_vals = {}
+        for mode in ("score", "parity"):
+            e.mode = mode
+            for _ in range(2):
+                e.score_device(pl.data_ptr(), B, v.data_ptr(), st.data_ptr(), True, sp)
+            ms = []
+            for _ in range(3):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(torch.cuda.current_stream(pl.device))
+                e.score_device(pl.data_ptr(), B, v.data_ptr(), st.data_ptr(), True, sp)
+                b.record(torch.cuda.current_stream(pl.device))
+                torch.cuda.synchronize(pl.device)
+                ms.append(a.elapsed_time(b))
+            rec[mode] = B / (min(ms) / 1e3)
+            out_vals[mode] = v.cpu().numpy().copy()
+        e.mode = "parity"
+        rec["nonzero_fraction"] = float((out_vals["parity"] > 0).mean())
+        rel = np.abs(out_vals["score"] - out_vals["parity"]) / np.maximum(1.0, np.abs(out_vals["parity"]))
+        rec["score_vs_parity_max_rel"] = float(rel.max())
+        if with_reference:
+            try:
+                sys.path.insert(0, os.path.join(ROOT, "tests"))
+                from _support import RefCluster  # test infrastructure: reference timing only
+                rc = RefCluster(d)
+                threads = os.cpu_count() or 1
+                n = min(B, 200 * threads if e.num_nodes > 100 else 2000 * threads)
+                host_rows = pl[:n].cpu().numpy()
+                t0 = time.perf_counter()
+                rv, _ = rc.score(host_rows, True, threads)
+                rec["reference"] = {"value": n / (time.perf_counter() - t0), "cores": threads,
+                                    "kind": "reference", "sample": f"first {n} candidates"}
+                rec["parity_bit_exact_on_sample"] = bool(np.array_equal(
+                    rv.view(np.int64), out_vals["parity"][:n].view(np.int64)))
+            except Exception as ex:
+                rec["reference"] = {"value": None, "sample": f"unavailable: {ex}"}
+        rows.append(rec)
+    return rows
+
+
 def run_reference(args):
     rank = env_int("RANK", 0)
     if rank != 0:
@@ -240,6 +309,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-routing", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--route-requests", type=int, default=1_000_000)
     ap.add_argument("--mode", default="score", choices=["score", "parity"],
                     help="headline scoring mode (the other mode is timed too and reported beside it)")
@@ -396,6 +466,13 @@ def main():
                "call": "helio_gpu_score_best_host (pinned host placements in; every value + status and the "
                        "first-max winner out)"}
 
+    cfg_table = None
+    if rank == 0 and not args.no_configs:
+        try:
+            cfg_table = config_table(h, clusters, local, sp, with_reference=(world == 1 and not args.no_cpu_baseline))
+        except Exception as ex:  # reported, never fatal
+            cfg_table = [{"error": str(ex)}]
+
     routing = None
     if rank == 0 and not args.no_routing:
         try:
@@ -429,7 +506,7 @@ def main():
                        "nonzero_fraction": nonzero, "status_nonzero": int((st_host != 0).sum()),
                        "best": {"value": win[0], "index": win[1]}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "routing": routing,
+            "routing": routing, "other_configs": cfg_table,
             "clocks": clk.summary(),
         }
         print(json.dumps(out))

@@ -184,6 +184,13 @@ int helio_gpu_best_exhaustive(helio_gpu_ctx* ctx, int allow_partial, int64_t max
                               double* h_best_value, int16_t* h_best_row, int64_t* h_leaves_scored,
                               int64_t* h_leaves_total);
 
+/* Link-walking covering chains (gen.h hg_candidate_walk) for sparse
+ * topologies, device and host (identical output). */
+int helio_gpu_generate_walk(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B,
+                            int16_t* d_out, void* stream);
+int helio_gpu_generate_walk_host(const helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B,
+                                 int16_t* h_out);
+
 /* IWRR routing of R requests over a plan (scheduler.cpp:58-190) in the AC8
  * admit/complete order: request r is admitted with in_len[r] and completed at
  * once with out_len[r].  Plan edges in plan order; placement is the plan's

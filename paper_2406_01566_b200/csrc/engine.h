@@ -89,6 +89,11 @@ struct helio_gpu_ctx {
   int64_t stage_cap = 0;
   cudaStream_t pipe[2] = {nullptr, nullptr};
 
+  // walk generator adjacency (gen.h hg_candidate_walk)
+  const int32_t* d_walk_beg = nullptr;
+  const int32_t* d_walk_list = nullptr;
+  std::vector<int32_t> h_walk_beg, h_walk_list;
+
   // routing arena (route.cu), grows only
   void* d_route = nullptr;
   size_t route_cap = 0;

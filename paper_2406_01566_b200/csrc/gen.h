@@ -78,3 +78,61 @@ HG_HD void hg_candidate(const int32_t* kmax, int32_t N, int32_t L, uint64_t seed
     out[2 * node + 1] = e;
   }
 }
+
+// Link-walking chains (mode "walk"): for sparse topologies, where plain
+// chains almost never connect.  From the coordinator, repeatedly step to a
+// uniformly chosen unused node reachable over a declared link (coordinator
+// -> node first), give it len ~ U[1, k]; on reaching L or a dead end,
+// restart from the coordinator at layer 0.  Adjacency: succ_beg[N+2] /
+// succ[] with row 0 = coordinator, row 1 + k = node k (link order).  `used`
+// is scratch of ceil(N/32) words.  Draw numbers follow the chain steps.
+HG_HD void hg_candidate_walk(const int32_t* kmax, int32_t N, int32_t L, uint64_t seed, uint64_t i,
+                             const int32_t* succ_beg, const int32_t* succ, uint32_t* used,
+                             int16_t* out) {
+  const uint64_t key = hg_key(seed, i);
+  for (int32_t w = 0; w < (N + 31) / 32; ++w) used[w] = 0u;
+  for (int32_t k = 0; k < N; ++k) {
+    out[2 * k] = 0;
+    out[2 * k + 1] = 0;
+  }
+  int32_t prev = -1, cur = 0;
+  uint32_t draw = 0;
+  for (int32_t step = 0; step < 2 * N; ++step) {
+    const int32_t b = succ_beg[prev + 1], e = succ_beg[prev + 2];
+    uint32_t cnt = 0;
+    for (int32_t p = b; p < e; ++p) {
+      const int32_t j = succ[p];
+      if (!((used[j >> 5] >> (j & 31)) & 1u) && kmax[j] >= 1) ++cnt;
+    }
+    if (cnt == 0) {
+      if (prev == -1) break;
+      prev = -1;
+      cur = 0;
+      continue;
+    }
+    uint32_t r = hg_uniform(hg_draw(key, draw++), cnt);
+    int32_t j = -1;
+    for (int32_t p = b; p < e; ++p) {
+      const int32_t q = succ[p];
+      if (!((used[q >> 5] >> (q & 31)) & 1u) && kmax[q] >= 1) {
+        if (r == 0) {
+          j = q;
+          break;
+        }
+        --r;
+      }
+    }
+    used[j >> 5] |= 1u << (j & 31);
+    const int32_t len = 1 + (int32_t)hg_uniform(hg_draw(key, draw++), (uint32_t)kmax[j]);
+    const int32_t en = cur + len < L ? cur + len : L;
+    out[2 * j] = (int16_t)cur;
+    out[2 * j + 1] = (int16_t)en;
+    if (en == L) {
+      prev = -1;
+      cur = 0;
+    } else {
+      prev = j;
+      cur = en;
+    }
+  }
+}

@@ -1418,6 +1418,15 @@ __global__ void gen_kernel(const int32_t* __restrict__ kmax, int N, int L, uint6
     hg_candidate(kmax, N, L, seed, (uint64_t)(first + i), ppm, perm, out + i * 2 * N);
 }
 
+__global__ void gen_walk_kernel(const int32_t* __restrict__ kmax, int N, int L, uint64_t seed, int64_t first,
+                                int64_t B, const int32_t* __restrict__ wbeg, const int32_t* __restrict__ wlist,
+                                int16_t* __restrict__ out) {
+  uint32_t used[GEN_MAX_N / 32];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < B;
+       i += (int64_t)gridDim.x * blockDim.x)
+    hg_candidate_walk(kmax, N, L, seed, (uint64_t)(first + i), wbeg, wlist, used, out + i * 2 * N);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1764,6 +1773,18 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
       ilist[2 * pi + 1] = i;
     }
   }
+  // walk generator adjacency: row 0 = coordinator's targets, row 1+k = node k's
+  // (declared links, compacted order)
+  std::vector<int32_t> wbeg(N + 2, 0), wlist;
+  for (int row = -1; row < N; ++row) {
+    wbeg[row + 1] = (int32_t)wlist.size();
+    for (int i = 0; i < Mv; ++i) {
+      int a = (int)(pack[i] & 0xffffu) - 1, b = (int)(pack[i] >> 16) - 1;
+      if (a == row && b >= 0) wlist.push_back(b);
+    }
+  }
+  wbeg[N + 1] = (int32_t)wlist.size();
+  if (wlist.empty()) wlist.push_back(0);
   // N <= 64: node sets fit one 64-bit word; out-neighbour masks and a pair ->
   // link-index matrix drive the cover-mask SCORE builder.
   const bool small_n = N <= 64;
@@ -1794,7 +1815,9 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   size_t o_ilist = o_olist + al(4 * olist.size());
   size_t o_omask = o_ilist + al(4 * ilist.size());
   size_t o_pair = o_omask + al(8 * outmask.size());
-  size_t total = o_pair + al(4 * pairlink.size());
+  size_t o_wbeg = o_pair + al(4 * pairlink.size());
+  size_t o_wlist = o_wbeg + al(4 * wbeg.size());
+  size_t total = o_wlist + al(4 * wlist.size());
   std::vector<char> hbuf(total, 0);
   std::memcpy(hbuf.data() + o_kmax, kmax16.data(), 2 * N);
   std::memcpy(hbuf.data() + o_lexrank, d->lex_rank, 4 * N);
@@ -1814,6 +1837,8 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   std::memcpy(hbuf.data() + o_ilist, ilist.data(), 4 * ilist.size());
   std::memcpy(hbuf.data() + o_omask, outmask.data(), 8 * outmask.size());
   std::memcpy(hbuf.data() + o_pair, pairlink.data(), 4 * pairlink.size());
+  std::memcpy(hbuf.data() + o_wbeg, wbeg.data(), 4 * wbeg.size());
+  std::memcpy(hbuf.data() + o_wlist, wlist.data(), 4 * wlist.size());
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->d_cluster) cudaFree(ctx->d_cluster);
   if (ctx->d_kmax32) cudaFree(ctx->d_kmax32);
@@ -1843,6 +1868,10 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   ctx->cd.in_list = reinterpret_cast<const int2*>(base + o_ilist);
   ctx->cd.out_mask = small_n ? reinterpret_cast<const unsigned long long*>(base + o_omask) : nullptr;
   ctx->cd.pair_link = small_n ? reinterpret_cast<const int32_t*>(base + o_pair) : nullptr;
+  ctx->d_walk_beg = reinterpret_cast<const int32_t*>(base + o_wbeg);
+  ctx->d_walk_list = reinterpret_cast<const int32_t*>(base + o_wlist);
+  ctx->h_walk_beg = wbeg;
+  ctx->h_walk_list = wlist;
   ctx->N = N;
   ctx->L = L;
   ctx->Mv = Mv;
@@ -2153,6 +2182,32 @@ int helio_gpu_generate(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t
   gen_kernel<<<grid, 128, 0, st>>>(ctx->d_kmax32, ctx->N, ctx->L, seed, first, B, ppm, d_out);
   CK(cudaGetLastError());
   ctx->launches++;
+  return HELIO_OK;
+}
+
+int helio_gpu_generate_walk(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B, int16_t* d_out,
+                            void* stream) {
+  if (!ctx) return HELIO_ERR_INVALID;
+  if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
+  if (ctx->N > GEN_MAX_N) return fail(ctx, HELIO_ERR_TOO_LARGE, "generator supports up to 1024 nodes");
+  if (B <= 0) return HELIO_OK;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  int grid = (int)std::min<int64_t>((B + 127) / 128, 8 * ctx->sm_count);
+  gen_walk_kernel<<<grid, 128, 0, st>>>(ctx->d_kmax32, ctx->N, ctx->L, seed, first, B, ctx->d_walk_beg,
+                                        ctx->d_walk_list, d_out);
+  CK(cudaGetLastError());
+  ctx->launches++;
+  return HELIO_OK;
+}
+
+int helio_gpu_generate_walk_host(const helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B,
+                                 int16_t* h_out) {
+  if (!ctx || !ctx->has_cluster || (B > 0 && !h_out)) return HELIO_ERR_INVALID;
+  std::vector<uint32_t> used((ctx->N + 31) / 32 + 1);
+  for (int64_t i = 0; i < B; ++i)
+    hg_candidate_walk(ctx->h_kmax.data(), ctx->N, ctx->L, seed, (uint64_t)(first + i), ctx->h_walk_beg.data(),
+                      ctx->h_walk_list.data(), used.data(), h_out + i * 2 * ctx->N);
   return HELIO_OK;
 }
 

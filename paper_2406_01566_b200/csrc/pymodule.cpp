@@ -740,6 +740,24 @@ PYBIND11_MODULE(_helio, m) {
           py::arg("seed"), py::arg("first"), py::arg("count"), py::arg("p_uniform_ppm"), py::arg("out_ptr"),
           py::arg("stream") = 0)
       .def(
+          "generate_walk_device",
+          [](PyEngine& e, uint64_t seed, int64_t first, int64_t B, uintptr_t out, uintptr_t stream) {
+            e.eng->check(helio_gpu_generate_walk(e.eng->ctx(), seed, first, B, reinterpret_cast<int16_t*>(out),
+                                                 reinterpret_cast<void*>(stream)),
+                         "helio_gpu_generate_walk");
+          },
+          py::arg("seed"), py::arg("first"), py::arg("count"), py::arg("out_ptr"), py::arg("stream") = 0)
+      .def(
+          "generate_walk_host",
+          [](PyEngine& e, uint64_t seed, int64_t first, int64_t B) {
+            const int N = e.eng->num_nodes();
+            py::array_t<int16_t> out({(py::ssize_t)B, (py::ssize_t)N, (py::ssize_t)2});
+            e.eng->check(helio_gpu_generate_walk_host(e.eng->ctx(), seed, first, B, out.mutable_data()),
+                         "helio_gpu_generate_walk_host");
+            return out;
+          },
+          py::arg("seed"), py::arg("first"), py::arg("count"))
+      .def(
           "argmax_device",
           [](PyEngine& e, uintptr_t values, uintptr_t status, int64_t B, int64_t base, uintptr_t best, uintptr_t index,
              uintptr_t stream) {

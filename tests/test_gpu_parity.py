@@ -314,3 +314,26 @@ def test_score_best_host_matches_first_max():
             assert np.array_equal(bits(v2), bits(vv)) and np.array_equal(s2, ss)
         finally:
             e.mode = "parity"
+
+
+def test_walk_generator_device_matches_host_and_syn256_walk_parity():
+    import torch
+    d = clusters.CONFIGS["syn256-120l"]("float")
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    B = 2000
+    out = torch.empty((B, e.num_nodes, 2), dtype=torch.int16, device="cuda")
+    e.generate_walk_device(7, 100, B, out.data_ptr(), 0)
+    torch.cuda.synchronize()
+    rows = e.generate_walk_host(7, 100, B)
+    assert np.array_equal(out.cpu().numpy(), rows)
+    o = Oracle(d)
+    sub = rows[:150]
+    vo, so = o.score(sub)
+    assert (vo > 0).mean() > 0.5  # walks connect on the sparse topology
+    v, s = e.score(sub)
+    assert np.array_equal(s, so) and np.array_equal(bits(v), bits(vo))
+    e.mode = "score"
+    v, s = e.score(sub)
+    assert np.array_equal(s, so)
+    assert np.all(np.abs(v - vo) <= 1e-6 * np.maximum(1.0, np.abs(vo)))
