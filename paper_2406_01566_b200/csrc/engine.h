@@ -31,6 +31,8 @@ struct ClusterDev {
   const int2* in_list;        // (src node, link index)
   const unsigned long long* out_mask;  // [N] (N <= 64 only) node -> node link targets
   const int32_t* pair_link;            // [N*N] (N <= 64 only) link index or -1
+  const unsigned long long* less_cout; // [N] (N <= 64 only) nodes whose coord->node link comes first
+  const unsigned long long* less_cin;  // [N] (N <= 64 only) nodes whose node->coord link comes first
 };
 
 // Shared-memory slot layout of one graph (byte offsets from the slot base).

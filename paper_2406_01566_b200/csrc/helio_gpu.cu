@@ -1125,6 +1125,198 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
   return value;
 }
 
+// PARITY builder for N <= 64: the reference's exact graph (vertex numbering in
+// id order, edge order, per-vertex arc order) without scanning every link.
+// Valid interconnects come from the per-layer cover/start masks as in the
+// SCORE builder; an arc's position in its vertex's list is its link's rank
+// among that vertex's valid links in declaration order, counted pairwise
+// over the ~2-3 valid links (pair_link holds compacted = declaration-ordered
+// link indices) and, for coordinator links, with the less_cout / less_cin
+// masks.  Produces exactly what build_graph produces (same vin/unode/abeg/
+// to/rv/cap), so solve_fifo2 and built_value are unchanged.
+__device__ int build_graph_small(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
+                                 int partial, int lane, int& V, int& E) {
+  const int N = cd.N, L = cd.L;
+  unsigned long long* cover = reinterpret_cast<unsigned long long*>(g.cap);  // scratch until arcs are written
+  unsigned long long* start = cover + L;
+  unsigned long long* inmask = reinterpret_cast<unsigned long long*>(g.vs);  // [N] sources of valid links into node
+  int bad = INT_MAX;
+  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = __ldg(row32 + k);
+    const int s = (int16_t)(w & 0xffff);
+    const int e = (int16_t)(w >> 16);
+    g.ps[k] = (int16_t)s;
+    g.pe[k] = (int16_t)e;
+    g.vin[k] = -1;
+    if (e > s) {
+      int code = 0;
+      if (s < 0 || e > L) code = 2;
+      else if (e - s > __ldg(cd.kmax + k)) code = 3;
+      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
+    }
+  }
+  bad = __reduce_min_sync(FULL, bad);
+  if (bad != INT_MAX) return bad & 3;
+  if (2 * L > lay.A) return ST_OVERFLOW;
+  for (int l = lane; l < 2 * L; l += 32) cover[l] = 0ull;
+  for (int k = lane; k < N; k += 32) inmask[k] = 0ull;
+  __syncwarp();
+  // vertices in id order (:63-69)
+  int U = 0;
+  for (int r0 = 0; r0 < N; r0 += 32) {
+    const int r = r0 + lane;
+    int k = -1;
+    bool used = false;
+    if (r < N) {
+      k = __ldg(cd.lexnode + r);
+      used = g.pe[k] > g.ps[k];
+    }
+    const unsigned m = __ballot_sync(FULL, used);
+    if (used) {
+      const int idx = U + __popc(m & lanemask_lt());
+      g.vin[k] = (int16_t)(2 + 2 * idx);
+      g.unode[idx] = (int16_t)k;
+    }
+    U += __popc(m);
+  }
+  V = 2 + 2 * U;
+  for (int k = lane; k < N; k += 32) {
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    const unsigned long long bit = 1ull << k;
+    atomicOr(&start[s], bit);
+    for (int l = s; l < e; ++l) atomicOr(&cover[l], bit);
+  }
+  __syncwarp();
+  // successor sets T (registers; lanes own nodes lane, lane + 32) and the
+  // coordinator-link sets SRC (coord -> node valid) / SNK (node -> coord valid)
+  unsigned long long T[2] = {0ull, 0ull};
+  bool src_ok[2] = {false, false}, snk_ok[2] = {false, false};
+  int nedges = 0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= N) continue;
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    unsigned long long t = 0ull;
+    if (e < L) t = (partial ? cover[e] : start[e]) & __ldg(cd.out_mask + k);
+    T[q] = t;
+    for (unsigned long long m = t; m; m &= m - 1) atomicOr(&inmask[__ffsll(m) - 1], 1ull << k);
+    src_ok[q] = s == 0 && __ldg(cd.cout_link + k) >= 0;
+    snk_ok[q] = e == L && __ldg(cd.cin_link + k) >= 0;
+    nedges += 1 + __popcll(t) + (src_ok[q] ? 1 : 0) + (snk_ok[q] ? 1 : 0);
+  }
+  const unsigned long long SRC =
+      ((unsigned long long)__ballot_sync(FULL, src_ok[1]) << 32) | __ballot_sync(FULL, src_ok[0]);
+  const unsigned long long SNK =
+      ((unsigned long long)__ballot_sync(FULL, snk_ok[1]) << 32) | __ballot_sync(FULL, snk_ok[0]);
+  E = __reduce_add_sync(FULL, nedges);
+  if (V > lay.V || 2 * E > lay.A) return ST_OVERFLOW;
+  __syncwarp();
+  // degrees -> arc offsets
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= N || g.vin[k] < 0) continue;
+    const int vi = g.vin[k];
+    g.cur[vi] = (int16_t)(1 + __popcll(inmask[k]) + (src_ok[q] ? 1 : 0));
+    g.cur[vi + 1] = (int16_t)(1 + __popcll(T[q]) + (snk_ok[q] ? 1 : 0));
+  }
+  if (lane == 0) {
+    g.cur[0] = (int16_t)__popcll(SRC);
+    g.cur[1] = (int16_t)__popcll(SNK);
+  }
+  __syncwarp();
+  int run = 0;
+  for (int x0 = 0; x0 < V; x0 += 32) {
+    const int x = x0 + lane;
+    const int d = x < V ? g.cur[x] : 0;
+    int incl = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (x < V) g.abeg[x] = (int16_t)(run + incl - d);
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) g.abeg[V] = (int16_t)run;
+  __syncwarp();
+  // rank of link (src -> dst) among dst's valid incoming links, after the compute arc
+  auto in_rank = [&](int dst, int lidx) -> int {
+    int r = 1;
+    for (unsigned long long m = inmask[dst]; m; m &= m - 1) {
+      const int i = __ffsll(m) - 1;
+      r += __ldg(cd.pair_link + i * N + dst) < lidx;
+    }
+    const int lc = __ldg(cd.cout_link + dst);
+    if (g.ps[dst] == 0 && lc >= 0 && lc < lidx) ++r;
+    return r;
+  };
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= N || g.vin[k] < 0) continue;
+    const int s = g.ps[k], e = g.pe[k];
+    const int vi = g.vin[k], vo = vi + 1;
+    const int ai = g.abeg[vi], ao = g.abeg[vo];
+    // compute edge: forward first at in, reverse first at out (:140-145)
+    g.to[ai] = (int16_t)vo;
+    g.rv[ai] = (int16_t)ao;
+    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
+    g.to[ao] = (int16_t)vi;
+    g.rv[ao] = (int16_t)ai;
+    g.cap[ao] = 0.0;
+    const int lk = __ldg(cd.cin_link + k);
+    // node -> node links, ranked among this out-vertex's valid links
+    for (unsigned long long m = T[q]; m; m &= m - 1) {
+      const int j = __ffsll(m) - 1;
+      const int lidx = __ldg(cd.pair_link + k * N + j);
+      int ro = 1;
+      for (unsigned long long m2 = T[q]; m2; m2 &= m2 - 1)
+        ro += __ldg(cd.pair_link + k * N + (__ffsll(m2) - 1)) < lidx;
+      if (snk_ok[q] && lk < lidx) ++ro;
+      const int vj = g.vin[j];
+      const int fa = ao + ro;
+      const int ra = g.abeg[vj] + in_rank(j, lidx);
+      g.to[fa] = (int16_t)vj;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lidx);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    if (src_ok[q]) {  // coordinator -> k
+      const int lc = __ldg(cd.cout_link + k);
+      const int fa = g.abeg[0] + __popcll(SRC & __ldg(cd.less_cout + k));
+      const int ra = ai + in_rank(k, lc);
+      g.to[fa] = (int16_t)vi;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lc);
+      g.to[ra] = 0;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    if (snk_ok[q]) {  // k -> coordinator
+      int ro = 1;
+      for (unsigned long long m2 = T[q]; m2; m2 &= m2 - 1)
+        ro += __ldg(cd.pair_link + k * N + (__ffsll(m2) - 1)) < lk;
+      const int fa = ao + ro;
+      const int ra = g.abeg[1] + __popcll(SNK & __ldg(cd.less_cin + k));
+      g.to[fa] = 1;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lk);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+  }
+  __syncwarp();
+  return 0;
+}
+
 // Net flow into the sink in edge order (:222-227).  In built graphs the only
 // edges touching the sink are node->coordinator links, whose order in
 // g.edges equals the order of the sink's arcs.
@@ -1232,7 +1424,9 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     int st = MODE == HELIO_MODE_SCORE
                  ? (cd.out_mask ? build_graph_score_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
                                 : build_graph_score(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E))
-                                      : build_graph(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E);
+                 : (cd.less_cout && !fo.edges
+                        ? build_graph_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
+                        : build_graph(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E));
     if (st == ST_OVERFLOW) {
       if (!big) {
         if (lane == 0) ovf[atomicAdd(ovf_count, 1u)] = b;
@@ -1790,13 +1984,22 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   const bool small_n = N <= 64;
   std::vector<unsigned long long> outmask(small_n ? N : 1, 0ull);
   std::vector<int32_t> pairlink(small_n ? (size_t)N * N : 1, -1);
-  if (small_n)
+  // less_cout[b] = nodes whose coordinator->node link precedes b's (link order);
+  // less_cin[a] likewise for node->coordinator links (PARITY small builder)
+  std::vector<unsigned long long> less_cout(small_n ? N : 1, 0ull), less_cin(small_n ? N : 1, 0ull);
+  if (small_n) {
     for (int i = 0; i < Mv; ++i) {
       int a = (int)(pack[i] & 0xffffu) - 1, b = (int)(pack[i] >> 16) - 1;
       if (a < 0 || b < 0) continue;
       outmask[a] |= 1ull << b;
       pairlink[(size_t)a * N + b] = i;
     }
+    for (int x = 0; x < N; ++x)
+      for (int y = 0; y < N; ++y) {
+        if (cout[x] >= 0 && cout[y] >= 0 && cout[y] < cout[x]) less_cout[x] |= 1ull << y;
+        if (cinl[x] >= 0 && cinl[y] >= 0 && cinl[y] < cinl[x]) less_cin[x] |= 1ull << y;
+      }
+  }
   // one device allocation for all constants
   auto al = [](size_t x) { return (x + 15) / 16 * 16; };
   size_t o_kmax = 0;
@@ -1815,7 +2018,9 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   size_t o_ilist = o_olist + al(4 * olist.size());
   size_t o_omask = o_ilist + al(4 * ilist.size());
   size_t o_pair = o_omask + al(8 * outmask.size());
-  size_t o_wbeg = o_pair + al(4 * pairlink.size());
+  size_t o_lcout = o_pair + al(4 * pairlink.size());
+  size_t o_lcin = o_lcout + al(8 * less_cout.size());
+  size_t o_wbeg = o_lcin + al(8 * less_cin.size());
   size_t o_wlist = o_wbeg + al(4 * wbeg.size());
   size_t total = o_wlist + al(4 * wlist.size());
   std::vector<char> hbuf(total, 0);
@@ -1837,6 +2042,8 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   std::memcpy(hbuf.data() + o_ilist, ilist.data(), 4 * ilist.size());
   std::memcpy(hbuf.data() + o_omask, outmask.data(), 8 * outmask.size());
   std::memcpy(hbuf.data() + o_pair, pairlink.data(), 4 * pairlink.size());
+  std::memcpy(hbuf.data() + o_lcout, less_cout.data(), 8 * less_cout.size());
+  std::memcpy(hbuf.data() + o_lcin, less_cin.data(), 8 * less_cin.size());
   std::memcpy(hbuf.data() + o_wbeg, wbeg.data(), 4 * wbeg.size());
   std::memcpy(hbuf.data() + o_wlist, wlist.data(), 4 * wlist.size());
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1868,6 +2075,8 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   ctx->cd.in_list = reinterpret_cast<const int2*>(base + o_ilist);
   ctx->cd.out_mask = small_n ? reinterpret_cast<const unsigned long long*>(base + o_omask) : nullptr;
   ctx->cd.pair_link = small_n ? reinterpret_cast<const int32_t*>(base + o_pair) : nullptr;
+  ctx->cd.less_cout = small_n ? reinterpret_cast<const unsigned long long*>(base + o_lcout) : nullptr;
+  ctx->cd.less_cin = small_n ? reinterpret_cast<const unsigned long long*>(base + o_lcin) : nullptr;
   ctx->d_walk_beg = reinterpret_cast<const int32_t*>(base + o_wbeg);
   ctx->d_walk_list = reinterpret_cast<const int32_t*>(base + o_wlist);
   ctx->h_walk_beg = wbeg;
