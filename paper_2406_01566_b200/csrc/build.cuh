@@ -1,0 +1,691 @@
+// build.cuh — K1: placement row -> the reference's flow network in a warp's
+// shared-memory slot (PARITY builders keep the reference's vertex/edge/arc
+// order; SCORE builders only its graph).
+#pragma once
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// K1: build the reference's FlowGraph for one placement row into the slot.
+// Vertex numbering (flow_graph.cpp:63-69): source 0, sink 1, then (in, out)
+// pairs of the used nodes in byte-lexicographic id order.  Edge order: compute
+// edges in that order (:71-84), then valid links in declaration order
+// (:86-134).  Arc order per vertex = edge order (:140-145), which for these
+// graphs is: the compute arc first, then link arcs in link order; so the
+// position of a link's arc at a vertex is 1 (0 at source/sink) + the number of
+// earlier valid links touching that vertex — a running counter per vertex,
+// advanced per 32-link chunk with __match_any_sync.
+//
+// Returns status (0 ok, 1-3 validation, ST_OVERFLOW), V and E.
+
+struct LinkEval {
+  bool valid;
+  int u, v;
+};
+
+__device__ __forceinline__ LinkEval eval_link(const ClusterDev& cd, const Gs& g, int l, int partial) {
+  LinkEval r{false, 0, 0};
+  const uint32_t pk = __ldg(cd.link_pack + l);
+  const int a = (int)(pk & 0xffffu) - 1;
+  const int bb = (int)(pk >> 16) - 1;
+  if (a < 0) {  // coordinator -> bb (:89-101)
+    const int vb = g.vin[bb];
+    if (vb >= 0 && g.ps[bb] == 0) {
+      r.valid = true;
+      r.u = 0;
+      r.v = vb;
+    }
+  } else if (bb < 0) {  // a -> coordinator (:102-114)
+    const int va = g.vin[a];
+    if (va >= 0 && g.pe[a] == cd.L) {
+      r.valid = true;
+      r.u = va + 1;
+      r.v = 1;
+    }
+  } else {  // a -> bb (:115-133)
+    const int va = g.vin[a], vb = g.vin[bb];
+    if (va >= 0 && vb >= 0) {
+      const int aend = g.pe[a], bs = g.ps[bb], be = g.pe[bb];
+      const bool ok = partial ? (bs <= aend && aend < be) : (aend == bs);
+      if (ok) {
+        r.valid = true;
+        r.u = va + 1;
+        r.v = vb;
+      }
+    }
+  }
+  return r;
+}
+
+__device__ int build_graph(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
+                           int partial, int lane, int& V, int& E) {
+  const int N = cd.N, L = cd.L;
+  // placement + validation in id order (:52-61): first failing node in lex order
+  int bad = INT_MAX;
+  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = __ldg(row32 + k);
+    const int s = (int16_t)(w & 0xffff);
+    const int e = (int16_t)(w >> 16);
+    g.ps[k] = (int16_t)s;
+    g.pe[k] = (int16_t)e;
+    g.vin[k] = -1;
+    if (e > s) {
+      int code = 0;
+      if (s < 0 || e > L) code = 2;
+      else if (e - s > __ldg(cd.kmax + k)) code = 3;
+      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
+    }
+  }
+  bad = __reduce_min_sync(FULL, bad);
+  if (bad != INT_MAX) return bad & 3;
+  __syncwarp();
+  // vertices in lex order (:63-69)
+  int U = 0;
+  for (int r0 = 0; r0 < N; r0 += 32) {
+    const int r = r0 + lane;
+    int k = -1;
+    bool used = false;
+    if (r < N) {
+      k = __ldg(cd.lexnode + r);
+      used = g.pe[k] > g.ps[k];
+    }
+    const unsigned m = __ballot_sync(FULL, used);
+    if (used) {
+      const int idx = U + __popc(m & lanemask_lt());
+      g.vin[k] = (int16_t)(2 + 2 * idx);
+      g.unode[idx] = (int16_t)k;
+    }
+    U += __popc(m);
+  }
+  V = 2 + 2 * U;
+  // degree count: compute arc (1 per used vertex) + link arcs
+  for (int x = lane; x < V; x += 32) g.cur[x] = x >= 2 ? 1 : 0;
+  __syncwarp();
+  int nvalid = 0;
+  for (int l0 = 0; l0 < cd.Mv; l0 += 32) {
+    const int l = l0 + lane;
+    LinkEval le{false, 0, 0};
+    if (l < cd.Mv) le = eval_link(cd, g, l, partial);
+    const unsigned vm = __ballot_sync(FULL, le.valid);
+    if (vm == 0u) continue;
+    nvalid += __popc(vm);
+    unsigned pu = 0, pv = 0;
+    int cu = 0, cv = 0;
+    if (le.valid) {
+      pu = __match_any_sync(vm, le.u);
+      pv = __match_any_sync(vm, le.v);
+      cu = g.cur[le.u];
+      cv = g.cur[le.v];
+    }
+    __syncwarp();
+    if (le.valid) {
+      const unsigned lt = lanemask_lt();
+      if ((pu & lt) == 0u) g.cur[le.u] = (int16_t)(cu + __popc(pu));
+      if ((pv & lt) == 0u) g.cur[le.v] = (int16_t)(cv + __popc(pv));
+    }
+    __syncwarp();
+  }
+  E = U + nvalid;
+  if (V > lay.V || 2 * E > lay.A) return ST_OVERFLOW;
+  // arc offsets: exclusive scan of degrees
+  int run = 0;
+  for (int x0 = 0; x0 < V; x0 += 32) {
+    const int x = x0 + lane;
+    const int d = x < V ? g.cur[x] : 0;
+    int incl = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (x < V) g.abeg[x] = (int16_t)(run + incl - d);
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) g.abeg[V] = (int16_t)run;
+  __syncwarp();
+  // compute arcs (edge j = in_j -> out_j, cap compute_edge_capacity)
+  for (int j = lane; j < U; j += 32) {
+    const int k = g.unode[j];
+    const int vi = 2 + 2 * j, vo = vi + 1;
+    const int ai = g.abeg[vi], ao = g.abeg[vo];
+    g.to[ai] = (int16_t)vo;
+    g.rv[ai] = (int16_t)ao;
+    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (g.pe[k] - g.ps[k]) - 1);
+    g.to[ao] = (int16_t)vi;
+    g.rv[ao] = (int16_t)ai;
+    g.cap[ao] = 0.0;
+  }
+  for (int x = lane; x < V; x += 32) g.cur[x] = x >= 2 ? 1 : 0;
+  __syncwarp();
+  // link arcs at their ranked positions
+  for (int l0 = 0; l0 < cd.Mv; l0 += 32) {
+    const int l = l0 + lane;
+    LinkEval le{false, 0, 0};
+    if (l < cd.Mv) le = eval_link(cd, g, l, partial);
+    const unsigned vm = __ballot_sync(FULL, le.valid);
+    if (vm == 0u) continue;
+    unsigned pu = 0, pv = 0;
+    int cu = 0, cv = 0;
+    if (le.valid) {
+      pu = __match_any_sync(vm, le.u);
+      pv = __match_any_sync(vm, le.v);
+      cu = g.cur[le.u];
+      cv = g.cur[le.v];
+    }
+    __syncwarp();
+    if (le.valid) {
+      const unsigned lt = lanemask_lt();
+      const int fa = g.abeg[le.u] + cu + __popc(pu & lt);
+      const int ra = g.abeg[le.v] + cv + __popc(pv & lt);
+      g.to[fa] = (int16_t)le.v;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + l);
+      g.to[ra] = (int16_t)le.u;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+      if ((pu & lt) == 0u) g.cur[le.u] = (int16_t)(cu + __popc(pu));
+      if ((pv & lt) == 0u) g.cur[le.v] = (int16_t)(cv + __popc(pv));
+    }
+    __syncwarp();
+  }
+  return 0;
+}
+
+// SCORE-mode builder.  Same graph as build_graph up to vertex numbering and
+// arc order, which the value does not depend on: node k owns vertices
+// in = 2 + 2k, out = 3 + 2k (unused nodes keep no arcs), and each lane walks
+// its node's precomputed out-/in-link lists instead of scanning every link
+// of the cluster.  Validation and status codes are shared with build_graph.
+__device__ __forceinline__ bool edge_ok(int aend, int bs, int be, int partial) {
+  return partial ? (bs <= aend && aend < be) : (aend == bs);
+}
+
+__device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
+                                 int partial, int lane, int& V, int& E) {
+  const int N = cd.N, L = cd.L;
+  int bad = INT_MAX;
+  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = __ldg(row32 + k);
+    const int s = (int16_t)(w & 0xffff);
+    const int e = (int16_t)(w >> 16);
+    g.ps[k] = (int16_t)s;
+    g.pe[k] = (int16_t)e;
+    if (e > s) {
+      int code = 0;
+      if (s < 0 || e > L) code = 2;
+      else if (e - s > __ldg(cd.kmax + k)) code = 3;
+      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
+    }
+  }
+  bad = __reduce_min_sync(FULL, bad);
+  if (bad != INT_MAX) return bad & 3;
+  V = 2 + 2 * N;
+  if (V > lay.V) return ST_OVERFLOW;
+  __syncwarp();
+  // degrees: in_k = compute + valid in-links + source arc; out_k = compute +
+  // valid out-links + sink arc.
+  int nedges = 0, dsrc = 0, dsink = 0;
+  int* fill = reinterpret_cast<int*>(g.ex);  // int counters per vertex during the build
+  for (int k = lane; k < N; k += 32) {
+    const int s = g.ps[k], e = g.pe[k];
+    int din = 0, dout = 0;
+    if (e > s) {
+      din = 1;
+      dout = 1;
+      ++nedges;
+      for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
+        const int j = __ldg(&cd.out_list[p].x);
+        const int sj = g.ps[j], ej = g.pe[j];
+        if (ej > sj && edge_ok(e, sj, ej, partial)) ++dout;
+      }
+      for (int p = __ldg(cd.in_beg + k), pe_ = __ldg(cd.in_beg + k + 1); p < pe_; ++p) {
+        const int i = __ldg(&cd.in_list[p].x);
+        const int si = g.ps[i], ei = g.pe[i];
+        if (ei > si && edge_ok(ei, s, e, partial)) ++din;
+      }
+      nedges += dout - 1;  // each link edge counted once, at its source
+      if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
+        ++din;
+        ++dsrc;
+        ++nedges;
+      }
+      if (e == L && __ldg(cd.cin_link + k) >= 0) {
+        ++dout;
+        ++dsink;
+        ++nedges;
+      }
+    }
+    g.cur[2 + 2 * k] = (int16_t)din;
+    g.cur[3 + 2 * k] = (int16_t)dout;
+  }
+  nedges = __reduce_add_sync(FULL, nedges);
+  dsrc = __reduce_add_sync(FULL, dsrc);
+  dsink = __reduce_add_sync(FULL, dsink);
+  E = nedges;
+  if (2 * E > lay.A) return ST_OVERFLOW;
+  if (lane == 0) {
+    g.cur[0] = (int16_t)dsrc;
+    g.cur[1] = (int16_t)dsink;
+  }
+  __syncwarp();
+  int run = 0;
+  for (int x0 = 0; x0 < V; x0 += 32) {
+    const int x = x0 + lane;
+    const int d = x < V ? g.cur[x] : 0;
+    int incl = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (x < V) {
+      g.abeg[x] = (int16_t)(run + incl - d);
+      fill[x] = 0;
+    }
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) g.abeg[V] = (int16_t)run;
+  __syncwarp();
+  // arcs: each lane places its node's compute pair and every edge it
+  // sources; the paired reverse arc takes the next free slot at its head.
+  for (int k = lane; k < N; k += 32) {
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    const int vi = 2 + 2 * k, vo = vi + 1;
+    const int ai = g.abeg[vi] + atomicAdd(&fill[vi], 1);
+    const int ao = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+    g.to[ai] = (int16_t)vo;
+    g.rv[ai] = (int16_t)ao;
+    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
+    g.to[ao] = (int16_t)vi;
+    g.rv[ao] = (int16_t)ai;
+    g.cap[ao] = 0.0;
+    for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
+      const int2 jl = __ldg(&cd.out_list[p]);
+      const int sj = g.ps[jl.x], ej = g.pe[jl.x];
+      if (!(ej > sj && edge_ok(e, sj, ej, partial))) continue;
+      const int vj = 2 + 2 * jl.x;
+      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+      const int ra = g.abeg[vj] + atomicAdd(&fill[vj], 1);
+      g.to[fa] = (int16_t)vj;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + jl.y);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    const int lc = __ldg(cd.cout_link + k);
+    if (s == 0 && lc >= 0) {
+      const int fa = g.abeg[0] + atomicAdd(&fill[0], 1);
+      const int ra = g.abeg[vi] + atomicAdd(&fill[vi], 1);
+      g.to[fa] = (int16_t)vi;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lc);
+      g.to[ra] = 0;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    const int lk = __ldg(cd.cin_link + k);
+    if (e == L && lk >= 0) {
+      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+      const int ra = g.abeg[1] + atomicAdd(&fill[1], 1);
+      g.to[fa] = 1;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lk);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+  }
+  __syncwarp();
+  return 0;
+}
+
+// SCORE builder for N <= 64: node sets are 64-bit words.  cover[l] = nodes
+// whose interval contains layer l, start[l] = nodes starting at l.  Node i's
+// valid successors are (partial ? cover[e_i] : start[e_i]) & out_mask[i]
+// (flow_graph.cpp:121: s_j <= e_i < e_j, resp. e_i == s_j), so each node
+// visits only its ~2-3 actual edges instead of every link of the cluster.
+__device__ int build_graph_score_small(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
+                                       int partial, int lane, int& V, int& E) {
+  const int N = cd.N, L = cd.L;
+  unsigned long long* cover = reinterpret_cast<unsigned long long*>(g.cap);  // [L] then start[L]; scratch
+  unsigned long long* start = cover + L;
+  int bad = INT_MAX;
+  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = __ldg(row32 + k);
+    const int s = (int16_t)(w & 0xffff);
+    const int e = (int16_t)(w >> 16);
+    g.ps[k] = (int16_t)s;
+    g.pe[k] = (int16_t)e;
+    if (e > s) {
+      int code = 0;
+      if (s < 0 || e > L) code = 2;
+      else if (e - s > __ldg(cd.kmax + k)) code = 3;
+      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
+    }
+  }
+  bad = __reduce_min_sync(FULL, bad);
+  if (bad != INT_MAX) return bad & 3;
+  V = 2 + 2 * N;
+  if (V > lay.V || 2 * L > lay.A) return ST_OVERFLOW;  // cover/start scratch lives in cap[]
+  for (int l = lane; l < 2 * L; l += 32) cover[l] = 0ull;
+  __syncwarp();
+  for (int k = lane; k < N; k += 32) {
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    const unsigned long long bit = 1ull << k;
+    atomicOr(&start[s], bit);
+    for (int l = s; l < e; ++l) atomicOr(&cover[l], bit);
+  }
+  __syncwarp();
+  // successor sets (kept in registers; lanes own nodes lane, lane+32)
+  unsigned long long T[2] = {0ull, 0ull};
+  int* fill = reinterpret_cast<int*>(g.vs);
+  for (int x = lane; x < V; x += 32) fill[x] = 0;
+  __syncwarp();
+  int nedges = 0, dsrc = 0, dsink = 0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= N) continue;
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    unsigned long long t = 0ull;
+    if (e < L) t = (partial ? cover[e] : start[e]) & __ldg(cd.out_mask + k);
+    T[q] = t;
+    const int nt = __popcll(t);
+    nedges += 1 + nt;
+    int dout = 1 + nt, din = 1;
+    if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
+      ++din;
+      ++dsrc;
+      ++nedges;
+    }
+    if (e == L && __ldg(cd.cin_link + k) >= 0) {
+      ++dout;
+      ++dsink;
+      ++nedges;
+    }
+    atomicAdd(&fill[2 + 2 * k], din);
+    atomicAdd(&fill[3 + 2 * k], dout);
+    for (unsigned long long m = t; m; m &= m - 1) atomicAdd(&fill[2 + 2 * (__ffsll(m) - 1)], 1);  // in_j
+  }
+  nedges = __reduce_add_sync(FULL, nedges);
+  dsrc = __reduce_add_sync(FULL, dsrc);
+  dsink = __reduce_add_sync(FULL, dsink);
+  E = nedges;
+  if (2 * E > lay.A) return ST_OVERFLOW;
+  __syncwarp();
+  if (lane == 0) {
+    fill[0] = dsrc;
+    fill[1] = dsink;
+  }
+  __syncwarp();
+  int run = 0;
+  for (int x0 = 0; x0 < V; x0 += 32) {
+    const int x = x0 + lane;
+    const int d = x < V ? fill[x] : 0;
+    int incl = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (x < V) g.abeg[x] = (int16_t)(run + incl - d);
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) g.abeg[V] = (int16_t)run;
+  __syncwarp();
+  for (int x = lane; x < V; x += 32) fill[x] = 0;
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= N) continue;
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    const int vi = 2 + 2 * k, vo = vi + 1;
+    const int ai = g.abeg[vi] + atomicAdd(&fill[vi], 1);
+    const int ao = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+    g.to[ai] = (int16_t)vo;
+    g.rv[ai] = (int16_t)ao;
+    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
+    g.to[ao] = (int16_t)vi;
+    g.rv[ao] = (int16_t)ai;
+    g.cap[ao] = 0.0;
+    for (unsigned long long m = T[q]; m; m &= m - 1) {
+      const int j = __ffsll(m) - 1;
+      const int vj = 2 + 2 * j;
+      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+      const int ra = g.abeg[vj] + atomicAdd(&fill[vj], 1);
+      g.to[fa] = (int16_t)vj;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + __ldg(cd.pair_link + k * N + j));
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    const int lc = __ldg(cd.cout_link + k);
+    if (s == 0 && lc >= 0) {
+      const int fa = g.abeg[0] + atomicAdd(&fill[0], 1);
+      const int ra = g.abeg[vi] + atomicAdd(&fill[vi], 1);
+      g.to[fa] = (int16_t)vi;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lc);
+      g.to[ra] = 0;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    const int lk = __ldg(cd.cin_link + k);
+    if (e == L && lk >= 0) {
+      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+      const int ra = g.abeg[1] + atomicAdd(&fill[1], 1);
+      g.to[fa] = 1;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lk);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+  }
+  __syncwarp();
+  return 0;
+}
+
+// PARITY builder for N <= 64: the reference's exact graph (vertex numbering in
+// id order, edge order, per-vertex arc order) without scanning every link.
+// Valid interconnects come from the per-layer cover/start masks as in the
+// SCORE builder; an arc's position in its vertex's list is its link's rank
+// among that vertex's valid links in declaration order, counted pairwise
+// over the ~2-3 valid links (pair_link holds compacted = declaration-ordered
+// link indices) and, for coordinator links, with the less_cout / less_cin
+// masks.  Produces exactly what build_graph produces (same vin/unode/abeg/
+// to/rv/cap), so solve_fifo2 and built_value are unchanged.
+__device__ int build_graph_small(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
+                                 int partial, int lane, int& V, int& E) {
+  const int N = cd.N, L = cd.L;
+  unsigned long long* cover = reinterpret_cast<unsigned long long*>(g.cap);  // scratch until arcs are written
+  unsigned long long* start = cover + L;
+  unsigned long long* inmask = reinterpret_cast<unsigned long long*>(g.vs);  // [N] sources of valid links into node
+  int bad = INT_MAX;
+  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = __ldg(row32 + k);
+    const int s = (int16_t)(w & 0xffff);
+    const int e = (int16_t)(w >> 16);
+    g.ps[k] = (int16_t)s;
+    g.pe[k] = (int16_t)e;
+    g.vin[k] = -1;
+    if (e > s) {
+      int code = 0;
+      if (s < 0 || e > L) code = 2;
+      else if (e - s > __ldg(cd.kmax + k)) code = 3;
+      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
+    }
+  }
+  bad = __reduce_min_sync(FULL, bad);
+  if (bad != INT_MAX) return bad & 3;
+  if (2 * L > lay.A) return ST_OVERFLOW;
+  for (int l = lane; l < 2 * L; l += 32) cover[l] = 0ull;
+  for (int k = lane; k < N; k += 32) inmask[k] = 0ull;
+  __syncwarp();
+  // vertices in id order (:63-69)
+  int U = 0;
+  for (int r0 = 0; r0 < N; r0 += 32) {
+    const int r = r0 + lane;
+    int k = -1;
+    bool used = false;
+    if (r < N) {
+      k = __ldg(cd.lexnode + r);
+      used = g.pe[k] > g.ps[k];
+    }
+    const unsigned m = __ballot_sync(FULL, used);
+    if (used) {
+      const int idx = U + __popc(m & lanemask_lt());
+      g.vin[k] = (int16_t)(2 + 2 * idx);
+      g.unode[idx] = (int16_t)k;
+    }
+    U += __popc(m);
+  }
+  V = 2 + 2 * U;
+  for (int k = lane; k < N; k += 32) {
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    const unsigned long long bit = 1ull << k;
+    atomicOr(&start[s], bit);
+    for (int l = s; l < e; ++l) atomicOr(&cover[l], bit);
+  }
+  __syncwarp();
+  // successor sets T (registers; lanes own nodes lane, lane + 32) and the
+  // coordinator-link sets SRC (coord -> node valid) / SNK (node -> coord valid)
+  unsigned long long T[2] = {0ull, 0ull};
+  bool src_ok[2] = {false, false}, snk_ok[2] = {false, false};
+  int nedges = 0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= N) continue;
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    unsigned long long t = 0ull;
+    if (e < L) t = (partial ? cover[e] : start[e]) & __ldg(cd.out_mask + k);
+    T[q] = t;
+    for (unsigned long long m = t; m; m &= m - 1) atomicOr(&inmask[__ffsll(m) - 1], 1ull << k);
+    src_ok[q] = s == 0 && __ldg(cd.cout_link + k) >= 0;
+    snk_ok[q] = e == L && __ldg(cd.cin_link + k) >= 0;
+    nedges += 1 + __popcll(t) + (src_ok[q] ? 1 : 0) + (snk_ok[q] ? 1 : 0);
+  }
+  const unsigned long long SRC =
+      ((unsigned long long)__ballot_sync(FULL, src_ok[1]) << 32) | __ballot_sync(FULL, src_ok[0]);
+  const unsigned long long SNK =
+      ((unsigned long long)__ballot_sync(FULL, snk_ok[1]) << 32) | __ballot_sync(FULL, snk_ok[0]);
+  E = __reduce_add_sync(FULL, nedges);
+  if (V > lay.V || 2 * E > lay.A) return ST_OVERFLOW;
+  __syncwarp();
+  // degrees -> arc offsets
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= N || g.vin[k] < 0) continue;
+    const int vi = g.vin[k];
+    g.cur[vi] = (int16_t)(1 + __popcll(inmask[k]) + (src_ok[q] ? 1 : 0));
+    g.cur[vi + 1] = (int16_t)(1 + __popcll(T[q]) + (snk_ok[q] ? 1 : 0));
+  }
+  if (lane == 0) {
+    g.cur[0] = (int16_t)__popcll(SRC);
+    g.cur[1] = (int16_t)__popcll(SNK);
+  }
+  __syncwarp();
+  int run = 0;
+  for (int x0 = 0; x0 < V; x0 += 32) {
+    const int x = x0 + lane;
+    const int d = x < V ? g.cur[x] : 0;
+    int incl = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (x < V) g.abeg[x] = (int16_t)(run + incl - d);
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) g.abeg[V] = (int16_t)run;
+  __syncwarp();
+  // rank of link (src -> dst) among dst's valid incoming links, after the compute arc
+  auto in_rank = [&](int dst, int lidx) -> int {
+    int r = 1;
+    for (unsigned long long m = inmask[dst]; m; m &= m - 1) {
+      const int i = __ffsll(m) - 1;
+      r += __ldg(cd.pair_link + i * N + dst) < lidx;
+    }
+    const int lc = __ldg(cd.cout_link + dst);
+    if (g.ps[dst] == 0 && lc >= 0 && lc < lidx) ++r;
+    return r;
+  };
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int k = lane + 32 * q;
+    if (k >= N || g.vin[k] < 0) continue;
+    const int s = g.ps[k], e = g.pe[k];
+    const int vi = g.vin[k], vo = vi + 1;
+    const int ai = g.abeg[vi], ao = g.abeg[vo];
+    // compute edge: forward first at in, reverse first at out (:140-145)
+    g.to[ai] = (int16_t)vo;
+    g.rv[ai] = (int16_t)ao;
+    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
+    g.to[ao] = (int16_t)vi;
+    g.rv[ao] = (int16_t)ai;
+    g.cap[ao] = 0.0;
+    const int lk = __ldg(cd.cin_link + k);
+    // node -> node links, ranked among this out-vertex's valid links
+    for (unsigned long long m = T[q]; m; m &= m - 1) {
+      const int j = __ffsll(m) - 1;
+      const int lidx = __ldg(cd.pair_link + k * N + j);
+      int ro = 1;
+      for (unsigned long long m2 = T[q]; m2; m2 &= m2 - 1)
+        ro += __ldg(cd.pair_link + k * N + (__ffsll(m2) - 1)) < lidx;
+      if (snk_ok[q] && lk < lidx) ++ro;
+      const int vj = g.vin[j];
+      const int fa = ao + ro;
+      const int ra = g.abeg[vj] + in_rank(j, lidx);
+      g.to[fa] = (int16_t)vj;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lidx);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    if (src_ok[q]) {  // coordinator -> k
+      const int lc = __ldg(cd.cout_link + k);
+      const int fa = g.abeg[0] + __popcll(SRC & __ldg(cd.less_cout + k));
+      const int ra = ai + in_rank(k, lc);
+      g.to[fa] = (int16_t)vi;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lc);
+      g.to[ra] = 0;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    if (snk_ok[q]) {  // k -> coordinator
+      int ro = 1;
+      for (unsigned long long m2 = T[q]; m2; m2 &= m2 - 1)
+        ro += __ldg(cd.pair_link + k * N + (__ffsll(m2) - 1)) < lk;
+      const int fa = ao + ro;
+      const int ra = g.abeg[1] + __popcll(SNK & __ldg(cd.less_cin + k));
+      g.to[fa] = 1;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lk);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+  }
+  __syncwarp();
+  return 0;
+}
+
+}  // namespace

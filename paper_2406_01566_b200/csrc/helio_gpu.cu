@@ -1,26 +1,26 @@
-// helio_gpu.cu — B200 (sm_100a) engine behind include/helio_gpu.h.
+// helio_gpu.cu — B200 (sm_100a) engine behind include/helio_gpu.h: kernels,
+// K0 cluster compiler, launchers and the C ABI entry points.
 //
-// Kernels (SIMT; the path is FP64 min/add/compare graph work — no tensor
+// Device code is split by role (all included into this translation unit):
+//   device_common.cuh  shared-memory slot layout, per-warp views, warp helpers
+//   build.cuh          K1: placement row -> flow network in shared memory
+//   solve_parity.cuh   K2 PARITY: bit-exact FIFO preflow-push replay + read-out
+//   solve_score.cuh    K2 SCORE: value-only Edmonds-Karp (bitset / queue BFS)
+//
+// Kernels here (SIMT; the path is FP64 min/add/compare graph work — no tensor
 // cores):
-//
-//   K1+K2  score_kernel   placement rows -> split-node flow network in shared
-//                         memory -> FIFO preflow-push max-flow -> value.
-//                         One warp per graph, persistent CTAs pulling work from
-//                         an atomic counter.  PARITY semantics: the discharge
-//                         sequence of src/flow_graph.cpp:138-229 is replayed
-//                         exactly (ballot = the sequential admissible-arc
-//                         scan), so values AND per-edge flows are bit-identical
-//                         to the reference's doubles.  Graphs whose arcs exceed
-//                         the small slot are queued and finished by the same
-//                         kernel launched with one warp per CTA and a large slot.
-//   raw    raw_kernel     max_flow on caller-supplied raw graphs (AC1 style).
-//   K4     argmax         (max value, min index) reduction (enumerate.hpp:59).
-//   gen    gen_kernel     counter-based candidate generator (gen.h).
-//   K3     route kernels  IWRR routing (scheduler.cpp:28-190), see route section.
+//   score_kernel<MODE>  placement rows -> graph -> max-flow value, one warp per
+//                       graph, persistent CTAs pulling work from an atomic
+//                       counter; graphs whose arcs exceed the small slot are
+//                       queued and finished by the same kernel launched with one
+//                       warp per CTA and a large slot.
+//   raw_kernel          max_flow on caller-supplied raw graphs (AC1 style).
+//   argmax_*            (max value, min index) reduction (enumerate.hpp:59).
+//   gen_kernel / gen_walk_kernel   counter-based candidate generators (gen.h).
+// route.cu holds K3 (IWRR routing), search.cu the exhaustive search.
 //
 // Everything is compiled with -fmad=false; the only FP operations on the path
-// are min / + / - / compare on doubles (flow) and the iwrr_weights scaling,
-// exactly the reference's operations in the reference's order.
+// are min / + / - / compare on doubles, in the reference's order.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -43,1357 +43,12 @@ using namespace helio_engine;
 #define FULL 0xffffffffu
 #define ST_OVERFLOW 100  // internal: arcs exceed the small slot
 
+#include "device_common.cuh"
+#include "build.cuh"
+#include "solve_parity.cuh"
+#include "solve_score.cuh"
+
 namespace {
-
-Layout make_layout(int V, int A, int N, int M) {
-  Layout l;
-  l.V = V; l.A = A; l.N = N; l.M = M;
-  int o = 0;
-  auto take = [&](int bytes, int align) {
-    o = (o + align - 1) / align * align;
-    int r = o;
-    o += bytes;
-    return r;
-  };
-  l.o_cap = take(8 * A, 16);
-  // 16 B per vertex: PARITY's packed VState; SCORE reuses the bytes as a
-  // double array (bottleneck) followed by an int16 array (BFS parent arc).
-  l.o_vs = take(16 * V, 16);
-  l.o_ex = l.o_vs;
-  l.o_h = l.o_vs + 8 * V;
-  l.o_to = take(2 * A, 2);
-  l.o_rv = take(2 * A, 2);
-  l.o_abeg = take(2 * (V + 1), 2);
-  l.o_cur = take(2 * V, 2);
-  l.o_q = take(2 * V, 2);
-  l.o_cnt = take(2 * (2 * V + 1), 2);
-  l.o_ps = take(2 * N, 4);
-  l.o_pe = take(2 * N, 2);
-  l.o_vin = take(2 * N, 2);
-  l.o_unode = take(2 * N, 2);
-  l.o_efwd = take(2 * M, 2);
-  l.o_inq = take(V, 1);
-  l.bytes = (o + 15) / 16 * 16;
-  return l;
-}
-
-// PARITY per-vertex solver state, one 16-byte shared-memory record so a
-// discharge loads it with a single LDS.128.
-struct __align__(16) VState {
-  double ex;     // excess
-  int16_t h;     // height
-  int16_t cur;   // current-arc index (relative)
-  int16_t b;     // first arc
-  int16_t deg;   // arc count
-};
-
-// Per-warp view of a slot.
-struct Gs {
-  VState* vs;
-  double* cap;
-  double* ex;
-  int16_t* to;
-  int16_t* rv;
-  int16_t* abeg;
-  int16_t* h;
-  int16_t* cur;
-  int16_t* q;
-  int16_t* cnt;
-  uint8_t* inq;
-  int16_t* ps;
-  int16_t* pe;
-  int16_t* vin;
-  int16_t* unode;
-  int16_t* efwd;
-};
-
-__device__ __forceinline__ Gs slot_view(char* base, const Layout& l) {
-  Gs g;
-  g.vs = reinterpret_cast<VState*>(base + l.o_vs);
-  g.cap = reinterpret_cast<double*>(base + l.o_cap);
-  g.ex = reinterpret_cast<double*>(base + l.o_ex);
-  g.to = reinterpret_cast<int16_t*>(base + l.o_to);
-  g.rv = reinterpret_cast<int16_t*>(base + l.o_rv);
-  g.abeg = reinterpret_cast<int16_t*>(base + l.o_abeg);
-  g.h = reinterpret_cast<int16_t*>(base + l.o_h);
-  g.cur = reinterpret_cast<int16_t*>(base + l.o_cur);
-  g.q = reinterpret_cast<int16_t*>(base + l.o_q);
-  g.cnt = reinterpret_cast<int16_t*>(base + l.o_cnt);
-  g.inq = reinterpret_cast<uint8_t*>(base + l.o_inq);
-  g.ps = reinterpret_cast<int16_t*>(base + l.o_ps);
-  g.pe = reinterpret_cast<int16_t*>(base + l.o_pe);
-  g.vin = reinterpret_cast<int16_t*>(base + l.o_vin);
-  g.unode = reinterpret_cast<int16_t*>(base + l.o_unode);
-  g.efwd = reinterpret_cast<int16_t*>(base + l.o_efwd);
-  return g;
-}
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-  unsigned m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
-// std::min(a, b) == (b < a) ? b : a
-__device__ __forceinline__ double ref_min(double a, double b) { return b < a ? b : a; }
-
-// ---------------------------------------------------------------------------
-// FIFO preflow-push with the gap heuristic, warp-cooperative replay of
-// max_flow (flow_graph.cpp:147-208).  Arcs for vertex x are
-// [abeg[x], abeg[x+1]) in the reference's adjacency order; rv[] is the global
-// index of the paired arc.  On return cap[] holds residual capacities.
-//
-// Replay argument: while vertex u discharges, nothing but u's own pushes
-// changes state, and a push either drains u (loop ends, current stays on the
-// arc) or saturates the arc to exactly 0.0 (the reference then re-tests it,
-// fails, and advances).  So "first admissible arc at index >= current" — one
-// ballot over 32 arcs — is exactly the arc the sequential scan reaches.
-// Relabel is a warp min-reduce (:183-186); the gap sweep (:190-198) only moves
-// integer counts, so it is done lane-parallel.  Queue order is preserved
-// because enqueues happen in push order.
-// (implemented by solve_fifo2 below)
-
-// ---------------------------------------------------------------------------
-// SCORE mode: value-only Edmonds-Karp (shortest augmenting paths), one warp
-// per graph — see solve_ek_batched below.  Exact on integer capacities (every
-// intermediate is an integer-valued double); on float capacities the value
-// differs from the reference's FIFO preflow-push only by rounding (north_star
-// tolerance 1e-6 relative; tests assert it).  Slot reuse: h = BFS parent arc,
-// q = BFS queue, ex = bottleneck capacity from the source.
-
-// ---------------------------------------------------------------------------
-// PARITY solver (the replay argued above), with little bookkeeping per step: per-vertex state in one 16-byte VState (one LDS.128 per pop, one
-// STS.128 per write-back), the in-queue set in registers when n <= 128
-// (every lane holds the same two 64-bit words, so the enqueue test is a
-// uniform register test), and a failed scan of the last arc chunk falls
-// straight into the relabel instead of taking another loop trip.
-__device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, const int lane) {
-  VState* vs = g.vs;
-  for (int x = lane; x < n; x += 32) {
-    VState v;
-    v.ex = 0.0;
-    v.h = (x == s) ? (int16_t)n : (int16_t)0;
-    v.cur = 0;
-    v.b = g.abeg[x];
-    v.deg = (int16_t)(g.abeg[x + 1] - g.abeg[x]);
-    vs[x] = v;
-    g.inq[x] = 0;
-  }
-  for (int x = lane; x <= 2 * n; x += 32) g.cnt[x] = 0;
-  __syncwarp();
-  if (lane == 0) {
-    g.cnt[0] = (int16_t)(n - 1);
-    g.cnt[n] += 1;
-  }
-  // in-queue flags: every lane writes them and every lane reads its own
-  // write, so no cross-lane ordering is needed (a byte test beat a register
-  // bitmask on issue slots)
-  auto in_queue = [&](int x) -> bool { return g.inq[x] != 0; };
-  auto mark = [&](int x, bool on) { g.inq[x] = on ? 1 : 0; };
-  int tail = 0, qcount = 0;
-  // saturate source arcs in adjacency order (:168-173): uniform loop, lane 0 stores
-  __syncwarp();
-  {
-    const int b = g.abeg[s], e = g.abeg[s + 1];
-    for (int a = b; a < e; ++a) {
-      __syncwarp();
-      const double c = g.cap[a];
-      if (c > FLOW_EPS) {
-        const int to = g.to[a];
-        const int r = g.rv[a];
-        double exs = vs[s].ex + c;
-        const double amt = ref_min(exs, g.cap[a]);
-        __syncwarp();
-        if (lane == 0) {
-          vs[s].ex = exs;
-          g.cap[a] -= amt;
-          g.cap[r] += amt;
-          vs[s].ex -= amt;
-          vs[to].ex += amt;
-        }
-        __syncwarp();
-        if (to != s && to != t && !in_queue(to)) {
-          mark(to, true);
-          if (lane == 0) g.q[tail] = (int16_t)to;
-          tail = tail + 1 == n ? 0 : tail + 1;
-          ++qcount;
-        }
-      }
-    }
-  }
-  int head = 0;
-  const int two_n = 2 * n;
-  while (qcount > 0) {
-    __syncwarp();
-    const int u = g.q[head];
-    head = head + 1 == n ? 0 : head + 1;
-    --qcount;
-    const VState su = vs[u];
-    double ex = su.ex;
-    int hu = su.h;
-    int cu = su.cur;
-    const int b = su.b;
-    const int deg = su.deg;
-    mark(u, false);
-    int kl = -1;
-    bool inr = false;
-    double ca = 0.0;
-    int ta = 0, ra = 0, hta = 0;
-    while (ex > FLOW_EPS) {
-      if (cu < deg) {
-        const int k = cu >> 5;
-        if (k != kl) {
-          const int jr = (k << 5) + lane;
-          inr = jr < deg;
-          if (inr) {
-            const int a = b + jr;
-            ca = g.cap[a];
-            ta = g.to[a];
-            ra = g.rv[a];
-            hta = vs[ta].h;
-          }
-          kl = k;
-        }
-        const int jr = (k << 5) + lane;
-        const bool adm = inr && jr >= cu && ca > FLOW_EPS && hu == hta + 1;
-        const unsigned m = __ballot_sync(FULL, adm);
-        if (m != 0u) {
-          const int j = __ffs(m) - 1;
-          cu = (k << 5) + j;
-          const double cj = __shfl_sync(FULL, ca, j);
-          const int tj = __shfl_sync(FULL, ta, j);
-          const double amt = ref_min(ex, cj);  // push (:156-166)
-          if (lane == j) {
-            ca -= amt;
-            g.cap[b + cu] = ca;
-            g.cap[ra] += amt;
-          }
-          if (lane == 0) vs[tj].ex += amt;
-          ex -= amt;
-          if (tj != s && tj != t && !in_queue(tj)) {
-            mark(tj, true);
-            if (lane == 0) g.q[tail] = (int16_t)tj;
-            tail = tail + 1 == n ? 0 : tail + 1;
-            ++qcount;
-          }
-          continue;
-        }
-        cu = min(deg, (k + 1) << 5);
-        if (cu < deg) continue;
-      }
-      // relabel (:180-199)
-      const int old = hu;
-      int best = two_n;
-      const int nch = (deg + 31) >> 5;
-      for (int k = 0; k < nch; ++k) {
-        if (k != kl) {
-          const int jr = (k << 5) + lane;
-          inr = jr < deg;
-          if (inr) {
-            const int a = b + jr;
-            ca = g.cap[a];
-            ta = g.to[a];
-            ra = g.rv[a];
-            hta = vs[ta].h;
-          }
-          kl = k;
-        }
-        const int cand = (inr && ca > FLOW_EPS) ? hta + 1 : two_n;
-        best = min(best, __reduce_min_sync(FULL, cand));
-      }
-      hu = best;
-      cu = 0;
-      int cold = 0;
-      if (lane == 0) {
-        vs[u].h = (int16_t)best;
-        cold = g.cnt[old] - 1;
-        g.cnt[old] = (int16_t)cold;
-        g.cnt[best] += 1;
-      }
-      cold = __shfl_sync(FULL, cold, 0);
-      __syncwarp();
-      if (old < n && cold == 0) {
-        int moved = 0;
-        for (int x = lane; x < n; x += 32) {
-          const int hx = vs[x].h;
-          if (x != s && hx > old && hx < n) {
-            vs[x].h = (int16_t)(n + 1);
-            ++moved;
-          }
-        }
-        moved = __reduce_add_sync(FULL, moved);
-        for (int hh = old + 1 + lane; hh < n; hh += 32) g.cnt[hh] = 0;
-        __syncwarp();
-        if (lane == 0) g.cnt[n + 1] += (int16_t)moved;
-        if (hu > old && hu < n) hu = n + 1;
-        if (inr) hta = vs[ta].h;
-      }
-      if (inr && ta == u) hta = hu;  // self-loop arcs see u's new height
-      if (best >= two_n) break;
-    }
-    if (lane == 0) {
-      VState w;
-      w.ex = ex;
-      w.h = (int16_t)hu;
-      w.cur = (int16_t)cu;
-      w.b = (int16_t)b;
-      w.deg = (int16_t)deg;
-      vs[u] = w;
-    }
-  }
-  __syncwarp();
-}
-
-// ---------------------------------------------------------------------------
-// K1: build the reference's FlowGraph for one placement row into the slot.
-// Vertex numbering (flow_graph.cpp:63-69): source 0, sink 1, then (in, out)
-// pairs of the used nodes in byte-lexicographic id order.  Edge order: compute
-// edges in that order (:71-84), then valid links in declaration order
-// (:86-134).  Arc order per vertex = edge order (:140-145), which for these
-// graphs is: the compute arc first, then link arcs in link order; so the
-// position of a link's arc at a vertex is 1 (0 at source/sink) + the number of
-// earlier valid links touching that vertex — a running counter per vertex,
-// advanced per 32-link chunk with __match_any_sync.
-//
-// Returns status (0 ok, 1-3 validation, ST_OVERFLOW), V and E.
-
-struct LinkEval {
-  bool valid;
-  int u, v;
-};
-
-__device__ __forceinline__ LinkEval eval_link(const ClusterDev& cd, const Gs& g, int l, int partial) {
-  LinkEval r{false, 0, 0};
-  const uint32_t pk = __ldg(cd.link_pack + l);
-  const int a = (int)(pk & 0xffffu) - 1;
-  const int bb = (int)(pk >> 16) - 1;
-  if (a < 0) {  // coordinator -> bb (:89-101)
-    const int vb = g.vin[bb];
-    if (vb >= 0 && g.ps[bb] == 0) {
-      r.valid = true;
-      r.u = 0;
-      r.v = vb;
-    }
-  } else if (bb < 0) {  // a -> coordinator (:102-114)
-    const int va = g.vin[a];
-    if (va >= 0 && g.pe[a] == cd.L) {
-      r.valid = true;
-      r.u = va + 1;
-      r.v = 1;
-    }
-  } else {  // a -> bb (:115-133)
-    const int va = g.vin[a], vb = g.vin[bb];
-    if (va >= 0 && vb >= 0) {
-      const int aend = g.pe[a], bs = g.ps[bb], be = g.pe[bb];
-      const bool ok = partial ? (bs <= aend && aend < be) : (aend == bs);
-      if (ok) {
-        r.valid = true;
-        r.u = va + 1;
-        r.v = vb;
-      }
-    }
-  }
-  return r;
-}
-
-__device__ int build_graph(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
-                           int partial, int lane, int& V, int& E) {
-  const int N = cd.N, L = cd.L;
-  // placement + validation in id order (:52-61): first failing node in lex order
-  int bad = INT_MAX;
-  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
-  for (int k = lane; k < N; k += 32) {
-    const int32_t w = __ldg(row32 + k);
-    const int s = (int16_t)(w & 0xffff);
-    const int e = (int16_t)(w >> 16);
-    g.ps[k] = (int16_t)s;
-    g.pe[k] = (int16_t)e;
-    g.vin[k] = -1;
-    if (e > s) {
-      int code = 0;
-      if (s < 0 || e > L) code = 2;
-      else if (e - s > __ldg(cd.kmax + k)) code = 3;
-      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
-    }
-  }
-  bad = __reduce_min_sync(FULL, bad);
-  if (bad != INT_MAX) return bad & 3;
-  __syncwarp();
-  // vertices in lex order (:63-69)
-  int U = 0;
-  for (int r0 = 0; r0 < N; r0 += 32) {
-    const int r = r0 + lane;
-    int k = -1;
-    bool used = false;
-    if (r < N) {
-      k = __ldg(cd.lexnode + r);
-      used = g.pe[k] > g.ps[k];
-    }
-    const unsigned m = __ballot_sync(FULL, used);
-    if (used) {
-      const int idx = U + __popc(m & lanemask_lt());
-      g.vin[k] = (int16_t)(2 + 2 * idx);
-      g.unode[idx] = (int16_t)k;
-    }
-    U += __popc(m);
-  }
-  V = 2 + 2 * U;
-  // degree count: compute arc (1 per used vertex) + link arcs
-  for (int x = lane; x < V; x += 32) g.cur[x] = x >= 2 ? 1 : 0;
-  __syncwarp();
-  int nvalid = 0;
-  for (int l0 = 0; l0 < cd.Mv; l0 += 32) {
-    const int l = l0 + lane;
-    LinkEval le{false, 0, 0};
-    if (l < cd.Mv) le = eval_link(cd, g, l, partial);
-    const unsigned vm = __ballot_sync(FULL, le.valid);
-    if (vm == 0u) continue;
-    nvalid += __popc(vm);
-    unsigned pu = 0, pv = 0;
-    int cu = 0, cv = 0;
-    if (le.valid) {
-      pu = __match_any_sync(vm, le.u);
-      pv = __match_any_sync(vm, le.v);
-      cu = g.cur[le.u];
-      cv = g.cur[le.v];
-    }
-    __syncwarp();
-    if (le.valid) {
-      const unsigned lt = lanemask_lt();
-      if ((pu & lt) == 0u) g.cur[le.u] = (int16_t)(cu + __popc(pu));
-      if ((pv & lt) == 0u) g.cur[le.v] = (int16_t)(cv + __popc(pv));
-    }
-    __syncwarp();
-  }
-  E = U + nvalid;
-  if (V > lay.V || 2 * E > lay.A) return ST_OVERFLOW;
-  // arc offsets: exclusive scan of degrees
-  int run = 0;
-  for (int x0 = 0; x0 < V; x0 += 32) {
-    const int x = x0 + lane;
-    const int d = x < V ? g.cur[x] : 0;
-    int incl = d;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (x < V) g.abeg[x] = (int16_t)(run + incl - d);
-    run += __shfl_sync(FULL, incl, 31);
-  }
-  if (lane == 0) g.abeg[V] = (int16_t)run;
-  __syncwarp();
-  // compute arcs (edge j = in_j -> out_j, cap compute_edge_capacity)
-  for (int j = lane; j < U; j += 32) {
-    const int k = g.unode[j];
-    const int vi = 2 + 2 * j, vo = vi + 1;
-    const int ai = g.abeg[vi], ao = g.abeg[vo];
-    g.to[ai] = (int16_t)vo;
-    g.rv[ai] = (int16_t)ao;
-    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (g.pe[k] - g.ps[k]) - 1);
-    g.to[ao] = (int16_t)vi;
-    g.rv[ao] = (int16_t)ai;
-    g.cap[ao] = 0.0;
-  }
-  for (int x = lane; x < V; x += 32) g.cur[x] = x >= 2 ? 1 : 0;
-  __syncwarp();
-  // link arcs at their ranked positions
-  for (int l0 = 0; l0 < cd.Mv; l0 += 32) {
-    const int l = l0 + lane;
-    LinkEval le{false, 0, 0};
-    if (l < cd.Mv) le = eval_link(cd, g, l, partial);
-    const unsigned vm = __ballot_sync(FULL, le.valid);
-    if (vm == 0u) continue;
-    unsigned pu = 0, pv = 0;
-    int cu = 0, cv = 0;
-    if (le.valid) {
-      pu = __match_any_sync(vm, le.u);
-      pv = __match_any_sync(vm, le.v);
-      cu = g.cur[le.u];
-      cv = g.cur[le.v];
-    }
-    __syncwarp();
-    if (le.valid) {
-      const unsigned lt = lanemask_lt();
-      const int fa = g.abeg[le.u] + cu + __popc(pu & lt);
-      const int ra = g.abeg[le.v] + cv + __popc(pv & lt);
-      g.to[fa] = (int16_t)le.v;
-      g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + l);
-      g.to[ra] = (int16_t)le.u;
-      g.rv[ra] = (int16_t)fa;
-      g.cap[ra] = 0.0;
-      if ((pu & lt) == 0u) g.cur[le.u] = (int16_t)(cu + __popc(pu));
-      if ((pv & lt) == 0u) g.cur[le.v] = (int16_t)(cv + __popc(pv));
-    }
-    __syncwarp();
-  }
-  return 0;
-}
-
-// SCORE-mode builder.  Same graph as build_graph up to vertex numbering and
-// arc order, which the value does not depend on: node k owns vertices
-// in = 2 + 2k, out = 3 + 2k (unused nodes keep no arcs), and each lane walks
-// its node's precomputed out-/in-link lists instead of scanning every link
-// of the cluster.  Validation and status codes are shared with build_graph.
-__device__ __forceinline__ bool edge_ok(int aend, int bs, int be, int partial) {
-  return partial ? (bs <= aend && aend < be) : (aend == bs);
-}
-
-__device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
-                                 int partial, int lane, int& V, int& E) {
-  const int N = cd.N, L = cd.L;
-  int bad = INT_MAX;
-  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
-  for (int k = lane; k < N; k += 32) {
-    const int32_t w = __ldg(row32 + k);
-    const int s = (int16_t)(w & 0xffff);
-    const int e = (int16_t)(w >> 16);
-    g.ps[k] = (int16_t)s;
-    g.pe[k] = (int16_t)e;
-    if (e > s) {
-      int code = 0;
-      if (s < 0 || e > L) code = 2;
-      else if (e - s > __ldg(cd.kmax + k)) code = 3;
-      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
-    }
-  }
-  bad = __reduce_min_sync(FULL, bad);
-  if (bad != INT_MAX) return bad & 3;
-  V = 2 + 2 * N;
-  if (V > lay.V) return ST_OVERFLOW;
-  __syncwarp();
-  // degrees: in_k = compute + valid in-links + source arc; out_k = compute +
-  // valid out-links + sink arc.
-  int nedges = 0, dsrc = 0, dsink = 0;
-  int* fill = reinterpret_cast<int*>(g.ex);  // int counters per vertex during the build
-  for (int k = lane; k < N; k += 32) {
-    const int s = g.ps[k], e = g.pe[k];
-    int din = 0, dout = 0;
-    if (e > s) {
-      din = 1;
-      dout = 1;
-      ++nedges;
-      for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
-        const int j = __ldg(&cd.out_list[p].x);
-        const int sj = g.ps[j], ej = g.pe[j];
-        if (ej > sj && edge_ok(e, sj, ej, partial)) ++dout;
-      }
-      for (int p = __ldg(cd.in_beg + k), pe_ = __ldg(cd.in_beg + k + 1); p < pe_; ++p) {
-        const int i = __ldg(&cd.in_list[p].x);
-        const int si = g.ps[i], ei = g.pe[i];
-        if (ei > si && edge_ok(ei, s, e, partial)) ++din;
-      }
-      nedges += dout - 1;  // each link edge counted once, at its source
-      if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
-        ++din;
-        ++dsrc;
-        ++nedges;
-      }
-      if (e == L && __ldg(cd.cin_link + k) >= 0) {
-        ++dout;
-        ++dsink;
-        ++nedges;
-      }
-    }
-    g.cur[2 + 2 * k] = (int16_t)din;
-    g.cur[3 + 2 * k] = (int16_t)dout;
-  }
-  nedges = __reduce_add_sync(FULL, nedges);
-  dsrc = __reduce_add_sync(FULL, dsrc);
-  dsink = __reduce_add_sync(FULL, dsink);
-  E = nedges;
-  if (2 * E > lay.A) return ST_OVERFLOW;
-  if (lane == 0) {
-    g.cur[0] = (int16_t)dsrc;
-    g.cur[1] = (int16_t)dsink;
-  }
-  __syncwarp();
-  int run = 0;
-  for (int x0 = 0; x0 < V; x0 += 32) {
-    const int x = x0 + lane;
-    const int d = x < V ? g.cur[x] : 0;
-    int incl = d;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (x < V) {
-      g.abeg[x] = (int16_t)(run + incl - d);
-      fill[x] = 0;
-    }
-    run += __shfl_sync(FULL, incl, 31);
-  }
-  if (lane == 0) g.abeg[V] = (int16_t)run;
-  __syncwarp();
-  // arcs: each lane places its node's compute pair and every edge it
-  // sources; the paired reverse arc takes the next free slot at its head.
-  for (int k = lane; k < N; k += 32) {
-    const int s = g.ps[k], e = g.pe[k];
-    if (e <= s) continue;
-    const int vi = 2 + 2 * k, vo = vi + 1;
-    const int ai = g.abeg[vi] + atomicAdd(&fill[vi], 1);
-    const int ao = g.abeg[vo] + atomicAdd(&fill[vo], 1);
-    g.to[ai] = (int16_t)vo;
-    g.rv[ai] = (int16_t)ao;
-    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
-    g.to[ao] = (int16_t)vi;
-    g.rv[ao] = (int16_t)ai;
-    g.cap[ao] = 0.0;
-    for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
-      const int2 jl = __ldg(&cd.out_list[p]);
-      const int sj = g.ps[jl.x], ej = g.pe[jl.x];
-      if (!(ej > sj && edge_ok(e, sj, ej, partial))) continue;
-      const int vj = 2 + 2 * jl.x;
-      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
-      const int ra = g.abeg[vj] + atomicAdd(&fill[vj], 1);
-      g.to[fa] = (int16_t)vj;
-      g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + jl.y);
-      g.to[ra] = (int16_t)vo;
-      g.rv[ra] = (int16_t)fa;
-      g.cap[ra] = 0.0;
-    }
-    const int lc = __ldg(cd.cout_link + k);
-    if (s == 0 && lc >= 0) {
-      const int fa = g.abeg[0] + atomicAdd(&fill[0], 1);
-      const int ra = g.abeg[vi] + atomicAdd(&fill[vi], 1);
-      g.to[fa] = (int16_t)vi;
-      g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + lc);
-      g.to[ra] = 0;
-      g.rv[ra] = (int16_t)fa;
-      g.cap[ra] = 0.0;
-    }
-    const int lk = __ldg(cd.cin_link + k);
-    if (e == L && lk >= 0) {
-      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
-      const int ra = g.abeg[1] + atomicAdd(&fill[1], 1);
-      g.to[fa] = 1;
-      g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + lk);
-      g.to[ra] = (int16_t)vo;
-      g.rv[ra] = (int16_t)fa;
-      g.cap[ra] = 0.0;
-    }
-  }
-  __syncwarp();
-  return 0;
-}
-
-// SCORE builder for N <= 64: node sets are 64-bit words.  cover[l] = nodes
-// whose interval contains layer l, start[l] = nodes starting at l.  Node i's
-// valid successors are (partial ? cover[e_i] : start[e_i]) & out_mask[i]
-// (flow_graph.cpp:121: s_j <= e_i < e_j, resp. e_i == s_j), so each node
-// visits only its ~2-3 actual edges instead of every link of the cluster.
-__device__ int build_graph_score_small(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
-                                       int partial, int lane, int& V, int& E) {
-  const int N = cd.N, L = cd.L;
-  unsigned long long* cover = reinterpret_cast<unsigned long long*>(g.cap);  // [L] then start[L]; scratch
-  unsigned long long* start = cover + L;
-  int bad = INT_MAX;
-  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
-  for (int k = lane; k < N; k += 32) {
-    const int32_t w = __ldg(row32 + k);
-    const int s = (int16_t)(w & 0xffff);
-    const int e = (int16_t)(w >> 16);
-    g.ps[k] = (int16_t)s;
-    g.pe[k] = (int16_t)e;
-    if (e > s) {
-      int code = 0;
-      if (s < 0 || e > L) code = 2;
-      else if (e - s > __ldg(cd.kmax + k)) code = 3;
-      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
-    }
-  }
-  bad = __reduce_min_sync(FULL, bad);
-  if (bad != INT_MAX) return bad & 3;
-  V = 2 + 2 * N;
-  if (V > lay.V || 2 * L > lay.A) return ST_OVERFLOW;  // cover/start scratch lives in cap[]
-  for (int l = lane; l < 2 * L; l += 32) cover[l] = 0ull;
-  __syncwarp();
-  for (int k = lane; k < N; k += 32) {
-    const int s = g.ps[k], e = g.pe[k];
-    if (e <= s) continue;
-    const unsigned long long bit = 1ull << k;
-    atomicOr(&start[s], bit);
-    for (int l = s; l < e; ++l) atomicOr(&cover[l], bit);
-  }
-  __syncwarp();
-  // successor sets (kept in registers; lanes own nodes lane, lane+32)
-  unsigned long long T[2] = {0ull, 0ull};
-  int* fill = reinterpret_cast<int*>(g.vs);
-  for (int x = lane; x < V; x += 32) fill[x] = 0;
-  __syncwarp();
-  int nedges = 0, dsrc = 0, dsink = 0;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int k = lane + 32 * q;
-    if (k >= N) continue;
-    const int s = g.ps[k], e = g.pe[k];
-    if (e <= s) continue;
-    unsigned long long t = 0ull;
-    if (e < L) t = (partial ? cover[e] : start[e]) & __ldg(cd.out_mask + k);
-    T[q] = t;
-    const int nt = __popcll(t);
-    nedges += 1 + nt;
-    int dout = 1 + nt, din = 1;
-    if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
-      ++din;
-      ++dsrc;
-      ++nedges;
-    }
-    if (e == L && __ldg(cd.cin_link + k) >= 0) {
-      ++dout;
-      ++dsink;
-      ++nedges;
-    }
-    atomicAdd(&fill[2 + 2 * k], din);
-    atomicAdd(&fill[3 + 2 * k], dout);
-    for (unsigned long long m = t; m; m &= m - 1) atomicAdd(&fill[2 + 2 * (__ffsll(m) - 1)], 1);  // in_j
-  }
-  nedges = __reduce_add_sync(FULL, nedges);
-  dsrc = __reduce_add_sync(FULL, dsrc);
-  dsink = __reduce_add_sync(FULL, dsink);
-  E = nedges;
-  if (2 * E > lay.A) return ST_OVERFLOW;
-  __syncwarp();
-  if (lane == 0) {
-    fill[0] = dsrc;
-    fill[1] = dsink;
-  }
-  __syncwarp();
-  int run = 0;
-  for (int x0 = 0; x0 < V; x0 += 32) {
-    const int x = x0 + lane;
-    const int d = x < V ? fill[x] : 0;
-    int incl = d;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (x < V) g.abeg[x] = (int16_t)(run + incl - d);
-    run += __shfl_sync(FULL, incl, 31);
-  }
-  if (lane == 0) g.abeg[V] = (int16_t)run;
-  __syncwarp();
-  for (int x = lane; x < V; x += 32) fill[x] = 0;
-  __syncwarp();
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int k = lane + 32 * q;
-    if (k >= N) continue;
-    const int s = g.ps[k], e = g.pe[k];
-    if (e <= s) continue;
-    const int vi = 2 + 2 * k, vo = vi + 1;
-    const int ai = g.abeg[vi] + atomicAdd(&fill[vi], 1);
-    const int ao = g.abeg[vo] + atomicAdd(&fill[vo], 1);
-    g.to[ai] = (int16_t)vo;
-    g.rv[ai] = (int16_t)ao;
-    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
-    g.to[ao] = (int16_t)vi;
-    g.rv[ao] = (int16_t)ai;
-    g.cap[ao] = 0.0;
-    for (unsigned long long m = T[q]; m; m &= m - 1) {
-      const int j = __ffsll(m) - 1;
-      const int vj = 2 + 2 * j;
-      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
-      const int ra = g.abeg[vj] + atomicAdd(&fill[vj], 1);
-      g.to[fa] = (int16_t)vj;
-      g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + __ldg(cd.pair_link + k * N + j));
-      g.to[ra] = (int16_t)vo;
-      g.rv[ra] = (int16_t)fa;
-      g.cap[ra] = 0.0;
-    }
-    const int lc = __ldg(cd.cout_link + k);
-    if (s == 0 && lc >= 0) {
-      const int fa = g.abeg[0] + atomicAdd(&fill[0], 1);
-      const int ra = g.abeg[vi] + atomicAdd(&fill[vi], 1);
-      g.to[fa] = (int16_t)vi;
-      g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + lc);
-      g.to[ra] = 0;
-      g.rv[ra] = (int16_t)fa;
-      g.cap[ra] = 0.0;
-    }
-    const int lk = __ldg(cd.cin_link + k);
-    if (e == L && lk >= 0) {
-      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
-      const int ra = g.abeg[1] + atomicAdd(&fill[1], 1);
-      g.to[fa] = 1;
-      g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + lk);
-      g.to[ra] = (int16_t)vo;
-      g.rv[ra] = (int16_t)fa;
-      g.cap[ra] = 0.0;
-    }
-  }
-  __syncwarp();
-  return 0;
-}
-
-// Edmonds-Karp with a batched BFS: each step takes as many queued vertices as
-// have <= 32 arcs between them and gives every lane one arc.  Lanes are in
-// queue order, and a vertex reached twice in one step keeps its lowest lane,
-// so the BFS tree — hence every augmenting path — is exactly that of the
-// one-vertex-at-a-time BFS.
-__device__ double solve_ek_batched(const Gs& g, const int n, const int s, const int t, const int lane) {
-  double value = 0.0;
-  const unsigned lt = lanemask_lt();
-  const unsigned le = lt | (1u << lane);
-  for (;;) {
-    for (int x = lane; x < n; x += 32) g.h[x] = -1;
-    __syncwarp();
-    if (lane == 0) {
-      g.h[s] = -2;
-      g.q[0] = (int16_t)s;
-      g.ex[s] = 1.0e300;
-    }
-    __syncwarp();
-    int qh = 0, qt = 1;
-    bool found = false;
-    while (qh < qt) {
-      const int avail = min(32, qt - qh);
-      int vi = 0, bi = 0, di = 0;
-      if (lane < avail) {
-        vi = g.q[qh + lane];
-        bi = g.abeg[vi];
-        di = g.abeg[vi + 1] - bi;
-      }
-      int incl = di;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int d0 = __shfl_sync(FULL, di, 0);
-      if (d0 > 32) {
-        // a wide vertex: scan it alone, 32 arcs at a time
-        const int u = vi, b = bi;
-        const double bu = g.ex[__shfl_sync(FULL, u, 0)];
-        const int ub = __shfl_sync(FULL, b, 0);
-        for (int a0 = ub; a0 < ub + d0; a0 += 32) {
-          const int a = a0 + lane;
-          bool ok = false;
-          int v = 0;
-          double c = 0.0;
-          if (a < ub + d0) {
-            c = g.cap[a];
-            if (c > FLOW_EPS) {
-              v = g.to[a];
-              ok = g.h[v] == -1;
-            }
-          }
-          const unsigned m = __ballot_sync(FULL, ok);
-          if (ok) {
-            g.h[v] = (int16_t)a;
-            g.q[qt + __popc(m & lt)] = (int16_t)v;
-            g.ex[v] = ref_min(bu, c);
-          }
-          qt += __popc(m);
-          if (__any_sync(FULL, ok && v == t)) {
-            found = true;
-            break;
-          }
-        }
-        qh += 1;
-      } else {
-        const unsigned fit = __ballot_sync(FULL, lane < avail && incl <= 32);
-        const int k = __popc(fit);  // >= 1: lane 0 fits (d0 <= 32)
-        const int start = incl - di;
-        const unsigned sm = __reduce_or_sync(FULL, (lane < k && di > 0) ? (1u << start) : 0u);
-        const int total = __shfl_sync(FULL, incl, k - 1);
-        const int slot = __popc(sm & le) - 1;
-        const int su = slot < 0 ? 0 : slot;
-        const int u_b = __shfl_sync(FULL, bi, su);
-        const int u_st = __shfl_sync(FULL, start, su);
-        const int u_v = __shfl_sync(FULL, vi, su);
-        bool ok = false;
-        int v = 0;
-        double c = 0.0;
-        if (lane < total) {
-          const int a = u_b + (lane - u_st);
-          c = g.cap[a];
-          if (c > FLOW_EPS) {
-            v = g.to[a];
-            ok = g.h[v] == -1;
-          }
-        }
-        const unsigned cand = __ballot_sync(FULL, ok);
-        if (ok) {
-          const unsigned peers = __match_any_sync(cand, v);
-          ok = (peers & lt) == 0u;
-        }
-        const unsigned m = __ballot_sync(FULL, ok);
-        if (ok) {
-          const int a = u_b + (lane - u_st);
-          g.h[v] = (int16_t)a;
-          g.q[qt + __popc(m & lt)] = (int16_t)v;
-          g.ex[v] = ref_min(g.ex[u_v], c);
-        }
-        qt += __popc(m);
-        qh += k;
-        if (__any_sync(FULL, ok && v == t)) found = true;
-      }
-      __syncwarp();
-      if (found) break;
-    }
-    if (!found) break;
-    const double f = g.ex[t];
-    if (lane == 0) {
-      int x = t;
-      while (x != s) {
-        const int a = g.h[x];
-        const int r = g.rv[a];
-        g.cap[a] -= f;
-        g.cap[r] += f;
-        x = g.to[r];
-      }
-    }
-    __syncwarp();
-    value += f;
-  }
-  return value;
-}
-
-// SCORE solver for n <= 128: Edmonds-Karp with a level-synchronous bitset
-// BFS.  Lane l owns vertices l, l+32, l+64, l+96 and keeps, in registers, the
-// set of their residual out-neighbours (two 64-bit words per vertex).  One
-// BFS level is: OR the rows of owned frontier vertices, REDUX.OR across the
-// warp, mask with the visited set.  Only BFS levels are stored; the
-// augmenting path is recovered backwards from the sink (at each step the
-// first arc, in adjacency order, from a vertex one level closer to the
-// source with residual capacity).  Deterministic; exact on integer
-// capacities like every SCORE path.
-__device__ __forceinline__ bool bit128(unsigned long long w0, unsigned long long w1, int x) {
-  return ((x < 64 ? w0 : w1) >> (x & 63)) & 1ull;
-}
-
-__device__ __forceinline__ unsigned long long warp_or64(unsigned long long v) {
-  const unsigned lo = __reduce_or_sync(FULL, (unsigned)(v & 0xffffffffull));
-  const unsigned hi = __reduce_or_sync(FULL, (unsigned)(v >> 32));
-  return ((unsigned long long)hi << 32) | lo;
-}
-
-// Pair closure: in this numbering a node's vertices are v and v^1 (in = 2+2k,
-// out = 3+2k), joined by its compute arc.  When a BFS level reaches one half
-// of a node whose pair arc has residual capacity, the other half joins the
-// same level (a shift on the 128-bit frontier), so the BFS walks nodes rather
-// than split vertices and needs about half the levels.  Paths remain valid
-// augmenting paths and the choice stays deterministic.
-__device__ __forceinline__ unsigned long long swap_pairs(unsigned long long x) {
-  return ((x & 0x5555555555555555ull) << 1) | ((x & 0xAAAAAAAAAAAAAAAAull) >> 1);
-}
-
-__device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int t, const int lane) {
-  // rows R[x] (residual out-neighbours of x, 128 bits) in the VState region;
-  // per-vertex BFS code (2*level, +1 if added by the pair closure) in the
-  // count region; canonical parent arc per vertex in `cur`; the augmenting
-  // path in the queue region.
-  ulonglong2* R = reinterpret_cast<ulonglong2*>(g.vs);
-  int16_t* dist = g.cnt;
-  int16_t* par = g.cur;
-  int16_t* path = g.q;
-  for (int x = lane; x < n; x += 32) {
-    unsigned long long r0 = 0ull, r1 = 0ull;
-    for (int a = g.abeg[x], e = g.abeg[x + 1]; a < e; ++a) {
-      if (g.cap[a] > FLOW_EPS) {
-        const int y = g.to[a];
-        if (y < 64) r0 |= 1ull << y;
-        else r1 |= 1ull << (y - 64);
-      }
-    }
-    R[x] = make_ulonglong2(r0, r1);
-  }
-  __syncwarp();
-  double value = 0.0;
-  for (;;) {
-    // pair arcs with residual capacity: bit v set iff R[v] holds v^1 (v >= 2)
-    unsigned long long P0, P1;
-    {
-      unsigned b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int v = lane + 32 * i;
-        bool pr = false;
-        if (v >= 2 && v < n) {
-          const ulonglong2 r = R[v];
-          const int w = v ^ 1;
-          pr = ((w < 64 ? r.x : r.y) >> (w & 63)) & 1ull;
-        }
-        b[i] = __ballot_sync(FULL, pr);
-      }
-      P0 = ((unsigned long long)b[1] << 32) | b[0];
-      P1 = ((unsigned long long)b[3] << 32) | b[2];
-    }
-    for (int x = lane; x < n; x += 32) dist[x] = (int16_t)(x == s ? 0 : -1);
-    unsigned long long F0 = s < 64 ? (1ull << s) : 0ull, F1 = s < 64 ? 0ull : (1ull << (s - 64));
-    unsigned long long V0 = F0, V1 = F1;
-    int d = 0;
-    bool found = false;
-    for (;;) {
-      unsigned long long a0 = 0ull, a1 = 0ull;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const unsigned long long w = (i < 2) ? F0 : F1;
-        if ((w >> (lane + 32 * (i & 1))) & 1ull) {
-          const ulonglong2 r = R[lane + 32 * i];
-          a0 |= r.x;
-          a1 |= r.y;
-        }
-      }
-      unsigned long long n0 = warp_or64(a0) & ~V0;
-      unsigned long long n1 = warp_or64(a1) & ~V1;
-      if ((n0 | n1) == 0ull) break;
-      ++d;
-      const unsigned long long c0 = swap_pairs(n0 & P0) & ~V0 & ~n0;
-      const unsigned long long c1 = swap_pairs(n1 & P1) & ~V1 & ~n1;
-      n0 |= c0;
-      n1 |= c1;
-      V0 |= n0;
-      V1 |= n1;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int sh = lane + 32 * (i & 1);
-        const unsigned long long w = (i < 2) ? n0 : n1;
-        const unsigned long long cw = (i < 2) ? c0 : c1;
-        if ((w >> sh) & 1ull) dist[lane + 32 * i] = (int16_t)(2 * d + (int)((cw >> sh) & 1ull));
-      }
-      F0 = n0;
-      F1 = n1;
-      if (bit128(n0, n1, t)) {
-        found = true;
-        break;
-      }
-    }
-    if (!found) break;
-    __syncwarp();
-    // canonical parent of every visited vertex: a closure vertex takes its
-    // pair arc; otherwise the first arc, in adjacency order, back to a vertex
-    // of the previous level with residual capacity
-    for (int x = lane; x < n; x += 32) {
-      const int cx = dist[x];
-      if (cx <= 0) continue;
-      const int want = (cx >> 1) - 1;
-      for (int a = g.abeg[x], e = g.abeg[x + 1]; a < e; ++a) {
-        const int u = g.to[a];
-        const int r = g.rv[a];
-        const bool ok = (cx & 1) ? (u == (x ^ 1)) : (dist[u] >= 0 && (dist[u] >> 1) == want && g.cap[r] > FLOW_EPS);
-        if (ok) {
-          par[x] = (int16_t)r;
-          break;
-        }
-      }
-    }
-    __syncwarp();
-    int len = 0;
-    if (lane == 0) {
-      int x = t;
-      while (x != s) {
-        const int a = par[x];
-        path[len++] = (int16_t)a;
-        x = g.to[g.rv[a]];
-      }
-    }
-    len = __shfl_sync(FULL, len, 0);
-    __syncwarp();
-    double f = 1.0e300;
-    for (int k = lane; k < len; k += 32) f = ref_min(f, g.cap[path[k]]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) f = ref_min(f, __shfl_xor_sync(FULL, f, o));
-    for (int k = lane; k < len; k += 32) {
-      const int a = path[k];
-      const int r = g.rv[a];
-      const int v = g.to[a];
-      const int u = g.to[r];
-      const double ca = g.cap[a] - f;
-      g.cap[a] = ca;
-      g.cap[r] += f;
-      if (ca <= FLOW_EPS) {
-        if (v < 64) atomicAnd(&R[u].x, ~(1ull << v));
-        else atomicAnd(&R[u].y, ~(1ull << (v - 64)));
-      }
-      if (u < 64) atomicOr(&R[v].x, 1ull << u);
-      else atomicOr(&R[v].y, 1ull << (u - 64));
-    }
-    value += f;
-    __syncwarp();
-  }
-  return value;
-}
-
-// PARITY builder for N <= 64: the reference's exact graph (vertex numbering in
-// id order, edge order, per-vertex arc order) without scanning every link.
-// Valid interconnects come from the per-layer cover/start masks as in the
-// SCORE builder; an arc's position in its vertex's list is its link's rank
-// among that vertex's valid links in declaration order, counted pairwise
-// over the ~2-3 valid links (pair_link holds compacted = declaration-ordered
-// link indices) and, for coordinator links, with the less_cout / less_cin
-// masks.  Produces exactly what build_graph produces (same vin/unode/abeg/
-// to/rv/cap), so solve_fifo2 and built_value are unchanged.
-__device__ int build_graph_small(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
-                                 int partial, int lane, int& V, int& E) {
-  const int N = cd.N, L = cd.L;
-  unsigned long long* cover = reinterpret_cast<unsigned long long*>(g.cap);  // scratch until arcs are written
-  unsigned long long* start = cover + L;
-  unsigned long long* inmask = reinterpret_cast<unsigned long long*>(g.vs);  // [N] sources of valid links into node
-  int bad = INT_MAX;
-  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
-  for (int k = lane; k < N; k += 32) {
-    const int32_t w = __ldg(row32 + k);
-    const int s = (int16_t)(w & 0xffff);
-    const int e = (int16_t)(w >> 16);
-    g.ps[k] = (int16_t)s;
-    g.pe[k] = (int16_t)e;
-    g.vin[k] = -1;
-    if (e > s) {
-      int code = 0;
-      if (s < 0 || e > L) code = 2;
-      else if (e - s > __ldg(cd.kmax + k)) code = 3;
-      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
-    }
-  }
-  bad = __reduce_min_sync(FULL, bad);
-  if (bad != INT_MAX) return bad & 3;
-  if (2 * L > lay.A) return ST_OVERFLOW;
-  for (int l = lane; l < 2 * L; l += 32) cover[l] = 0ull;
-  for (int k = lane; k < N; k += 32) inmask[k] = 0ull;
-  __syncwarp();
-  // vertices in id order (:63-69)
-  int U = 0;
-  for (int r0 = 0; r0 < N; r0 += 32) {
-    const int r = r0 + lane;
-    int k = -1;
-    bool used = false;
-    if (r < N) {
-      k = __ldg(cd.lexnode + r);
-      used = g.pe[k] > g.ps[k];
-    }
-    const unsigned m = __ballot_sync(FULL, used);
-    if (used) {
-      const int idx = U + __popc(m & lanemask_lt());
-      g.vin[k] = (int16_t)(2 + 2 * idx);
-      g.unode[idx] = (int16_t)k;
-    }
-    U += __popc(m);
-  }
-  V = 2 + 2 * U;
-  for (int k = lane; k < N; k += 32) {
-    const int s = g.ps[k], e = g.pe[k];
-    if (e <= s) continue;
-    const unsigned long long bit = 1ull << k;
-    atomicOr(&start[s], bit);
-    for (int l = s; l < e; ++l) atomicOr(&cover[l], bit);
-  }
-  __syncwarp();
-  // successor sets T (registers; lanes own nodes lane, lane + 32) and the
-  // coordinator-link sets SRC (coord -> node valid) / SNK (node -> coord valid)
-  unsigned long long T[2] = {0ull, 0ull};
-  bool src_ok[2] = {false, false}, snk_ok[2] = {false, false};
-  int nedges = 0;
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int k = lane + 32 * q;
-    if (k >= N) continue;
-    const int s = g.ps[k], e = g.pe[k];
-    if (e <= s) continue;
-    unsigned long long t = 0ull;
-    if (e < L) t = (partial ? cover[e] : start[e]) & __ldg(cd.out_mask + k);
-    T[q] = t;
-    for (unsigned long long m = t; m; m &= m - 1) atomicOr(&inmask[__ffsll(m) - 1], 1ull << k);
-    src_ok[q] = s == 0 && __ldg(cd.cout_link + k) >= 0;
-    snk_ok[q] = e == L && __ldg(cd.cin_link + k) >= 0;
-    nedges += 1 + __popcll(t) + (src_ok[q] ? 1 : 0) + (snk_ok[q] ? 1 : 0);
-  }
-  const unsigned long long SRC =
-      ((unsigned long long)__ballot_sync(FULL, src_ok[1]) << 32) | __ballot_sync(FULL, src_ok[0]);
-  const unsigned long long SNK =
-      ((unsigned long long)__ballot_sync(FULL, snk_ok[1]) << 32) | __ballot_sync(FULL, snk_ok[0]);
-  E = __reduce_add_sync(FULL, nedges);
-  if (V > lay.V || 2 * E > lay.A) return ST_OVERFLOW;
-  __syncwarp();
-  // degrees -> arc offsets
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int k = lane + 32 * q;
-    if (k >= N || g.vin[k] < 0) continue;
-    const int vi = g.vin[k];
-    g.cur[vi] = (int16_t)(1 + __popcll(inmask[k]) + (src_ok[q] ? 1 : 0));
-    g.cur[vi + 1] = (int16_t)(1 + __popcll(T[q]) + (snk_ok[q] ? 1 : 0));
-  }
-  if (lane == 0) {
-    g.cur[0] = (int16_t)__popcll(SRC);
-    g.cur[1] = (int16_t)__popcll(SNK);
-  }
-  __syncwarp();
-  int run = 0;
-  for (int x0 = 0; x0 < V; x0 += 32) {
-    const int x = x0 + lane;
-    const int d = x < V ? g.cur[x] : 0;
-    int incl = d;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (x < V) g.abeg[x] = (int16_t)(run + incl - d);
-    run += __shfl_sync(FULL, incl, 31);
-  }
-  if (lane == 0) g.abeg[V] = (int16_t)run;
-  __syncwarp();
-  // rank of link (src -> dst) among dst's valid incoming links, after the compute arc
-  auto in_rank = [&](int dst, int lidx) -> int {
-    int r = 1;
-    for (unsigned long long m = inmask[dst]; m; m &= m - 1) {
-      const int i = __ffsll(m) - 1;
-      r += __ldg(cd.pair_link + i * N + dst) < lidx;
-    }
-    const int lc = __ldg(cd.cout_link + dst);
-    if (g.ps[dst] == 0 && lc >= 0 && lc < lidx) ++r;
-    return r;
-  };
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int k = lane + 32 * q;
-    if (k >= N || g.vin[k] < 0) continue;
-    const int s = g.ps[k], e = g.pe[k];
-    const int vi = g.vin[k], vo = vi + 1;
-    const int ai = g.abeg[vi], ao = g.abeg[vo];
-    // compute edge: forward first at in, reverse first at out (:140-145)
-    g.to[ai] = (int16_t)vo;
-    g.rv[ai] = (int16_t)ao;
-    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
-    g.to[ao] = (int16_t)vi;
-    g.rv[ao] = (int16_t)ai;
-    g.cap[ao] = 0.0;
-    const int lk = __ldg(cd.cin_link + k);
-    // node -> node links, ranked among this out-vertex's valid links
-    for (unsigned long long m = T[q]; m; m &= m - 1) {
-      const int j = __ffsll(m) - 1;
-      const int lidx = __ldg(cd.pair_link + k * N + j);
-      int ro = 1;
-      for (unsigned long long m2 = T[q]; m2; m2 &= m2 - 1)
-        ro += __ldg(cd.pair_link + k * N + (__ffsll(m2) - 1)) < lidx;
-      if (snk_ok[q] && lk < lidx) ++ro;
-      const int vj = g.vin[j];
-      const int fa = ao + ro;
-      const int ra = g.abeg[vj] + in_rank(j, lidx);
-      g.to[fa] = (int16_t)vj;
-      g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + lidx);
-      g.to[ra] = (int16_t)vo;
-      g.rv[ra] = (int16_t)fa;
-      g.cap[ra] = 0.0;
-    }
-    if (src_ok[q]) {  // coordinator -> k
-      const int lc = __ldg(cd.cout_link + k);
-      const int fa = g.abeg[0] + __popcll(SRC & __ldg(cd.less_cout + k));
-      const int ra = ai + in_rank(k, lc);
-      g.to[fa] = (int16_t)vi;
-      g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + lc);
-      g.to[ra] = 0;
-      g.rv[ra] = (int16_t)fa;
-      g.cap[ra] = 0.0;
-    }
-    if (snk_ok[q]) {  // k -> coordinator
-      int ro = 1;
-      for (unsigned long long m2 = T[q]; m2; m2 &= m2 - 1)
-        ro += __ldg(cd.pair_link + k * N + (__ffsll(m2) - 1)) < lk;
-      const int fa = ao + ro;
-      const int ra = g.abeg[1] + __popcll(SNK & __ldg(cd.less_cin + k));
-      g.to[fa] = 1;
-      g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + lk);
-      g.to[ra] = (int16_t)vo;
-      g.rv[ra] = (int16_t)fa;
-      g.cap[ra] = 0.0;
-    }
-  }
-  __syncwarp();
-  return 0;
-}
-
-// Net flow into the sink in edge order (:222-227).  In built graphs the only
-// edges touching the sink are node->coordinator links, whose order in
-// g.edges equals the order of the sink's arcs.
-__device__ double built_value(const ClusterDev& cd, const Gs& g, int lane) {
-  double value = 0.0;
-  if (lane == 0) {
-    const int b = g.abeg[1], e = g.abeg[2];
-    for (int a = b; a < e; ++a) {
-      const int fa = g.rv[a];
-      const int node = g.unode[(g.to[a] - 2) >> 1];
-      double f = __ldg(cd.cin_cap + node) - g.cap[fa];
-      if (f < FLOW_EPS) f = 0.0;
-      value += f;
-    }
-  }
-  return __shfl_sync(FULL, value, 0);
-}
-
-// Per-edge records in g.edges order with flows (:210-221).
-__device__ void emit_edges(const ClusterDev& cd, const Gs& g, int U, int partial, int lane,
-                           helio_edge* out) {
-  for (int j = lane; j < U; j += 32) {
-    const int k = g.unode[j];
-    const int vi = 2 + 2 * j;
-    const int ai = g.abeg[vi];
-    const double c0 = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (g.pe[k] - g.ps[k]) - 1);
-    double f = c0 - g.cap[ai];
-    if (f < FLOW_EPS) f = 0.0;
-    helio_edge ed;
-    ed.u = vi; ed.v = vi + 1; ed.kind = HELIO_EDGE_COMPUTE;
-    ed.exec_start = g.ps[k]; ed.exec_end = g.pe[k];
-    ed.src_node = k; ed.dst_node = k; ed.pad = 0;
-    ed.cap = c0; ed.flow = f;
-    out[j] = ed;
-  }
-  for (int x = lane; x < 2 + 2 * U; x += 32) g.cur[x] = x >= 2 ? 1 : 0;
-  __syncwarp();
-  int eidx = U;
-  for (int l0 = 0; l0 < cd.Mv; l0 += 32) {
-    const int l = l0 + lane;
-    LinkEval le{false, 0, 0};
-    if (l < cd.Mv) le = eval_link(cd, g, l, partial);
-    const unsigned vm = __ballot_sync(FULL, le.valid);
-    if (vm == 0u) continue;
-    unsigned pu = 0;
-    int cu = 0;
-    if (le.valid) {
-      pu = __match_any_sync(vm, le.u);
-      cu = g.cur[le.u];
-    }
-    __syncwarp();
-    if (le.valid) {
-      const unsigned lt = lanemask_lt();
-      const int fa = g.abeg[le.u] + cu + __popc(pu & lt);
-      const uint32_t pk = __ldg(cd.link_pack + l);
-      const int a = (int)(pk & 0xffffu) - 1, bb = (int)(pk >> 16) - 1;
-      const double c0 = __ldg(cd.link_cap + l);
-      double f = c0 - g.cap[fa];
-      if (f < FLOW_EPS) f = 0.0;
-      helio_edge ed;
-      ed.u = le.u; ed.v = le.v;
-      ed.src_node = a; ed.dst_node = bb; ed.pad = 0;
-      if (a < 0) {
-        ed.kind = HELIO_EDGE_COORD_OUT; ed.exec_start = 0; ed.exec_end = g.pe[bb];
-      } else if (bb < 0) {
-        ed.kind = HELIO_EDGE_COORD_IN; ed.exec_start = cd.L; ed.exec_end = cd.L;
-      } else {
-        ed.kind = HELIO_EDGE_INTERCONNECT; ed.exec_start = g.pe[a]; ed.exec_end = g.pe[bb];
-      }
-      ed.cap = c0; ed.flow = f;
-      out[eidx + __popc(vm & lt)] = ed;
-      if ((pu & lt) == 0u) g.cur[le.u] = (int16_t)(cu + __popc(pu));
-    }
-    eidx += __popc(vm);
-    __syncwarp();
-  }
-}
 
 struct FlowOut {
   helio_edge* edges;  // [B][max_e] or nullptr
