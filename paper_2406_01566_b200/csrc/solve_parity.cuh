@@ -93,6 +93,88 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
     const int b = su.b;
     const int deg = su.deg;
     mark(u, false);
+    if (deg <= 32) {
+      // Single-chunk fast path (almost every vertex): lane j holds arc b + j for
+      // the whole discharge.  A failed ballot means the scan reached the end of
+      // the list, i.e. the reference's relabel (:180).
+      const bool inr = lane < deg;
+      double ca = 0.0;
+      int ta = 0, ra = 0, hta = 0;
+      if (inr) {
+        const int a = b + lane;
+        ca = g.cap[a];
+        ta = g.to[a];
+        ra = g.rv[a];
+        hta = vs[ta].h;
+      }
+      while (ex > FLOW_EPS) {
+        const bool adm = inr && lane >= cu && ca > FLOW_EPS && hu == hta + 1;
+        const unsigned m = __ballot_sync(FULL, adm);
+        if (m != 0u) {
+          const int j = __ffs(m) - 1;
+          cu = j;
+          const double cj = __shfl_sync(FULL, ca, j);
+          const int tj = __shfl_sync(FULL, ta, j);
+          const double amt = ref_min(ex, cj);  // push (:156-166)
+          if (lane == j) {
+            ca -= amt;
+            g.cap[b + j] = ca;
+            g.cap[ra] += amt;
+          }
+          if (lane == 0) vs[tj].ex += amt;
+          ex -= amt;
+          if (tj != s && tj != t && !in_queue(tj)) {
+            mark(tj, true);
+            if (lane == 0) g.q[tail] = (int16_t)tj;
+            tail = tail + 1 == n ? 0 : tail + 1;
+            ++qcount;
+          }
+          continue;
+        }
+        // relabel (:180-199)
+        const int old = hu;
+        const int best = __reduce_min_sync(FULL, (inr && ca > FLOW_EPS) ? hta + 1 : two_n);
+        hu = best;
+        cu = 0;
+        int cold = 0;
+        if (lane == 0) {
+          vs[u].h = (int16_t)best;
+          cold = g.cnt[old] - 1;
+          g.cnt[old] = (int16_t)cold;
+          g.cnt[best] += 1;
+        }
+        cold = __shfl_sync(FULL, cold, 0);
+        __syncwarp();
+        if (old < n && cold == 0) {
+          int moved = 0;
+          for (int x = lane; x < n; x += 32) {
+            const int hx = vs[x].h;
+            if (x != s && hx > old && hx < n) {
+              vs[x].h = (int16_t)(n + 1);
+              ++moved;
+            }
+          }
+          moved = __reduce_add_sync(FULL, moved);
+          for (int hh = old + 1 + lane; hh < n; hh += 32) g.cnt[hh] = 0;
+          __syncwarp();
+          if (lane == 0) g.cnt[n + 1] += (int16_t)moved;
+          if (hu > old && hu < n) hu = n + 1;
+          if (inr) hta = vs[ta].h;
+        }
+        if (inr && ta == u) hta = hu;  // self-loop arcs see u's new height
+        if (best >= two_n) break;
+      }
+      if (lane == 0) {
+        VState w;
+        w.ex = ex;
+        w.h = (int16_t)hu;
+        w.cur = (int16_t)cu;
+        w.b = (int16_t)b;
+        w.deg = (int16_t)deg;
+        vs[u] = w;
+      }
+      continue;
+    }
     int kl = -1;
     bool inr = false;
     double ca = 0.0;
