@@ -260,6 +260,43 @@ def config_table(h, clusters, dev, sp, with_reference):
     return rows
 
 
+def split_leg(eng, dev, sp, B=200_000):
+    """The split K1 -> HBM -> K2 pipeline beside the fused kernel (PARITY), on
+    the headline workload: device times, bytes through HBM, and whether the
+    values are bit-identical."""
+    import numpy as np
+    import torch
+
+    N = eng.num_nodes
+    pl = torch.empty((B, N, 2), dtype=torch.int16, device=f"cuda:{dev}")
+    eng.generate_device(SEED, 0, B, 0, pl.data_ptr(), sp)
+    sb = eng.csr_slab_bytes
+    slabs = torch.empty(B * sb, dtype=torch.uint8, device=pl.device)
+    st = torch.empty(B, dtype=torch.int32, device=pl.device)
+    v_split = torch.empty(B, dtype=torch.float64, device=pl.device)
+    v_fused = torch.empty(B, dtype=torch.float64, device=pl.device)
+    mode = eng.mode
+    eng.mode = "parity"
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    cur = torch.cuda.current_stream(pl.device)
+    for it in range(3):
+        ev[0].record(cur)
+        eng.build_csr_device(pl.data_ptr(), B, slabs.data_ptr(), st.data_ptr(), True, sp)
+        ev[1].record(cur)
+        eng.solve_csr_device(slabs.data_ptr(), B, v_split.data_ptr(), st.data_ptr(), sp)
+        ev[2].record(cur)
+        eng.score_device(pl.data_ptr(), B, v_fused.data_ptr(), st.data_ptr(), True, sp)
+        ev[3].record(cur)
+        torch.cuda.synchronize(pl.device)
+    eng.mode = mode
+    k1, k2, fused = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])
+    same = bool(torch.equal(v_split.view(torch.int64), v_fused.view(torch.int64)))
+    return {"candidates": B, "slab_bytes": sb, "k1_build_ms": k1, "k2_solve_ms": k2, "fused_ms": fused,
+            "split_evals_per_s": B / ((k1 + k2) / 1e3), "fused_evals_per_s": B / (fused / 1e3),
+            "k1_write_gbs": B * sb / (k1 / 1e3) / 1e9, "k2_read_gbs": B * sb / (k2 / 1e3) / 1e9,
+            "bit_identical_to_fused": same}
+
+
 def run_reference(args):
     rank = env_int("RANK", 0)
     if rank != 0:
@@ -466,6 +503,13 @@ def main():
                "call": "helio_gpu_score_best_host (pinned host placements in; every value + status and the "
                        "first-max winner out)"}
 
+    split = None
+    if rank == 0 and not args.no_configs:
+        try:
+            split = split_leg(eng, local, sp)
+        except Exception as ex:  # reported, never fatal
+            split = {"error": str(ex)}
+
     cfg_table = None
     if rank == 0 and not args.no_configs:
         try:
@@ -506,7 +550,7 @@ def main():
                        "nonzero_fraction": nonzero, "status_nonzero": int((st_host != 0).sum()),
                        "best": {"value": win[0], "index": win[1]}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "routing": routing, "other_configs": cfg_table,
+            "routing": routing, "other_configs": cfg_table, "split_pipeline": split,
             "clocks": clk.summary(),
         }
         print(json.dumps(out))

@@ -144,6 +144,22 @@ int helio_gpu_score_best_host(helio_gpu_ctx* ctx, const int16_t* h_placements, i
                               int allow_partial, double* h_values, int32_t* h_status,
                               double* h_best, int64_t* h_index);
 
+/* The split K1 -> HBM -> K2 pipeline (north_star's builder and solver as
+ * separate launches; the fused helio_gpu_score is the production path).
+ * helio_gpu_build_csr writes each candidate's flow network — the reference's
+ * vertex, edge and per-vertex arc order — to a fixed-size slab of
+ * helio_gpu_csr_slab_bytes() bytes: int32 {V, E, status, 0}, int32 arc
+ * offsets [V+1], int32 arcs (head | reverse-arc << 16) [2E], float64
+ * capacities [2E] (each section 16-byte aligned).  helio_gpu_solve_csr runs
+ * the PARITY solver on the slabs; values are bit-identical to
+ * helio_gpu_score in PARITY mode.  Graphs larger than the slab get
+ * HELIO_CAND_TOO_LARGE. */
+int64_t helio_gpu_csr_slab_bytes(const helio_gpu_ctx* ctx);
+int helio_gpu_build_csr(helio_gpu_ctx* ctx, const int16_t* d_placements, int64_t B, int allow_partial,
+                        void* d_slabs, int32_t* d_status, void* stream);
+int helio_gpu_solve_csr(helio_gpu_ctx* ctx, const void* d_slabs, int64_t B, double* d_values,
+                        int32_t* d_status, void* stream);
+
 /* Full FlowGraph (edges in reference order, with max_flow's per-edge flows)
  * for K candidates; synchronous, host buffers.  h_edges is [K][max_edges]. */
 int helio_gpu_flows_host(helio_gpu_ctx* ctx, const int16_t* h_placements, int64_t K,

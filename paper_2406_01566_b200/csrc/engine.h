@@ -72,7 +72,7 @@ struct helio_gpu_ctx {
   bool big_ok = false;
 
   // scratch, two sets (one per pipeline stream)
-  unsigned long long* d_work = nullptr;  // [4]
+  unsigned long long* d_work = nullptr;  // [8]: score sets 0/1 use [0,1]/[2,3], split.cu [4]/[5]
   unsigned int* d_ovf_count = nullptr;   // [2]
   int64_t* d_ovf[2] = {nullptr, nullptr};
   int64_t ovf_cap[2] = {0, 0};

@@ -452,7 +452,7 @@ int helio_gpu_create(int device, helio_gpu_ctx** out) {
       cudaStreamCreateWithFlags(&ctx->pipe[0], cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->pipe[1], cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
-      cudaMalloc(&ctx->d_work, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_work, 8 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMalloc(&ctx->d_ovf_count, 2 * sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc(&ctx->d_pv, 3 * 4096 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&ctx->d_pi, 3 * 4096 * sizeof(long long)) != cudaSuccess ||

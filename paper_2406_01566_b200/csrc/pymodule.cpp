@@ -757,6 +757,27 @@ PYBIND11_MODULE(_helio, m) {
             return out;
           },
           py::arg("seed"), py::arg("first"), py::arg("count"))
+      .def_property_readonly("csr_slab_bytes", [](const PyEngine& e) { return helio_gpu_csr_slab_bytes(e.eng->ctx()); })
+      .def(
+          "build_csr_device",
+          [](PyEngine& e, uintptr_t pl, int64_t B, uintptr_t slabs, uintptr_t status, bool allow_partial,
+             uintptr_t stream) {
+            e.eng->check(helio_gpu_build_csr(e.eng->ctx(), reinterpret_cast<const int16_t*>(pl), B, allow_partial ? 1 : 0,
+                                             reinterpret_cast<void*>(slabs), reinterpret_cast<int32_t*>(status),
+                                             reinterpret_cast<void*>(stream)),
+                         "helio_gpu_build_csr");
+          },
+          py::arg("placements_ptr"), py::arg("count"), py::arg("slabs_ptr"), py::arg("status_ptr"),
+          py::arg("allow_partial") = true, py::arg("stream") = 0)
+      .def(
+          "solve_csr_device",
+          [](PyEngine& e, uintptr_t slabs, int64_t B, uintptr_t values, uintptr_t status, uintptr_t stream) {
+            e.eng->check(helio_gpu_solve_csr(e.eng->ctx(), reinterpret_cast<const void*>(slabs), B,
+                                             reinterpret_cast<double*>(values), reinterpret_cast<int32_t*>(status),
+                                             reinterpret_cast<void*>(stream)),
+                         "helio_gpu_solve_csr");
+          },
+          py::arg("slabs_ptr"), py::arg("count"), py::arg("values_ptr"), py::arg("status_ptr"), py::arg("stream") = 0)
       .def(
           "argmax_device",
           [](PyEngine& e, uintptr_t values, uintptr_t status, int64_t B, int64_t base, uintptr_t best, uintptr_t index,

@@ -337,3 +337,30 @@ def test_walk_generator_device_matches_host_and_syn256_walk_parity():
     v, s = e.score(sub)
     assert np.array_equal(s, so)
     assert np.all(np.abs(v - vo) <= 1e-6 * np.maximum(1.0, np.abs(vo)))
+
+
+@pytest.mark.parametrize("key", ["het42-70b_float", "geo24_float", "single24-30b_int", "syn256-120l_float"])
+def test_split_pipeline_bit_exact_with_fused(key):
+    import torch
+    c, e = engine(key)
+    z = golden(f"cand_{key}.npz")
+    rows = np.concatenate([z["rows"], h.generate_host(list(e.kmax), c.num_layers, 3, 0, 3000, 100000)])
+    B = len(rows)
+    pl = torch.from_numpy(rows).cuda()
+    slabs = torch.empty(B * e.csr_slab_bytes, dtype=torch.uint8, device="cuda")
+    st1 = torch.empty(B, dtype=torch.int32, device="cuda")
+    st2 = torch.empty(B, dtype=torch.int32, device="cuda")
+    v = torch.empty(B, dtype=torch.float64, device="cuda")
+    e.build_csr_device(pl.data_ptr(), B, slabs.data_ptr(), st1.data_ptr(), True, 0)
+    e.solve_csr_device(slabs.data_ptr(), B, v.data_ptr(), st2.data_ptr(), 0)
+    torch.cuda.synchronize()
+    vf, sf = e.score(rows, True)  # fused PARITY
+    s2 = st2.cpu().numpy()
+    ok = s2 != 4  # graphs beyond the slab report TOO_LARGE in the split path
+    assert np.array_equal(s2[ok], sf[ok]) and np.array_equal(st1.cpu().numpy(), s2)
+    assert np.array_equal(bits(v.cpu().numpy()[ok]), bits(vf[ok]))
+    if not key.startswith("syn256"):
+        assert ok.all()
+    # slab layout: meta V, E, status
+    meta = slabs.view(B, -1)[:, :16].cpu().numpy().view(np.int32)
+    assert np.array_equal(meta[:, 2], s2)
