@@ -291,9 +291,12 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   const int N = ctx->N, V = 2 * N + 2;
   ctx->Vmax = V;
   // Small slot: sized for the common case; rarer dense graphs overflow to the
-  // big slot.  Arc budget 2 * (4N + 16) edges: covering chains average E ~3.3N
-  // (het42: mean 140, p99 159, max 165 of 184; geo24 p99 98 of 112).
-  int a_small = 2 * (4 * N + 16);
+  // big slot.  Arc budget 8N (4N edges): covering chains average E ~3.3N
+  // (het42: mean 140, p99 159, max seen 165 of 168), and at N = 42 the slot
+  // (12A + 27V + 8N bytes = 6.7 KB) lets 8 four-warp CTAs share an SM — the
+  // register limit at 64 registers — instead of 7.
+  int a_small = 8 * N;
+  if (a_small < 2 * ctx->L + 2) a_small = 2 * ctx->L + 2;  // cover/start masks live in cap[]
   int a_struct = 2 * (N + ctx->Mv);
   if (a_small > a_struct) a_small = a_struct;
   if (a_small < 2) a_small = 2;
