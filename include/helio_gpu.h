@@ -23,7 +23,9 @@
  * throws across the ABI; helio_gpu_last_error() holds the message of the last
  * failure.  Buffers are caller-owned.  "d_" pointers are device memory,
  * "h_" pointers host memory (pinned or pageable).  A context is bound to one
- * device and is thread-compatible, not thread-safe.  `stream` is a
+ * device; concurrent calls on one context are serialised by the context
+ * (graphs may be solved from many threads); use one context per
+ * thread for parallelism.  `stream` is a
  * cudaStream_t (NULL = the context's own stream).
  *
  * Placements are int16 [B][N][2] rows (start, end) in the cluster's declared

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -46,6 +47,7 @@ struct Layout {
 }  // namespace helio_engine
 
 struct helio_gpu_ctx {
+  mutable std::recursive_mutex mu;  // every C ABI entry holds it: a context serialises its callers
   int device = 0;
   int sm_count = 148;
   cudaStream_t stream = nullptr;

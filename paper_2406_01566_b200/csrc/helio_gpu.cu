@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -504,6 +505,7 @@ const char* helio_gpu_last_error(const helio_gpu_ctx* ctx) { return ctx ? ctx->e
 
 int helio_gpu_sync(helio_gpu_ctx* ctx) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaStreamSynchronize(ctx->pipe[0]));
@@ -520,6 +522,7 @@ int helio_gpu_sync(helio_gpu_ctx* ctx) {
 // add_merged_edge does (flow_graph.cpp:25-34).
 int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32_t* k_out) {
   if (!ctx || !d) return fail(ctx, HELIO_ERR_INVALID, "null argument");
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   CK(cudaSetDevice(ctx->device));
   const int N = d->num_nodes, M = d->num_links, L = d->num_layers;
   if (N < 1 || N > 16000) return fail(ctx, HELIO_ERR_INVALID, "num_nodes must be in [1, 16000]");
@@ -762,6 +765,7 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
 
 int helio_gpu_set_mode(helio_gpu_ctx* ctx, int mode) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (mode != HELIO_MODE_PARITY && mode != HELIO_MODE_SCORE) return fail(ctx, HELIO_ERR_INVALID, "unknown mode");
   ctx->mode = mode;
   return HELIO_OK;
@@ -770,7 +774,9 @@ int helio_gpu_set_mode(helio_gpu_ctx* ctx, int mode) {
 int helio_gpu_get_mode(const helio_gpu_ctx* ctx) { return ctx ? ctx->mode : -1; }
 
 int helio_gpu_compute_edge_capacity(const helio_gpu_ctx* ctx, int32_t node, int32_t j, double* out) {
-  if (!ctx || !ctx->has_cluster || !out) return HELIO_ERR_NO_CLUSTER;
+  if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+  if (!ctx->has_cluster || !out) return HELIO_ERR_NO_CLUSTER;
   if (node < 0 || node >= ctx->N || j < 1 || j > ctx->h_kmax[node]) return HELIO_ERR_INVALID;
   *out = ctx->h_cap_tab[ctx->h_cap_off[node] + j - 1];
   return HELIO_OK;
@@ -779,6 +785,7 @@ int helio_gpu_compute_edge_capacity(const helio_gpu_ctx* ctx, int32_t node, int3
 int helio_gpu_score(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int allow_partial,
                     double* d_values, int32_t* d_status, void* stream) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (B < 0 || (B > 0 && (!d_pl || !d_values || !d_status))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   CK(cudaSetDevice(ctx->device));
@@ -801,6 +808,7 @@ int argmax_on(helio_gpu_ctx* ctx, int scratch, const double* d_values, const int
 int score_host_impl(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allow_partial, double* h_values,
                     int32_t* h_status, double* h_best, int64_t* h_index) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (B < 0 || (B > 0 && (!h_pl || (!h_values) != (!h_status) || (!h_values && !h_best))))
     return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
@@ -900,6 +908,7 @@ int helio_gpu_flows_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t K, int
                          int32_t max_edges, int32_t* h_nv, int32_t* h_ne, helio_edge* h_edges,
                          double* h_values, int32_t* h_status) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (K <= 0) return HELIO_OK;
   if (!h_pl || !h_nv || !h_ne || !h_values || !h_status || max_edges < 0 || (max_edges > 0 && !h_edges))
@@ -943,6 +952,7 @@ int helio_gpu_maxflow_raw_host(helio_gpu_ctx* ctx, int64_t G, const int32_t* h_n
                                const int32_t* h_v, const double* h_cap, double* h_values,
                                double* h_flows) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (G <= 0) return HELIO_OK;
   if (!h_n || !h_s || !h_t || !h_off || !h_values) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   CK(cudaSetDevice(ctx->device));
@@ -1031,6 +1041,7 @@ extern "C" {
 int helio_gpu_argmax(helio_gpu_ctx* ctx, const double* d_values, const int32_t* d_status, int64_t B,
                      int64_t index_base, double* d_best, int64_t* d_index, void* stream) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!d_best || !d_index || (B > 0 && (!d_values || !d_status))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
@@ -1040,6 +1051,7 @@ int helio_gpu_argmax(helio_gpu_ctx* ctx, const double* d_values, const int32_t* 
 int helio_gpu_generate(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B, uint32_t ppm,
                        int16_t* d_out, void* stream) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (ctx->N > GEN_MAX_N) return fail(ctx, HELIO_ERR_TOO_LARGE, "generator supports up to 1024 nodes");
   if (B <= 0) return HELIO_OK;
@@ -1055,6 +1067,7 @@ int helio_gpu_generate(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t
 int helio_gpu_generate_walk(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B, int16_t* d_out,
                             void* stream) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (ctx->N > GEN_MAX_N) return fail(ctx, HELIO_ERR_TOO_LARGE, "generator supports up to 1024 nodes");
   if (B <= 0) return HELIO_OK;
@@ -1070,7 +1083,9 @@ int helio_gpu_generate_walk(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, in
 
 int helio_gpu_generate_walk_host(const helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B,
                                  int16_t* h_out) {
-  if (!ctx || !ctx->has_cluster || (B > 0 && !h_out)) return HELIO_ERR_INVALID;
+  if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+  if (!ctx->has_cluster || (B > 0 && !h_out)) return HELIO_ERR_INVALID;
   std::vector<uint32_t> used((ctx->N + 31) / 32 + 1);
   for (int64_t i = 0; i < B; ++i)
     hg_candidate_walk(ctx->h_kmax.data(), ctx->N, ctx->L, seed, (uint64_t)(first + i), ctx->h_walk_beg.data(),

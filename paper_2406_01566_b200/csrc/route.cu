@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <vector>
 
@@ -225,6 +226,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
                                     int32_t* h_nh, int32_t* h_hn, int32_t* h_hs, int32_t* h_he,
                                     int64_t* h_deferred) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (!h_pl || (ne > 0 && !pe) || R < 0 || max_hops < 0 || (R > 0 && (!h_in || !h_out || !h_nh)) ||
       (R > 0 && max_hops > 0 && (!h_hn || (!h_hs) != (!h_he))))
@@ -498,6 +500,7 @@ __global__ void iwrr_picks_kernel(int n, const long long* __restrict__ w, long l
 
 extern "C" int helio_gpu_iwrr_weights(helio_gpu_ctx* ctx, const double* h_flows, int32_t n, int64_t* h_w) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (n < 0 || (n > 0 && (!h_flows || !h_w))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   if (n == 0) return HELIO_OK;
   CK(cudaSetDevice(ctx->device));
@@ -519,6 +522,7 @@ extern "C" int helio_gpu_iwrr_weights(helio_gpu_ctx* ctx, const double* h_flows,
 extern "C" int helio_gpu_iwrr_picks(helio_gpu_ctx* ctx, const int64_t* h_w, int32_t n, int64_t* h_round,
                                     int64_t* h_idx, int32_t calls, const uint64_t* h_masks, int32_t* h_out) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (n < 0 || calls < 0 || !h_round || !h_idx || (n > 0 && !h_w) || (calls > 0 && (!h_out || (n > 0 && !h_masks))))
     return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   if (calls == 0) return HELIO_OK;

@@ -13,6 +13,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "engine.h"
@@ -68,6 +69,7 @@ extern "C" int helio_gpu_best_exhaustive(helio_gpu_ctx* ctx, int allow_partial, 
                                          double* h_best_value, int16_t* h_best_row, int64_t* h_scored,
                                          int64_t* h_total) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (!h_best_value || !h_best_row) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   const int N = ctx->N, L = ctx->L;

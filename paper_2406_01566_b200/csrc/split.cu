@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <climits>
 #include <cstring>
 #include <string>
@@ -174,6 +175,7 @@ extern "C" int64_t helio_gpu_csr_slab_bytes(const helio_gpu_ctx* ctx) {
 extern "C" int helio_gpu_build_csr(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int allow_partial,
                                    void* d_slabs, int32_t* d_status, void* stream) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (B < 0 || (B > 0 && (!d_pl || !d_slabs || !d_status))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   if (B == 0) return HELIO_OK;
@@ -197,6 +199,7 @@ extern "C" int helio_gpu_build_csr(helio_gpu_ctx* ctx, const int16_t* d_pl, int6
 extern "C" int helio_gpu_solve_csr(helio_gpu_ctx* ctx, const void* d_slabs, int64_t B, double* d_values,
                                    int32_t* d_status, void* stream) {
   if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (B < 0 || (B > 0 && (!d_slabs || !d_values || !d_status))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   if (B == 0) return HELIO_OK;

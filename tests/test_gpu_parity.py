@@ -365,3 +365,21 @@ def test_split_pipeline_bit_exact_with_fused(key):
     # slab layout: meta V, E, status
     meta = slabs.view(B, -1)[:, :16].cpu().numpy().view(np.int32)
     assert np.array_equal(meta[:, 2], s2)
+
+
+def test_concurrent_callers_on_one_engine():
+    # graphs may be solved concurrently — a shared context
+    # serialises its callers, results equal the sequential ones
+    from concurrent.futures import ThreadPoolExecutor
+    c, e = engine("geo24_float")
+    batches = [h.generate_host(list(e.kmax), c.num_layers, 1000 + i, 0, 20_000, 50_000) for i in range(8)]
+    want = [e.score(b) for b in batches]
+
+    def job(i):
+        return e.score(batches[i]), h.plan_for_placement(c, {"a0": (0, 12), "a1": (12, 24)}).objective
+
+    with ThreadPoolExecutor(8) as ex:
+        got = list(ex.map(job, range(8)))
+    for (v, s), ((gv, gs), obj) in zip(want, got):
+        assert np.array_equal(bits(v), bits(gv)) and np.array_equal(s, gs)
+    assert len({obj for _, obj in got}) == 1
