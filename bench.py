@@ -335,7 +335,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="het42-70b")
@@ -503,22 +503,24 @@ def main():
                "call": "helio_gpu_score_best_host (pinned host placements in; every value + status and the "
                        "first-max winner out)"}
 
+    # extras (single-GPU views) only at N = 1: at N > 1 the other ranks must not
+    # wait on rank 0 outside the timed region
     split = None
-    if rank == 0 and not args.no_configs:
+    if world == 1 and not args.no_configs:
         try:
             split = split_leg(eng, local, sp)
         except Exception as ex:  # reported, never fatal
             split = {"error": str(ex)}
 
     cfg_table = None
-    if rank == 0 and not args.no_configs:
+    if world == 1 and not args.no_configs:
         try:
             cfg_table = config_table(h, clusters, local, sp, with_reference=(world == 1 and not args.no_cpu_baseline))
         except Exception as ex:  # reported, never fatal
             cfg_table = [{"error": str(ex)}]
 
     routing = None
-    if rank == 0 and not args.no_routing:
+    if world == 1 and not args.no_routing:
         try:
             routing = routing_leg(h, clusters, local, sp, args.route_requests,
                                   with_reference=(world == 1 and not args.no_cpu_baseline))
