@@ -44,6 +44,27 @@ def env_int(k, d):
         return d
 
 
+PROFILE_GRAPHS = 200_000  # tools/profile_score.py default: candidates in the profiled launch
+
+
+def ncu_traffic_per_eval(mode):
+    """DRAM bytes (read + write) per candidate of the committed ncu --set full
+    capture of score_kernel in this mode (profiles/r01_<mode>_mode_raw.csv)."""
+    import csv
+    path = os.path.join(ROOT, "profiles", f"r01_{mode}_mode_raw.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+        h, u, v = rows[0], rows[1], rows[2]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(name)
+            tot += float(v[i].replace(",", "")) * scale.get(u[i], 1.0)
+        return tot / PROFILE_GRAPHS, os.path.relpath(path, ROOT)
+    except Exception:
+        return None, None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -290,8 +311,12 @@ def split_leg(eng, dev, sp, B=200_000):
         torch.cuda.synchronize(pl.device)
     eng.mode = mode
     k1, k2, fused = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])
-    same = bool(torch.equal(v_split.view(torch.int64), v_fused.view(torch.int64)))
-    return {"candidates": B, "slab_bytes": sb, "k1_build_ms": k1, "k2_solve_ms": k2, "fused_ms": fused,
+    eng.solve_csr_device(slabs.data_ptr(), B, v_split.data_ptr(), st.data_ptr(), sp)  # statuses of the split path
+    torch.cuda.synchronize(pl.device)
+    ok = st == 0  # graphs denser than the slab are refused (the fused path finishes them in its large slot)
+    same = bool(torch.equal(v_split[ok].view(torch.int64), v_fused[ok].view(torch.int64)))
+    return {"candidates": B, "slab_bytes": sb, "refused_fraction": float((~ok).float().mean().item()),
+            "k1_build_ms": k1, "k2_solve_ms": k2, "fused_ms": fused,
             "split_evals_per_s": B / ((k1 + k2) / 1e3), "fused_evals_per_s": B / (fused / 1e3),
             "k1_write_gbs": B * sb / (k1 / 1e3) / 1e9, "k2_read_gbs": B * sb / (k2 / 1e3) / 1e9,
             "bit_identical_to_fused": same}
@@ -468,8 +493,13 @@ def main():
     avg_kernel_ms = sum(kms) / len(kms) if kms else ms_per_step
     achieved = bytes_per_eval * B / (avg_kernel_ms / 1e3) / 1e9
     peak, peak_src = load_peaks()
+    tpe, tsrc = ncu_traffic_per_eval(args.mode)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak,
+                "traffic": (tpe * B) if tpe is not None else None,
+                "traffic_unit": "bytes per launch (DRAM read + write)",
+                "traffic_source": f"{tsrc}: ncu --set full of one {PROFILE_GRAPHS}-candidate launch, per candidate x {B}",
+                "algorithmic_bytes_per_launch": bytes_per_eval * B,
                 "kernel": f"score_kernel<{args.mode}> (fused K1 build + K2 solve, one warp per graph)",
                 "kernel_ms": avg_kernel_ms, "kernel_share_of_step": avg_kernel_ms / ms_per_step,
                 "bytes_per_eval": bytes_per_eval, "peak_source": peak_src,
