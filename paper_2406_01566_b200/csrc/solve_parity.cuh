@@ -99,16 +99,17 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
       // the list, i.e. the reference's relabel (:180).
       const bool inr = lane < deg;
       double ca = 0.0;
-      int ta = 0, ra = 0, hta = 0;
+      int ta = 0, ra = 0, hp1 = 0;  // hp1 = height[to] + 1
       if (inr) {
         const int a = b + lane;
         ca = g.cap[a];
         ta = g.to[a];
         ra = g.rv[a];
-        hta = vs[ta].h;
+        hp1 = vs[ta].h + 1;
       }
+      bool live = inr && ca > FLOW_EPS;  // residual arc: changes only when this lane pushes
       while (ex > FLOW_EPS) {
-        const bool adm = inr && lane >= cu && ca > FLOW_EPS && hu == hta + 1;
+        const bool adm = live && lane >= cu && hu == hp1;
         const unsigned m = __ballot_sync(FULL, adm);
         if (m != 0u) {
           const int j = __ffs(m) - 1;
@@ -118,6 +119,7 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
           const double amt = ref_min(ex, cj);  // push (:156-166)
           if (lane == j) {
             ca -= amt;
+            live = ca > FLOW_EPS;
             g.cap[b + j] = ca;
             g.cap[ra] += amt;
           }
@@ -133,7 +135,7 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
         }
         // relabel (:180-199)
         const int old = hu;
-        const int best = __reduce_min_sync(FULL, (inr && ca > FLOW_EPS) ? hta + 1 : two_n);
+        const int best = __reduce_min_sync(FULL, live ? hp1 : two_n);
         hu = best;
         cu = 0;
         int cold = 0;
@@ -159,9 +161,9 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
           __syncwarp();
           if (lane == 0) g.cnt[n + 1] += (int16_t)moved;
           if (hu > old && hu < n) hu = n + 1;
-          if (inr) hta = vs[ta].h;
+          if (inr) hp1 = vs[ta].h + 1;
         }
-        if (inr && ta == u) hta = hu;  // self-loop arcs see u's new height
+        if (inr && ta == u) hp1 = hu + 1;  // self-loop arcs see u's new height
         if (best >= two_n) break;
       }
       if (lane == 0) {

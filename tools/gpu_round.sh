@@ -1,5 +1,3 @@
 set -x
-timeout 900 python bench.py > gpurun_out/bench_final.log 2>&1; echo bench=$?; tail -1 gpurun_out/bench_final.log | cut -c1-300
-timeout 300 python tools/profile_score.py --mode score > gpurun_out/prof_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_kernel -c 1 -o gpurun_out/r01_score python tools/profile_score.py --mode score > gpurun_out/ncu_s.log 2>&1; echo ncu_s=$?
-timeout 300 python tools/profile_score.py --mode parity > gpurun_out/prof_plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_kernel -c 1 -o gpurun_out/r01_parity python tools/profile_score.py --mode parity > gpurun_out/ncu_p.log 2>&1; echo ncu_p=$?
-timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-routing --no-configs > gpurun_out/plain_launch.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-routing --no-configs > gpurun_out/ncu_launch.log 2>&1; echo ncu_l=$?
+timeout 900 python -m pytest tests -q -m gpu --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --no-routing --no-configs --no-cpu-baseline > gpurun_out/bench_full.log 2>&1; echo bench=$?; tail -1 gpurun_out/bench_full.log | cut -c1-150; grep -o '"other_mode": {[^}]*}' gpurun_out/bench_full.log
