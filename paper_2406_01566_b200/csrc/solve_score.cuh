@@ -136,133 +136,146 @@ __device__ double solve_ek_batched(const Gs& g, const int n, const int s, const 
 }
 
 // SCORE solver for n <= 128: Edmonds-Karp with a level-synchronous bitset
-// BFS.  Lane l owns vertices l, l+32, l+64, l+96 and keeps, in registers, the
-// set of their residual out-neighbours (two 64-bit words per vertex).  One
-// BFS level is: OR the rows of owned frontier vertices, REDUX.OR across the
-// warp, mask with the visited set.  Only BFS levels are stored; the
-// augmenting path is recovered backwards from the sink (at each step the
-// first arc, in adjacency order, from a vertex one level closer to the
-// source with residual capacity).  Deterministic; exact on integer
-// capacities like every SCORE path.
-__device__ __forceinline__ bool bit128(unsigned long long w0, unsigned long long w1, int x) {
-  return ((x < 64 ? w0 : w1) >> (x & 63)) & 1ull;
-}
-
-__device__ __forceinline__ unsigned long long warp_or64(unsigned long long v) {
-  const unsigned lo = __reduce_or_sync(FULL, (unsigned)(v & 0xffffffffull));
-  const unsigned hi = __reduce_or_sync(FULL, (unsigned)(v >> 32));
-  return ((unsigned long long)hi << 32) | lo;
-}
-
-// Pair closure: in this numbering a node's vertices are v and v^1 (in = 2+2k,
-// out = 3+2k), joined by its compute arc.  When a BFS level reaches one half
-// of a node whose pair arc has residual capacity, the other half joins the
-// same level (a shift on the 128-bit frontier), so the BFS walks nodes rather
-// than split vertices and needs about half the levels.  Paths remain valid
-// augmenting paths and the choice stays deterministic.
-__device__ __forceinline__ unsigned long long swap_pairs(unsigned long long x) {
-  return ((x & 0x5555555555555555ull) << 1) | ((x & 0xAAAAAAAAAAAAAAAAull) >> 1);
+// BFS.  Vertex sets are four 32-bit words (vertex v = bit v & 31 of word
+// v >> 5), so lane l owns vertices l, l+32, l+64, l+96 and its bit in every
+// word is simply bit l.  R[v] (shared memory) is the set of residual
+// out-neighbours of v, kept exact by the augmentations.
+//
+// Pair closure: in this numbering a node's two vertices are v and v^1 (in =
+// 2+2k, out = 3+2k), joined by its compute arc.  When a level reaches one
+// half of a node whose pair arc has residual capacity, the other half joins
+// the same level, so the BFS walks nodes rather than split vertices and needs
+// about half the levels.  It is folded into each lane's rows once per
+// augmentation: Q[v] = R[v] | swap(R[v] & P), P = vertices whose pair arc has
+// residual capacity.  A level is then: OR the Q rows of owned frontier
+// vertices, four REDUX.OR, mask with the visited set.
+//
+// Path recovery: a vertex at level d takes the first arc (adjacency order)
+// from a level d-1 vertex with residual capacity; a vertex without one was
+// added through its partner's pair arc.  Paths are valid augmenting paths,
+// chosen deterministically.
+__device__ __forceinline__ unsigned swap_pairs32(unsigned x) {
+  return ((x & 0x55555555u) << 1) | ((x >> 1) & 0x55555555u);
 }
 
 __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int t, const int lane) {
-  // rows R[x] (residual out-neighbours of x, 128 bits) in the VState region;
-  // per-vertex BFS code (2*level, +1 if added by the pair closure) in the
-  // count region; canonical parent arc per vertex in `cur`; the augmenting
-  // path in the queue region.
-  ulonglong2* R = reinterpret_cast<ulonglong2*>(g.vs);
+  // R in the VState region; BFS level per vertex in the count region;
+  // parent arc per vertex in `cur`; the augmenting path in the queue region.
+  uint4* R = reinterpret_cast<uint4*>(g.vs);
   int16_t* dist = g.cnt;
   int16_t* par = g.cur;
   int16_t* path = g.q;
+  const unsigned lb = 1u << lane;
   for (int x = lane; x < n; x += 32) {
-    unsigned long long r0 = 0ull, r1 = 0ull;
-    for (int a = g.abeg[x], e = g.abeg[x + 1]; a < e; ++a) {
+    unsigned r[4] = {0u, 0u, 0u, 0u};
+    for (int a = g.abeg[x], e = g.abeg[x + 1]; a < e; ++a)
       if (g.cap[a] > FLOW_EPS) {
         const int y = g.to[a];
-        if (y < 64) r0 |= 1ull << y;
-        else r1 |= 1ull << (y - 64);
+        r[y >> 5] |= 1u << (y & 31);
       }
-    }
-    R[x] = make_ulonglong2(r0, r1);
+    R[x] = make_uint4(r[0], r[1], r[2], r[3]);
   }
   __syncwarp();
   double value = 0.0;
   for (;;) {
-    // pair arcs with residual capacity: bit v set iff R[v] holds v^1 (v >= 2)
-    unsigned long long P0, P1;
-    {
-      unsigned b[4];
+    // P: vertices v >= 2 whose pair arc v -> v^1 has residual capacity; then
+    // this lane's closure rows Q
+    uint4 Q[4];
+    unsigned P[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int v = lane + 32 * i;
-        bool pr = false;
-        if (v >= 2 && v < n) {
-          const ulonglong2 r = R[v];
+    for (int i = 0; i < 4; ++i) {
+      const int v = lane + 32 * i;
+      bool pr = false;
+      Q[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (v < n) {
+        Q[i] = R[v];
+        if (v >= 2) {
           const int w = v ^ 1;
-          pr = ((w < 64 ? r.x : r.y) >> (w & 63)) & 1ull;
+          const unsigned ww = (w >> 5) == 0 ? Q[i].x : (w >> 5) == 1 ? Q[i].y : (w >> 5) == 2 ? Q[i].z : Q[i].w;
+          pr = (ww >> (w & 31)) & 1u;
         }
-        b[i] = __ballot_sync(FULL, pr);
       }
-      P0 = ((unsigned long long)b[1] << 32) | b[0];
-      P1 = ((unsigned long long)b[3] << 32) | b[2];
+      P[i] = __ballot_sync(FULL, pr);
     }
-    for (int x = lane; x < n; x += 32) dist[x] = (int16_t)(x == s ? 0 : -1);
-    unsigned long long F0 = s < 64 ? (1ull << s) : 0ull, F1 = s < 64 ? 0ull : (1ull << (s - 64));
-    unsigned long long V0 = F0, V1 = F1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      Q[i].x |= swap_pairs32(Q[i].x & P[0]);
+      Q[i].y |= swap_pairs32(Q[i].y & P[1]);
+      Q[i].z |= swap_pairs32(Q[i].z & P[2]);
+      Q[i].w |= swap_pairs32(Q[i].w & P[3]);
+    }
+    // BFS levels from s
+    unsigned F[4] = {0u, 0u, 0u, 0u}, Vs[4];
+    F[s >> 5] = 1u << (s & 31);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) Vs[k] = F[k];
+    int dl[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dl[i] = (lane + 32 * i == s) ? 0 : -1;
     int d = 0;
     bool found = false;
     for (;;) {
-      unsigned long long a0 = 0ull, a1 = 0ull;
+      unsigned a0 = 0u, a1 = 0u, a2 = 0u, a3 = 0u;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const unsigned long long w = (i < 2) ? F0 : F1;
-        if ((w >> (lane + 32 * (i & 1))) & 1ull) {
-          const ulonglong2 r = R[lane + 32 * i];
-          a0 |= r.x;
-          a1 |= r.y;
+      for (int i = 0; i < 4; ++i)
+        if (F[i] & lb) {
+          a0 |= Q[i].x;
+          a1 |= Q[i].y;
+          a2 |= Q[i].z;
+          a3 |= Q[i].w;
         }
-      }
-      unsigned long long n0 = warp_or64(a0) & ~V0;
-      unsigned long long n1 = warp_or64(a1) & ~V1;
-      if ((n0 | n1) == 0ull) break;
+      const unsigned n0 = __reduce_or_sync(FULL, a0) & ~Vs[0];
+      const unsigned n1 = __reduce_or_sync(FULL, a1) & ~Vs[1];
+      const unsigned n2 = __reduce_or_sync(FULL, a2) & ~Vs[2];
+      const unsigned n3 = __reduce_or_sync(FULL, a3) & ~Vs[3];
+      if ((n0 | n1 | n2 | n3) == 0u) break;
       ++d;
-      const unsigned long long c0 = swap_pairs(n0 & P0) & ~V0 & ~n0;
-      const unsigned long long c1 = swap_pairs(n1 & P1) & ~V1 & ~n1;
-      n0 |= c0;
-      n1 |= c1;
-      V0 |= n0;
-      V1 |= n1;
+      Vs[0] |= n0;
+      Vs[1] |= n1;
+      Vs[2] |= n2;
+      Vs[3] |= n3;
+      F[0] = n0;
+      F[1] = n1;
+      F[2] = n2;
+      F[3] = n3;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int sh = lane + 32 * (i & 1);
-        const unsigned long long w = (i < 2) ? n0 : n1;
-        const unsigned long long cw = (i < 2) ? c0 : c1;
-        if ((w >> sh) & 1ull) dist[lane + 32 * i] = (int16_t)(2 * d + (int)((cw >> sh) & 1ull));
-      }
-      F0 = n0;
-      F1 = n1;
-      if (bit128(n0, n1, t)) {
+      for (int i = 0; i < 4; ++i) dl[i] = (F[i] & lb) ? d : dl[i];
+      if ((F[t >> 5] >> (t & 31)) & 1u) {
         found = true;
         break;
       }
     }
     if (!found) break;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < n) dist[lane + 32 * i] = (int16_t)dl[i];
     __syncwarp();
-    // canonical parent of every visited vertex: a closure vertex takes its
-    // pair arc; otherwise the first arc, in adjacency order, back to a vertex
-    // of the previous level with residual capacity
-    for (int x = lane; x < n; x += 32) {
-      const int cx = dist[x];
-      if (cx <= 0) continue;
-      const int want = (cx >> 1) - 1;
+    // parent of every visited vertex
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int x = lane + 32 * i;
+      const int dx = dl[i];
+      if (x >= n || dx <= 0) continue;
+      int pick = -1, pair_arc = -1;
       for (int a = g.abeg[x], e = g.abeg[x + 1]; a < e; ++a) {
         const int u = g.to[a];
         const int r = g.rv[a];
-        const bool ok = (cx & 1) ? (u == (x ^ 1)) : (dist[u] >= 0 && (dist[u] >> 1) == want && g.cap[r] > FLOW_EPS);
-        if (ok) {
-          par[x] = (int16_t)r;
+        if (dist[u] == dx - 1 && g.cap[r] > FLOW_EPS) {
+          pick = r;
           break;
         }
+        if (u == (x ^ 1) && x >= 2) pair_arc = r;
       }
+      if (pick < 0) {  // reached through its partner's pair arc at the same level
+        if (pair_arc < 0)
+          for (int a = g.abeg[x], e = g.abeg[x + 1]; a < e; ++a)
+            if (g.to[a] == (x ^ 1)) {
+              pair_arc = g.rv[a];
+              break;
+            }
+        pick = pair_arc;
+      }
+      par[x] = (int16_t)pick;
     }
     __syncwarp();
     int len = 0;
@@ -280,6 +293,7 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
     for (int k = lane; k < len; k += 32) f = ref_min(f, g.cap[path[k]]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) f = ref_min(f, __shfl_xor_sync(FULL, f, o));
+    unsigned* Rw = reinterpret_cast<unsigned*>(R);
     for (int k = lane; k < len; k += 32) {
       const int a = path[k];
       const int r = g.rv[a];
@@ -288,12 +302,8 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
       const double ca = g.cap[a] - f;
       g.cap[a] = ca;
       g.cap[r] += f;
-      if (ca <= FLOW_EPS) {
-        if (v < 64) atomicAnd(&R[u].x, ~(1ull << v));
-        else atomicAnd(&R[u].y, ~(1ull << (v - 64)));
-      }
-      if (u < 64) atomicOr(&R[v].x, 1ull << u);
-      else atomicOr(&R[v].y, 1ull << (u - 64));
+      if (ca <= FLOW_EPS) atomicAnd(&Rw[4 * u + (v >> 5)], ~(1u << (v & 31)));
+      atomicOr(&Rw[4 * v + (u >> 5)], 1u << (u & 31));
     }
     value += f;
     __syncwarp();
