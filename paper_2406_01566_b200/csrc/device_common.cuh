@@ -26,7 +26,7 @@ Layout make_layout(int V, int A, int N, int M) {
   l.o_abeg = take(2 * (V + 1), 2);
   l.o_cur = take(2 * V, 2);
   l.o_q = take(2 * V, 2);
-  l.o_cnt = take(2 * (2 * V + 1), 2);
+  l.o_cnt = take(2 * (2 * V + 1), 4);  // SCORE: int32 parent words
   l.o_ps = take(2 * N, 4);
   l.o_pe = take(2 * N, 2);
   l.o_vin = take(2 * N, 2);

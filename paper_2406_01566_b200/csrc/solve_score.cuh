@@ -159,11 +159,12 @@ __device__ __forceinline__ unsigned swap_pairs32(unsigned x) {
 }
 
 __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int t, const int lane) {
-  // R in the VState region; BFS level per vertex in the count region;
-  // parent arc per vertex in `cur`; the augmenting path in the queue region.
+  // R in the VState region; BFS level per vertex (int8, n <= 128 levels) in
+  // the in-queue bytes; parent arc | parent vertex << 16 per vertex in the
+  // count region (4V + 2 bytes); the augmenting path in the queue region.
   uint4* R = reinterpret_cast<uint4*>(g.vs);
-  int16_t* dist = g.cnt;
-  int16_t* par = g.cur;
+  int8_t* dist = reinterpret_cast<int8_t*>(g.inq);
+  int32_t* par = reinterpret_cast<int32_t*>(g.cnt);
   int16_t* path = g.q;
   const unsigned lb = 1u << lane;
   for (int x = lane; x < n; x += 32) {
@@ -248,7 +249,7 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
     if (!found) break;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (lane + 32 * i < n) dist[lane + 32 * i] = (int16_t)dl[i];
+      if (lane + 32 * i < n) dist[lane + 32 * i] = (int8_t)dl[i];
     __syncwarp();
     // parent of every visited vertex
 #pragma unroll
@@ -256,12 +257,13 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
       const int x = lane + 32 * i;
       const int dx = dl[i];
       if (x >= n || dx <= 0) continue;
-      int pick = -1, pair_arc = -1;
+      int pick = -1, pu = -1, pair_arc = -1;
       for (int a = g.abeg[x], e = g.abeg[x + 1]; a < e; ++a) {
         const int u = g.to[a];
         const int r = g.rv[a];
         if (dist[u] == dx - 1 && g.cap[r] > FLOW_EPS) {
           pick = r;
+          pu = u;
           break;
         }
         if (u == (x ^ 1) && x >= 2) pair_arc = r;
@@ -274,17 +276,18 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
               break;
             }
         pick = pair_arc;
+        pu = x ^ 1;
       }
-      par[x] = (int16_t)pick;
+      par[x] = (int32_t)(uint16_t)pick | (pu << 16);
     }
     __syncwarp();
     int len = 0;
     if (lane == 0) {
       int x = t;
       while (x != s) {
-        const int a = par[x];
-        path[len++] = (int16_t)a;
-        x = g.to[g.rv[a]];
+        const int32_t w = par[x];
+        path[len++] = (int16_t)(w & 0xffff);
+        x = w >> 16;
       }
     }
     len = __shfl_sync(FULL, len, 0);
