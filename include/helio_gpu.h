@@ -202,6 +202,19 @@ int helio_gpu_best_exhaustive(helio_gpu_ctx* ctx, int allow_partial, int64_t max
                               double* h_best_value, int16_t* h_best_row, int64_t* h_leaves_scored,
                               int64_t* h_leaves_total);
 
+/* Best-improvement local search from a seed placement (
+ * seeds typically come from the heuristics of src/heuristics.cpp:12-131).
+ * Each iteration scores, in the context's mode, every placement that differs
+ * from the current one in exactly one node's interval (node-major; per node
+ * the choices of enumerate.hpp:21-28: idle, then [s, e) with e - s <= k_i in
+ * (s, e) order) and moves to the first strict maximum when it beats the
+ * current value (enumerate.hpp:59).  Stops at a local optimum or after
+ * max_moves moves (< 0: no limit).  The seed must pass validation
+ * (HELIO_ERR_INVALID otherwise).  Outputs the final value and int16 [N][2]
+ * row, the number of moves taken and the placements scored (seed included). */
+int helio_gpu_local_search(helio_gpu_ctx* ctx, const int16_t* h_seed, int allow_partial, int32_t max_moves,
+                           double* h_value, int16_t* h_row, int32_t* h_moves, int64_t* h_scored);
+
 /* Link-walking covering chains (gen.h hg_candidate_walk) for sparse
  * topologies, device and host (identical output). */
 int helio_gpu_generate_walk(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B,

@@ -10,6 +10,7 @@
 //   iwrr_weights / IwrrPicker        proj/src/scheduler.cpp:28-56
 //   Scheduler::admit / complete      proj/src/scheduler.cpp:58-190
 //   generate_trace                   proj/src/workload.cpp:37-57
+//   swarm / petals / sp heuristics   proj/src/heuristics.cpp:12-131
 //   AC1 random raw graphs            proj/tests/acceptance/acceptance_main.cpp:266-295
 //   test_flow random graphs          proj/tests/test_flow.cpp:141-188
 //
@@ -27,6 +28,7 @@
 #include "helio/cluster.hpp"
 #include "helio/errors.hpp"
 #include "helio/flow_graph.hpp"
+#include "helio/heuristics.hpp"
 #include "helio/placement.hpp"
 #include "helio/rng.hpp"
 #include "helio/scheduler.hpp"
@@ -360,6 +362,30 @@ double refh_best_exhaustive(void* cp, int allow_partial, int16_t* best_row, int6
   }
   *scored = n;
   return v;
+}
+
+// swarm_placement / petals_placement / separate_pipelines_placement
+// (heuristics.cpp:12-131), method 0 / 1 / 2: the placement as an int16 [N][2]
+// row and the warnings joined by newlines.  Returns the number of warnings,
+// or -1 with the exception text in `warn` when the heuristic throws.
+int refh_heuristic(void* cp, int method, int16_t* row, char* warn, int warnlen) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  try {
+    HeuristicResult h = method == 0 ? swarm_placement(c) : method == 1 ? petals_placement(c)
+                                                                       : separate_pipelines_placement(c);
+    for (size_t k = 0; k < c.nodes.size(); ++k) {
+      auto it = h.placement.find(c.nodes[k].id);
+      row[2 * k] = it == h.placement.end() ? 0 : static_cast<int16_t>(it->second.start);
+      row[2 * k + 1] = it == h.placement.end() ? 0 : static_cast<int16_t>(it->second.end);
+    }
+    std::string all;
+    for (size_t i = 0; i < h.warnings.size(); ++i) all += (i ? "\n" : "") + h.warnings[i];
+    set_err(warn, warnlen, all);
+    return static_cast<int>(h.warnings.size());
+  } catch (const std::exception& e) {
+    set_err(warn, warnlen, e.what());
+    return -1;
+  }
 }
 
 }  // extern "C"

@@ -8,7 +8,11 @@ batched entry points of the B200 engine:
 * ``Engine(cluster, device)``: ``score`` (host arrays, copies inside),
   ``score_device`` (device pointers), ``flows`` (per-edge flows in reference
   edge order), ``route`` (IWRR routes), ``generate_device``, ``argmax_device``;
-* ``max_flow_values`` / ``best_placement`` / ``route_requests`` helpers.
+* ``max_flow_values`` / ``best_placement`` / ``route_requests`` helpers;
+* placement search: ``heuristic_placement`` (swarm / petals / sp, the
+  reference's heuristics.cpp), ``local_search`` and ``plan(cluster, "local")``
+  (device best-improvement search seeded from those heuristics),
+  ``Engine.best_exhaustive``.
 
 Every result is computed by the CUDA kernels in ``csrc/`` (sm_100a).  There is
 no CPU fallback: importing fails loudly if the extension is missing, and using
@@ -39,10 +43,13 @@ from ._helio import (  # noqa: E402
     build_flow_graph,
     generate_host,
     generate_trace,
+    heuristic_placement,
     iwrr_weights,
+    local_search,
     max_flow,
     max_flow_raw,
     max_flow_value,
+    plan,
     plan_for_placement,
     route_requests,
 )
@@ -89,5 +96,6 @@ __all__ = [
     "Cluster", "Engine", "FlowGraph", "InternalError", "IwrrPicker", "ParseError", "Plan",
     "ValidationError", "best_placement", "build_flow_graph", "generate_host", "generate_trace",
     "iwrr_weights", "max_flow", "max_flow_raw", "max_flow_value", "max_flow_values",
-    "placement_rows", "plan_for_placement", "route_requests",
+    "placement_rows", "plan_for_placement", "route_requests", "heuristic_placement", "local_search",
+    "plan",
 ]

@@ -26,9 +26,9 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-f
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-sign-compare"]
 
 CU_SOURCES = ["helio_gpu.cu", "route.cu", "search.cu", "split.cu"]
-SHIM_SOURCES = ["shim_cluster.cpp", "shim_flow.cpp", "shim_plan.cpp", "shim_sched.cpp"]
+SHIM_SOURCES = ["shim_cluster.cpp", "shim_flow.cpp", "shim_plan.cpp", "shim_sched.cpp", "shim_heuristics.cpp"]
 HEADERS = ["engine.h", "gen.h", "device_common.cuh", "build.cuh", "solve_parity.cuh", "solve_score.cuh", "shim.hpp", "shim_engine.hpp", "helio/cluster.hpp", "helio/errors.hpp",
-           "helio/flow_graph.hpp", "helio/placement.hpp", "helio/scheduler.hpp"]
+           "helio/flow_graph.hpp", "helio/placement.hpp", "helio/scheduler.hpp", "helio/heuristics.hpp"]
 
 
 def _run(cmd, quiet=False):

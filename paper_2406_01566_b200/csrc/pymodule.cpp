@@ -15,6 +15,7 @@
 #include <random>
 
 #include "shim.hpp"
+#include "helio/heuristics.hpp"
 
 namespace py = pybind11;
 using namespace helio;
@@ -554,6 +555,76 @@ PYBIND11_MODULE(_helio, m) {
       .def("min_cut_source_side", [](const FlowGraph& g) { return min_cut_source_side(g); });
 
   m.def(
+      "plan",
+      [](const ClusterSpec& c, const std::string& method, bool allow_partial, int max_moves) {
+        // pymodule.cpp:130-157 for the heuristics; "local" is this engine's
+        // search and "milp" stays with the reference
+        if (method == "swarm" || method == "petals" || method == "sp") {
+          HeuristicResult h = method == "swarm"    ? swarm_placement(c)
+                              : method == "petals" ? petals_placement(c)
+                                                   : separate_pipelines_placement(c);
+          PlacementPlan plan = plan_from_placement(c, h.placement, allow_partial, method);
+          for (const std::string& w : h.warnings) plan.warnings.push_back(w);
+          return plan;
+        }
+        if (method == "local") {
+          // seeds as the reference's MILP warm starts (placement.cpp:491-498)
+          std::vector<HeuristicResult> seeds{swarm_placement(c), petals_placement(c)};
+          if (std::all_of(c.nodes.begin(), c.nodes.end(), [](const NodeSpec& n) { return !n.type.empty(); }))
+            seeds.push_back(separate_pipelines_placement(c));
+          Placement best;
+          double best_value = 0;
+          std::vector<std::string> warnings;
+          for (const HeuristicResult& h : seeds) {
+            for (const std::string& w : h.warnings) warnings.push_back(w);
+            LocalSearchResult r;
+            {
+              py::gil_scoped_release rel;
+              r = local_search_placement(c, h.placement, allow_partial, max_moves);
+            }
+            if (r.value > best_value) {
+              best_value = r.value;
+              best = r.placement;
+            }
+          }
+          PlacementPlan plan = plan_from_placement(c, best, allow_partial, "local");
+          for (const std::string& w : warnings) plan.warnings.push_back(w);
+          return plan;
+        }
+        if (method == "milp")
+          throw ValidationError("method 'milp' is the reference's planner; link it over this engine (INTEGRATION.md)");
+        throw ValidationError("unknown method '" + method + "'");
+      },
+      py::arg("cluster"), py::arg("method") = "local", py::arg("allow_partial") = true, py::arg("max_moves") = -1,
+      "Compute a placement plan (method: swarm, petals, sp, or local = device local search from those seeds).");
+
+  m.def(
+      "heuristic_placement",
+      [](const ClusterSpec& c, const std::string& method) {
+        HeuristicResult h;
+        if (method == "swarm") h = swarm_placement(c);
+        else if (method == "petals") h = petals_placement(c);
+        else if (method == "sp") h = separate_pipelines_placement(c);
+        else throw ValidationError("unknown method '" + method + "'");
+        return py::make_tuple(placement_to_dict(h.placement), h.warnings);
+      },
+      py::arg("cluster"), py::arg("method"), "(placement, warnings) of a baseline heuristic (heuristics.cpp).");
+
+  m.def(
+      "local_search",
+      [](const ClusterSpec& c, const py::dict& seed, bool allow_partial, int max_moves) {
+        const Placement p = placement_from_dict(seed);
+        LocalSearchResult r;
+        {
+          py::gil_scoped_release rel;
+          r = local_search_placement(c, p, allow_partial, max_moves);
+        }
+        return py::make_tuple(placement_to_dict(r.placement), r.value, r.moves, r.scored);
+      },
+      py::arg("cluster"), py::arg("seed"), py::arg("allow_partial") = true, py::arg("max_moves") = -1,
+      "Device local search from a placement: (placement, value, moves, placements scored).");
+
+  m.def(
       "plan_for_placement",
       [](const ClusterSpec& c, const py::dict& placement, bool allow_partial) {
         return plan_from_placement(c, placement_from_dict(placement), allow_partial, "custom");
@@ -847,5 +918,27 @@ PYBIND11_MODULE(_helio, m) {
           },
           py::arg("allow_partial") = true, py::arg("max_leaves") = 2000000000LL,
           "Exhaustive search in the reference's enumeration order: (best value, row, leaves scored, leaf space).")
+      .def(
+          "local_search",
+          [](PyEngine& e, py::array_t<int16_t, py::array::c_style | py::array::forcecast> seed, bool allow_partial,
+             int32_t max_moves) {
+            const int N = e.eng->num_nodes();
+            if (seed.ndim() != 2 || seed.shape(0) != N || seed.shape(1) != 2)
+              throw py::value_error("seed must be int16 [num_nodes, 2]");
+            py::array_t<int16_t> row({(py::ssize_t)N, (py::ssize_t)2});
+            double value = 0;
+            int32_t moves = 0;
+            int64_t scored = 0;
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = helio_gpu_local_search(e.eng->ctx(), seed.data(), allow_partial ? 1 : 0, max_moves, &value,
+                                          row.mutable_data(), &moves, &scored);
+            }
+            e.eng->check(rc, "helio_gpu_local_search");
+            return py::make_tuple(value, row, moves, scored);
+          },
+          py::arg("seed"), py::arg("allow_partial") = true, py::arg("max_moves") = -1,
+          "Best-improvement single-node-move local search: (value, row, moves, placements scored).")
       .def("sync", [](PyEngine& e) { e.eng->check(helio_gpu_sync(e.eng->ctx()), "helio_gpu_sync"); });
 }

@@ -202,3 +202,125 @@ extern "C" int helio_gpu_best_exhaustive(helio_gpu_ctx* ctx, int allow_partial, 
   if (h_total) *h_total = total;
   return HELIO_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Best-improvement local search over single-node moves (SURVEY.md §8(f) rank
+// 1: the enumerate consumer generalised to clusters whose placement space is
+// far beyond exhaustive search, seeded from the heuristics of
+// src/heuristics.cpp:12-131).  One iteration scores every placement that
+// differs from the current one in exactly one node's interval — node i
+// takes any choice of enumerate.hpp:21-28 ({idle} then [s, e) with
+// e - s <= k_i in (s, e) order), neighbours ordered node-major — with the
+// context's scoring mode, and moves to the first strict maximum if it beats
+// the current value (enumerate.hpp:59's strict '>' and first-wins rule).
+namespace {
+
+__global__ void neighbour_rows(const int32_t* __restrict__ cur, int N, const int16_t* __restrict__ node_of,
+                               const int32_t* __restrict__ choice, int64_t C, int32_t* __restrict__ rows) {
+  const int64_t words = C * N;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < words;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = q / N;
+    const int k = (int)(q - t * N);
+    rows[q] = k == node_of[t] ? choice[t] : __ldg(cur + k);
+  }
+}
+
+}  // namespace
+
+extern "C" int helio_gpu_local_search(helio_gpu_ctx* ctx, const int16_t* h_seed, int allow_partial,
+                                      int32_t max_moves, double* h_value, int16_t* h_row, int32_t* h_moves,
+                                      int64_t* h_scored) {
+  if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
+  if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
+  if (!h_seed || !h_value || !h_row) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  const int N = ctx->N, L = ctx->L;
+  CK(cudaSetDevice(ctx->device));
+  // the move list: (node, packed interval) in neighbour order
+  std::vector<int16_t> node_of;
+  std::vector<int32_t> choice;
+  auto pack = [](int s, int e) { return (int32_t)(uint16_t)s | (int32_t)((uint32_t)(uint16_t)e << 16); };
+  for (int i = 0; i < N; ++i) {
+    node_of.push_back((int16_t)i);
+    choice.push_back(0);
+    const int k = ctx->h_kmax[i];
+    for (int s = 0; s < L; ++s)
+      for (int e = s + 1; e <= L && e - s <= k; ++e) {
+        node_of.push_back((int16_t)i);
+        choice.push_back(pack(s, e));
+      }
+  }
+  const int64_t C = (int64_t)choice.size();
+  cudaStream_t st = ctx->stream;
+  int rc = HELIO_OK;
+  int16_t* d_node = nullptr;
+  int32_t *d_choice = nullptr, *d_cur = nullptr, *d_rows = nullptr, *d_st = nullptr;
+  double *d_val = nullptr, *d_best = nullptr;
+  int64_t* d_bidx = nullptr;
+  auto A = [&](void** p, size_t bytes) {
+    if (!rc && cudaMalloc(p, std::max<size_t>(bytes, 8)) != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "local search alloc");
+  };
+  A((void**)&d_node, 2 * C);
+  A((void**)&d_choice, 4 * C);
+  A((void**)&d_cur, 4 * N);
+  A((void**)&d_rows, 4 * (size_t)N * C);
+  A((void**)&d_val, 8 * C);
+  A((void**)&d_st, 4 * C);
+  A((void**)&d_best, 8);
+  A((void**)&d_bidx, 8);
+  std::vector<int32_t> cur(N);
+  for (int i = 0; i < N; ++i) cur[i] = pack(h_seed[2 * i], h_seed[2 * i + 1]);
+  double value = 0.0;
+  int32_t moves = 0;
+  int64_t scored = 0;
+  auto sync_read = [&](void* dst, const void* src, size_t bytes) {
+    if (!rc && (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess))
+      rc = fail(ctx, HELIO_ERR_CUDA, std::string("local search readback: ") + cudaGetErrorString(cudaGetLastError()));
+  };
+  if (!rc) {
+    cudaMemcpyAsync(d_node, node_of.data(), 2 * C, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_choice, choice.data(), 4 * C, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_cur, cur.data(), 4 * N, cudaMemcpyHostToDevice, st);
+    // the seed's own value and status
+    rc = helio_gpu_score(ctx, reinterpret_cast<const int16_t*>(d_cur), 1, allow_partial, d_val, d_st, st);
+    int32_t s0 = 0;
+    sync_read(&value, d_val, 8);
+    sync_read(&s0, d_st, 4);
+    scored = 1;
+    if (!rc && s0 != 0) rc = fail(ctx, HELIO_ERR_INVALID, "seed placement fails validation (status " + std::to_string(s0) + ")");
+  }
+  while (!rc && (max_moves < 0 || moves < max_moves)) {
+    const int grid = (int)std::min<int64_t>((C * N + 255) / 256, 16 * ctx->sm_count);
+    neighbour_rows<<<grid, 256, 0, st>>>(d_cur, N, d_node, d_choice, C, d_rows);
+    ctx->launches++;
+    rc = helio_gpu_score(ctx, reinterpret_cast<const int16_t*>(d_rows), C, allow_partial, d_val, d_st, st);
+    if (rc) break;
+    rc = helio_gpu_argmax(ctx, d_val, d_st, C, 0, d_best, d_bidx, st);
+    if (rc) break;
+    double best = 0.0;
+    int64_t bi = -1;
+    sync_read(&best, d_best, 8);
+    sync_read(&bi, d_bidx, 8);
+    scored += C;
+    if (rc || bi < 0 || !(best > value)) break;
+    value = best;
+    cur[node_of[bi]] = choice[bi];
+    ++moves;
+    if (cudaMemcpyAsync(d_cur, cur.data(), 4 * N, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      rc = fail(ctx, HELIO_ERR_CUDA, "local search upload");
+  }
+  if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "local search sync");
+  cudaFree(d_node); cudaFree(d_choice); cudaFree(d_cur); cudaFree(d_rows); cudaFree(d_val); cudaFree(d_st);
+  cudaFree(d_best); cudaFree(d_bidx);
+  if (rc) return rc;
+  *h_value = value;
+  for (int i = 0; i < N; ++i) {
+    h_row[2 * i] = (int16_t)(cur[i] & 0xffff);
+    h_row[2 * i + 1] = (int16_t)((uint32_t)cur[i] >> 16);
+  }
+  if (h_moves) *h_moves = moves;
+  if (h_scored) *h_scored = scored;
+  return HELIO_OK;
+}

@@ -426,3 +426,60 @@ CAND_FIXTURES = [f"{n}_{c}" for n in ("single24-70b", "single24-30b", "het42-70b
 def bits(a):
     """Exact bit pattern of a float64 array (for bit-exact comparisons)."""
     return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+def neighbour_moves(kmax, L):
+    """Single-node moves in helio_gpu_local_search's order: node-major, per node
+    the choices of enumerate.hpp:21-28 (idle, then [s, e) with e - s <= k_i in
+    (s, e) order).  -> (node int[C], start int[C], end int[C])."""
+    node, st, en = [], [], []
+    for i, k in enumerate(kmax):
+        node.append(i); st.append(0); en.append(0)
+        for s in range(L):
+            for e in range(s + 1, min(L, s + k) + 1):
+                node.append(i); st.append(s); en.append(e)
+    return np.array(node), np.array(st, np.int16), np.array(en, np.int16)
+
+
+def local_search_oracle(score, kmax, L, seed_row, max_moves=-1):
+    """CPU statement of the device local search over any scorer
+    score(rows int16[B,N,2]) -> (values, status): best-improvement single-node
+    moves, first strict maximum over status-OK positive values
+    (enumerate.hpp:59).  -> (value, row, moves, scored)."""
+    node, st, en = neighbour_moves(kmax, L)
+    C_ = len(node)
+    cur = np.array(seed_row, np.int16).copy()
+    v, s = score(cur[None])
+    assert s[0] == 0, "seed must validate"
+    value, scored, moves = float(v[0]), 1, 0
+    while max_moves < 0 or moves < max_moves:
+        rows = np.repeat(cur[None], C_, axis=0)
+        rows[np.arange(C_), node, 0] = st
+        rows[np.arange(C_), node, 1] = en
+        vals, sts = score(rows)
+        scored += C_
+        ok = (sts == 0) & (vals > 0)
+        if not ok.any():
+            break
+        bi = int(np.argmax(np.where(ok, vals, -np.inf)))
+        if not vals[bi] > value:
+            break
+        value = float(vals[bi])
+        cur[node[bi]] = (st[bi], en[bi])
+        moves += 1
+    return value, cur, moves, scored
+
+
+def ref_heuristic(rc: "RefCluster", method: str):
+    """The reference's swarm / petals / sp placement as an int16 [N][2] row plus
+    its warnings (or the exception text as a ValueError)."""
+    lib = ref()
+    lib.refh_heuristic.argtypes = [C.c_void_p, C.c_int, _i16p, C.c_char_p, C.c_int]
+    lib.refh_heuristic.restype = C.c_int
+    row = np.zeros((rc.N, 2), np.int16)
+    buf = C.create_string_buffer(8192)
+    n = lib.refh_heuristic(rc.h, {"swarm": 0, "petals": 1, "sp": 2}[method], row, buf, 8192)
+    text = buf.value.decode()
+    if n < 0:
+        raise ValueError(text)
+    return row, (text.split("\n") if n > 0 else [])

@@ -1,0 +1,169 @@
+"""Placement search: the reference's baseline
+heuristics (src/heuristics.cpp:12-131) restated on the host as local-search
+seeds, and the device best-improvement local search checked move for move
+against the same driver run over the reference's own scorer."""
+import ctypes as C
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2406_01566_b200 as h
+from paper_2406_01566_b200 import clusters
+
+from _support import RefCluster, local_search_oracle, ref, ref_available, ref_heuristic
+
+needs_ref = pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+METHODS = ("swarm", "petals", "sp")
+
+
+def _cluster(d):
+    return h.Cluster.from_json(json.dumps(d))
+
+
+def _row(c, placement):
+    return h.placement_rows(c, [{k: tuple(v) for k, v in placement.items()}])[0]
+
+
+def _random_cluster(seed, max_nodes=10, lo=4, hi=10):
+    # random_cluster.hpp loops forever unless 2 * (max_hold + 2) >= L: keep L <= 10
+    lib = ref()
+    lib.refh_random_cluster_json.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_int]
+    lib.refh_random_cluster_json.restype = C.c_int
+    buf = C.create_string_buffer(1 << 16)
+    n = lib.refh_random_cluster_json(seed, max_nodes, lo, hi, buf, 1 << 16)
+    assert n > 0
+    return json.loads(buf.value.decode())
+
+
+# --- heuristics (host; no GPU) ------------------------------------------------
+
+@needs_ref
+@pytest.mark.parametrize("name", ["het42-70b", "geo24", "single24-30b", "single24-70b", "syn256-120l"])
+@pytest.mark.parametrize("method", METHODS)
+def test_heuristic_matches_reference(name, method):
+    d = clusters.CONFIGS[name]()
+    c = _cluster(d)
+    want_row, want_warn = ref_heuristic(RefCluster(d), method)
+    placement, warnings = h.heuristic_placement(c, method)
+    assert np.array_equal(_row(c, placement), want_row)
+    assert warnings == want_warn
+
+
+@needs_ref
+def test_heuristics_match_reference_on_random_clusters():
+    checked = 0
+    for seed in range(60):
+        d = _random_cluster(9100 + seed)
+        c = _cluster(d)
+        rc = RefCluster(d)
+        for method in METHODS:
+            want_row, want_warn = ref_heuristic(rc, method)
+            placement, warnings = h.heuristic_placement(c, method)
+            assert np.array_equal(_row(c, placement), want_row), (seed, method)
+            assert warnings == want_warn, (seed, method)
+            checked += 1
+    assert checked == 180
+
+
+@needs_ref
+def test_separate_pipelines_needs_types():
+    d = clusters.CONFIGS["geo24"]()
+    d["nodes"][3]["type"] = ""
+    with pytest.raises(ValueError) as want:
+        ref_heuristic(RefCluster(d), "sp")
+    with pytest.raises(h.ValidationError) as got:
+        h.heuristic_placement(_cluster(d), "sp")
+    assert str(got.value) == str(want.value)
+
+
+def test_neighbour_order_is_enumerate_choice_order():
+    from _support import neighbour_moves
+
+    node, s, e = neighbour_moves([1, 2], 3)
+    got = list(zip(node.tolist(), s.tolist(), e.tolist()))
+    assert got == [(0, 0, 0), (0, 0, 1), (0, 1, 2), (0, 2, 3),
+                   (1, 0, 0), (1, 0, 1), (1, 0, 2), (1, 1, 2), (1, 1, 3), (1, 2, 3)]
+
+
+# --- device local search ------------------------------------------------------
+
+def _ref_scorer(d, partial=True):
+    rc = RefCluster(d)
+    threads = os.cpu_count() or 1
+    return rc, (lambda rows: rc.score(rows, partial, threads))
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("name,seed_method,max_moves", [
+    ("geo24", "petals", -1), ("geo24", "swarm", -1), ("single24-30b", "petals", -1),
+    ("het42-70b", "petals", 2),
+])
+def test_local_search_matches_reference_driver(name, seed_method, max_moves):
+    d = clusters.CONFIGS[name]()
+    c = _cluster(d)
+    seed = _row(c, h.heuristic_placement(c, seed_method)[0])
+    e = h.Engine(c)  # PARITY: every value is the reference's double
+    value, row, moves, scored = e.local_search(seed, True, max_moves)
+    rc, score = _ref_scorer(d)
+    w_value, w_row, w_moves, w_scored = local_search_oracle(score, list(e.kmax), rc.L, seed, max_moves)
+    assert value == w_value
+    assert np.array_equal(row, w_row)
+    assert (moves, scored) == (w_moves, w_scored)
+    if max_moves < 0:
+        assert moves > 0
+
+
+@pytest.mark.gpu
+def test_local_search_score_mode_integer_capacities_equal_parity():
+    d = clusters.CONFIGS["het42-70b"]("int")
+    c = _cluster(d)
+    seed = _row(c, h.heuristic_placement(c, "swarm")[0])
+    e = h.Engine(c)
+    par = e.local_search(seed, True, 4)
+    e.mode = "score"
+    sco = e.local_search(seed, True, 4)
+    assert par[0] == sco[0] and np.array_equal(par[1], sco[1]) and par[2:] == sco[2:]
+
+
+@pytest.mark.gpu
+def test_local_search_is_a_local_optimum():
+    d = clusters.CONFIGS["geo24"]()
+    c = _cluster(d)
+    e = h.Engine(c)
+    seed = _row(c, h.heuristic_placement(c, "swarm")[0])
+    value, row, moves, scored = e.local_search(seed)
+    again = e.local_search(row)
+    assert again[0] == value and again[2] == 0 and np.array_equal(again[1], row)
+    # and the value is the device's PARITY value of the final row
+    v, st = e.score(row[None])
+    assert st[0] == 0 and v[0] == value
+
+
+@pytest.mark.gpu
+def test_plan_local_beats_its_seeds():
+    d = clusters.CONFIGS["geo24"]()
+    c = _cluster(d)
+    p = h.plan(c, "local")
+    assert p.method == "local"
+    for m in METHODS:
+        assert p.objective >= h.plan(c, m).objective
+    assert p.objective == h.max_flow_value(c, p.placement)
+    # the best seed's local optimum, via the module-level entry
+    best = max((h.local_search(c, h.heuristic_placement(c, m)[0])[1] for m in METHODS))
+    assert p.objective == best
+
+
+@pytest.mark.gpu
+def test_local_search_rejects_invalid_seed():
+    d = clusters.CONFIGS["geo24"]()
+    c = _cluster(d)
+    e = h.Engine(c)
+    bad = np.zeros((len(d["nodes"]), 2), np.int16)
+    bad[0] = (0, 24)  # longer than node 0's VRAM allows
+    with pytest.raises(Exception):
+        e.local_search(bad)
+    with pytest.raises(h.ValidationError):
+        h.local_search(c, {d["nodes"][0]["id"]: (0, 24)})
