@@ -322,6 +322,36 @@ def split_leg(eng, dev, sp, B=200_000):
             "bit_identical_to_fused": same}
 
 
+def search_leg(h, clusters, dev):
+    """device local search (helio_gpu_local_search)
+    on het42-70b from the reference's three heuristics, in both modes; host
+    wall clock around each call (neighbour generation, scoring, argmax and the
+    per-move readback all inside)."""
+    import numpy as np
+
+    d = clusters.CONFIGS["het42-70b"]("float")
+    c = h.Cluster.from_json(json.dumps(d))
+    eng = h.Engine(c, dev)
+    out = {"workload": "het42-70b: best-improvement single-node moves from swarm / petals / sp seeds",
+           "neighbours_per_move": None, "runs": []}
+    for method in ("swarm", "petals", "sp"):
+        placement, _ = h.heuristic_placement(c, method)
+        seed = h.placement_rows(c, [{k: tuple(v) for k, v in placement.items()}])[0]
+        for mode in ("score", "parity"):
+            eng.mode = mode
+            eng.local_search(seed, True, 1)  # warm (allocations, first launch)
+            t0 = time.perf_counter()
+            value, row, moves, scored = eng.local_search(seed, True, -1)
+            dt = time.perf_counter() - t0
+            v0, _ = eng.score(seed[None])
+            out["runs"].append({"seed": method, "mode": mode, "seed_value": float(v0[0]), "value": value,
+                                "moves": moves, "scored": scored, "seconds": dt,
+                                "evals_per_s": scored / dt if dt > 0 else None})
+    out["neighbours_per_move"] = int((out["runs"][0]["scored"] - 1) // max(1, out["runs"][0]["moves"] + 1))
+    eng.mode = "score"
+    return out
+
+
 def run_reference(args):
     rank = env_int("RANK", 0)
     if rank != 0:
@@ -557,6 +587,13 @@ def main():
         except Exception as ex:  # reported, never fatal
             routing = {"value": None, "error": str(ex)}
 
+    search = None
+    if world == 1 and not args.no_configs:
+        try:
+            search = search_leg(h, clusters, local)
+        except Exception as ex:  # reported, never fatal
+            search = {"error": str(ex)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -567,6 +604,10 @@ def main():
                              f"build_flow_graph+max_flow on a {threads}-thread std::thread pool"}
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "evals/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
+
+    if search and cpu and cpu.get("value") and "runs" in search:
+        for r in search["runs"]:  # the same scoring on the reference, at the measured host rate
+            r["reference_equivalent_seconds"] = r["scored"] / cpu["value"]
 
     if rank == 0:
         out = {
@@ -582,7 +623,7 @@ def main():
                        "nonzero_fraction": nonzero, "status_nonzero": int((st_host != 0).sum()),
                        "best": {"value": win[0], "index": win[1]}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "routing": routing, "other_configs": cfg_table, "split_pipeline": split,
+            "routing": routing, "other_configs": cfg_table, "split_pipeline": split, "search": search,
             "clocks": clk.summary(),
         }
         print(json.dumps(out))
