@@ -158,7 +158,10 @@ __device__ __forceinline__ unsigned swap_pairs32(unsigned x) {
   return ((x & 0x55555555u) << 1) | ((x >> 1) & 0x55555555u);
 }
 
-__device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int t, const int lane) {
+// NW = 32-bit words per vertex set = ceil(n / 32): lane l owns vertices l + 32i
+// for i < NW, so every loop below is unrolled to exactly the words in use.
+template <int NW>
+__device__ double solve_ek_bits_w(const Gs& g, const int n, const int s, const int t, const int lane) {
   // R in the VState region; BFS level per vertex (int8, n <= 128 levels) in
   // the in-queue bytes; parent arc | parent vertex << 16 per vertex in the
   // count region (4V + 2 bytes); the augmenting path in the queue region.
@@ -179,68 +182,62 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
   __syncwarp();
   double value = 0.0;
   for (;;) {
-    // P: vertices v >= 2 whose pair arc v -> v^1 has residual capacity; then
-    // this lane's closure rows Q
-    uint4 Q[4];
-    unsigned P[4];
+    // P: vertices v >= 2 whose pair arc v -> v^1 has residual capacity (v^1
+    // is bit lane^1 of v's own word); then this lane's closure rows Q
+    unsigned Q[NW][NW];
+    unsigned P[NW];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < NW; ++i) {
       const int v = lane + 32 * i;
       bool pr = false;
-      Q[i] = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int w = 0; w < NW; ++w) Q[i][w] = 0u;
       if (v < n) {
-        Q[i] = R[v];
-        if (v >= 2) {
-          const int w = v ^ 1;
-          const unsigned ww = (w >> 5) == 0 ? Q[i].x : (w >> 5) == 1 ? Q[i].y : (w >> 5) == 2 ? Q[i].z : Q[i].w;
-          pr = (ww >> (w & 31)) & 1u;
-        }
+        const uint4 r = R[v];
+        const unsigned rw[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int w = 0; w < NW; ++w) Q[i][w] = rw[w];
+        pr = v >= 2 && ((Q[i][i] >> (lane ^ 1)) & 1u);
       }
       P[i] = __ballot_sync(FULL, pr);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      Q[i].x |= swap_pairs32(Q[i].x & P[0]);
-      Q[i].y |= swap_pairs32(Q[i].y & P[1]);
-      Q[i].z |= swap_pairs32(Q[i].z & P[2]);
-      Q[i].w |= swap_pairs32(Q[i].w & P[3]);
-    }
+    for (int i = 0; i < NW; ++i)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) Q[i][w] |= swap_pairs32(Q[i][w] & P[w]);
     // BFS levels from s
-    unsigned F[4] = {0u, 0u, 0u, 0u}, Vs[4];
-    F[s >> 5] = 1u << (s & 31);
+    unsigned F[NW], Vs[NW];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) Vs[k] = F[k];
-    int dl[4];
+    for (int w = 0; w < NW; ++w) {
+      F[w] = (s >> 5) == w ? 1u << (s & 31) : 0u;
+      Vs[w] = F[w];
+    }
+    int dl[NW];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) dl[i] = (lane + 32 * i == s) ? 0 : -1;
+    for (int i = 0; i < NW; ++i) dl[i] = (lane + 32 * i == s) ? 0 : -1;
     int d = 0;
     bool found = false;
     for (;;) {
-      unsigned a0 = 0u, a1 = 0u, a2 = 0u, a3 = 0u;
+      unsigned a[NW];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (F[i] & lb) {
-          a0 |= Q[i].x;
-          a1 |= Q[i].y;
-          a2 |= Q[i].z;
-          a3 |= Q[i].w;
-        }
-      const unsigned n0 = __reduce_or_sync(FULL, a0) & ~Vs[0];
-      const unsigned n1 = __reduce_or_sync(FULL, a1) & ~Vs[1];
-      const unsigned n2 = __reduce_or_sync(FULL, a2) & ~Vs[2];
-      const unsigned n3 = __reduce_or_sync(FULL, a3) & ~Vs[3];
-      if ((n0 | n1 | n2 | n3) == 0u) break;
+      for (int w = 0; w < NW; ++w) a[w] = 0u;
+#pragma unroll
+      for (int i = 0; i < NW; ++i)
+        if (F[i] & lb)
+#pragma unroll
+          for (int w = 0; w < NW; ++w) a[w] |= Q[i][w];
+      unsigned any = 0u;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        F[w] = __reduce_or_sync(FULL, a[w]) & ~Vs[w];
+        any |= F[w];
+      }
+      if (any == 0u) break;
       ++d;
-      Vs[0] |= n0;
-      Vs[1] |= n1;
-      Vs[2] |= n2;
-      Vs[3] |= n3;
-      F[0] = n0;
-      F[1] = n1;
-      F[2] = n2;
-      F[3] = n3;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) dl[i] = (F[i] & lb) ? d : dl[i];
+      for (int w = 0; w < NW; ++w) Vs[w] |= F[w];
+#pragma unroll
+      for (int i = 0; i < NW; ++i) dl[i] = (F[i] & lb) ? d : dl[i];
       if ((F[t >> 5] >> (t & 31)) & 1u) {
         found = true;
         break;
@@ -248,12 +245,12 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
     }
     if (!found) break;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < NW; ++i)
       if (lane + 32 * i < n) dist[lane + 32 * i] = (int8_t)dl[i];
     __syncwarp();
     // parent of every visited vertex
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < NW; ++i) {
       const int x = lane + 32 * i;
       const int dx = dl[i];
       if (x >= n || dx <= 0) continue;
@@ -312,6 +309,13 @@ __device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int
     __syncwarp();
   }
   return value;
+}
+
+__device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int t, const int lane) {
+  if (n <= 32) return solve_ek_bits_w<1>(g, n, s, t, lane);
+  if (n <= 64) return solve_ek_bits_w<2>(g, n, s, t, lane);
+  if (n <= 96) return solve_ek_bits_w<3>(g, n, s, t, lane);
+  return solve_ek_bits_w<4>(g, n, s, t, lane);
 }
 
 }  // namespace
