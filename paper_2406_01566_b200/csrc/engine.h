@@ -73,25 +73,38 @@ struct helio_gpu_ctx {
   int mode = 0;  // HELIO_MODE_PARITY
   bool big_ok = false;
 
-  // scratch, two sets (one per pipeline stream)
-  unsigned long long* d_work = nullptr;  // [8]: score sets 0/1 use [0,1]/[2,3], split.cu [4]/[5]
-  unsigned int* d_ovf_count = nullptr;   // [2]
-  int64_t* d_ovf[2] = {nullptr, nullptr};
-  int64_t ovf_cap[2] = {0, 0};
-  double* d_pv = nullptr;
+  // scratch sets: kPipeSets for the host-buffer pipeline (one per stream;
+  // three so a chunk's overflow pass, which waits for the next chunk's kernel
+  // to release the SMs, never holds up the following H2D), plus kApiSet for
+  // the device-pointer entries and search.cu
+  static constexpr int kPipeSets = 3, kApiSet = 3, kSets = 4;
+  unsigned long long* d_work = nullptr;  // [16]: set k uses [2k, 2k+1], split.cu [8]/[9]
+  unsigned int* d_ovf_count = nullptr;   // [kSets]
+  int64_t* d_ovf[kSets] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t ovf_cap[kSets] = {0, 0, 0, 0};
+  double* d_pv = nullptr;      // argmax partials: kSets + 1 scratch rows of 4096
   long long* d_pi = nullptr;
   double* d_best = nullptr;   // per-chunk best of score_best_host
   int64_t* d_bidx = nullptr;
 
   // host-call staging
-  int16_t* d_pl[2] = {nullptr, nullptr};
-  double* d_val[2] = {nullptr, nullptr};
-  int32_t* d_st[2] = {nullptr, nullptr};
-  int16_t* h_pl_pin[2] = {nullptr, nullptr};
-  double* h_val_pin[2] = {nullptr, nullptr};
-  int32_t* h_st_pin[2] = {nullptr, nullptr};
+  int16_t* d_pl[kPipeSets] = {nullptr, nullptr, nullptr};
+  double* d_val[kPipeSets] = {nullptr, nullptr, nullptr};
+  int32_t* d_st[kPipeSets] = {nullptr, nullptr, nullptr};
+  int16_t* h_pl_pin[kPipeSets] = {nullptr, nullptr, nullptr};
+  double* h_val_pin[kPipeSets] = {nullptr, nullptr, nullptr};
+  int32_t* h_st_pin[kPipeSets] = {nullptr, nullptr, nullptr};
   int64_t stage_cap = 0;
-  cudaStream_t pipe[2] = {nullptr, nullptr};
+  cudaStream_t pipe[kPipeSets] = {nullptr, nullptr, nullptr};
+
+  // resident staging for pinned callers: the whole batch on the device, its
+  // H2D issued up front on `copy`, one event per chunk
+  int16_t* d_pl_all = nullptr;
+  double* d_val_all = nullptr;
+  int32_t* d_st_all = nullptr;
+  int64_t all_cap = 0;
+  cudaStream_t copy = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_out;
 
   // walk generator adjacency (gen.h hg_candidate_walk)
   const int32_t* d_walk_beg = nullptr;

@@ -332,6 +332,9 @@ int configure_layouts(helio_gpu_ctx* ctx) {
                   reinterpret_cast<void*>(score_kernel<HELIO_MODE_SCORE>)};
   for (int m = 0; m < 2; ++m) {
     CK(cudaFuncSetAttribute(fns[m], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem));
+    // the whole unified L1/shared array as shared memory: the driver's default
+    // carveout (200 KB here) would cap het42 at 7 four-warp CTAs per SM
+    CK(cudaFuncSetAttribute(fns[m], cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[m], 32 * ctx->small_warps,
                                                      ctx->small.bytes * ctx->small_warps));
@@ -395,14 +398,14 @@ int launch_score(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, in
 int helio_engine_score_parity(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int partial, double* d_val,
                               int32_t* d_st, cudaStream_t st) {
   FlowOut fo{nullptr, nullptr, nullptr, 0};
-  return launch_score(ctx, 0, d_pl, B, partial, d_val, d_st, st, fo, false, HELIO_MODE_PARITY);
+  return launch_score(ctx, helio_gpu_ctx::kApiSet, d_pl, B, partial, d_val, d_st, st, fo, false, HELIO_MODE_PARITY);
 }
 
 namespace {
 
 int ensure_stage(helio_gpu_ctx* ctx, int64_t chunk) {
   if (ctx->stage_cap >= chunk) return HELIO_OK;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < helio_gpu_ctx::kPipeSets; ++i) {
     if (ctx->d_pl[i]) cudaFree(ctx->d_pl[i]);
     if (ctx->d_val[i]) cudaFree(ctx->d_val[i]);
     if (ctx->d_st[i]) cudaFree(ctx->d_st[i]);
@@ -455,11 +458,13 @@ int helio_gpu_create(int device, helio_gpu_ctx** out) {
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->pipe[0], cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->pipe[1], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->pipe[2], cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
-      cudaMalloc(&ctx->d_work, 8 * sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMalloc(&ctx->d_ovf_count, 2 * sizeof(unsigned int)) != cudaSuccess ||
-      cudaMalloc(&ctx->d_pv, 3 * 4096 * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&ctx->d_pi, 3 * 4096 * sizeof(long long)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_work, 16 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_ovf_count, helio_gpu_ctx::kSets * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_pv, (helio_gpu_ctx::kSets + 1) * 4096 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_pi, (helio_gpu_ctx::kSets + 1) * 4096 * sizeof(long long)) != cudaSuccess ||
       cudaMalloc(&ctx->d_best, 2 * 4096 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&ctx->d_bidx, 2 * 4096 * sizeof(int64_t)) != cudaSuccess) {
     helio_gpu_destroy(ctx);
@@ -473,7 +478,7 @@ void helio_gpu_destroy(helio_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < helio_gpu_ctx::kPipeSets; ++i) {
     if (ctx->pipe[i]) {
       cudaStreamSynchronize(ctx->pipe[i]);
       cudaStreamDestroy(ctx->pipe[i]);
@@ -484,8 +489,17 @@ void helio_gpu_destroy(helio_gpu_ctx* ctx) {
     cudaFreeHost(ctx->h_pl_pin[i]);
     cudaFreeHost(ctx->h_val_pin[i]);
     cudaFreeHost(ctx->h_st_pin[i]);
-    cudaFree(ctx->d_ovf[i]);
   }
+  for (int i = 0; i < helio_gpu_ctx::kSets; ++i) cudaFree(ctx->d_ovf[i]);
+  if (ctx->copy) {
+    cudaStreamSynchronize(ctx->copy);
+    cudaStreamDestroy(ctx->copy);
+  }
+  cudaFree(ctx->d_pl_all);
+  cudaFree(ctx->d_val_all);
+  cudaFree(ctx->d_st_all);
+  for (cudaEvent_t e : ctx->ev_in) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_out) cudaEventDestroy(e);
   cudaFree(ctx->d_cluster);
   cudaFree(ctx->d_kmax32);
   cudaFree(ctx->d_work);
@@ -508,8 +522,7 @@ int helio_gpu_sync(helio_gpu_ctx* ctx) {
   std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
-  CK(cudaStreamSynchronize(ctx->pipe[0]));
-  CK(cudaStreamSynchronize(ctx->pipe[1]));
+  for (int i = 0; i < helio_gpu_ctx::kPipeSets; ++i) CK(cudaStreamSynchronize(ctx->pipe[i]));
   return HELIO_OK;
 }
 
@@ -791,7 +804,8 @@ int helio_gpu_score(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int allo
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   FlowOut fo{nullptr, nullptr, nullptr, 0};
-  return launch_score(ctx, 0, d_pl, B, allow_partial ? 1 : 0, d_values, d_status, st, fo, true, ctx->mode);
+  return launch_score(ctx, helio_gpu_ctx::kApiSet, d_pl, B, allow_partial ? 1 : 0, d_values, d_status, st, fo, true,
+                      ctx->mode);
 }
 
 }  // extern "C"
@@ -799,6 +813,88 @@ int helio_gpu_score(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int allo
 namespace {
 int argmax_on(helio_gpu_ctx* ctx, int scratch, const double* d_values, const int32_t* d_status, int64_t B,
               int64_t index_base, double* d_best, int64_t* d_index, cudaStream_t st);
+
+// Pinned caller buffers and a batch that fits kResidentStageBytes: every
+// chunk's H2D is issued up front on the copy stream into a device-resident
+// copy of the batch (no staging reuse, so copies stream back to back at full
+// link rate); chunk c's kernels on pipe[0] wait only for chunk c's copy, and
+// its D2H runs on pipe[1] behind an event, off the kernel stream.
+constexpr size_t kResidentStageBytes = size_t(2) << 30;
+
+int score_host_resident(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allow_partial, double* h_values,
+                        int32_t* h_status, double* h_best, int64_t* h_index, const std::vector<int64_t>& clo,
+                        const std::vector<int64_t>& cn) {
+  const size_t row = sizeof(int16_t) * 2 * ctx->N;
+  const int64_t nchunks = (int64_t)clo.size();
+  if (ctx->all_cap < B) {
+    cudaFree(ctx->d_pl_all);
+    cudaFree(ctx->d_val_all);
+    cudaFree(ctx->d_st_all);
+    ctx->d_pl_all = nullptr;
+    ctx->d_val_all = nullptr;
+    ctx->d_st_all = nullptr;
+    ctx->all_cap = 0;
+    CK(cudaMalloc(&ctx->d_pl_all, row * B));
+    CK(cudaMalloc(&ctx->d_val_all, sizeof(double) * B));
+    CK(cudaMalloc(&ctx->d_st_all, sizeof(int32_t) * B));
+    ctx->all_cap = B;
+  }
+  while ((int64_t)ctx->ev_in.size() < nchunks) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    ctx->ev_in.push_back(a);
+    ctx->ev_out.push_back(b);
+  }
+  for (int64_t c = 0; c < nchunks; ++c) {
+    CK(cudaMemcpyAsync(ctx->d_pl_all + clo[c] * 2 * ctx->N, h_pl + clo[c] * 2 * ctx->N, row * cn[c],
+                       cudaMemcpyHostToDevice, ctx->copy));
+    CK(cudaEventRecord(ctx->ev_in[c], ctx->copy));
+  }
+  FlowOut fo{nullptr, nullptr, nullptr, 0};
+  // kernels alternate between pipe[0] and pipe[2] (scratch sets 0 and 2) so
+  // one chunk's tail overlaps the next chunk's start; D2H on pipe[1]
+  cudaStream_t os = ctx->pipe[1];
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t lo = clo[c], n = cn[c];
+    const int set = (c & 1) ? 2 : 0;
+    cudaStream_t ks = ctx->pipe[set];
+    CK(cudaStreamWaitEvent(ks, ctx->ev_in[c], 0));
+    int rc = launch_score(ctx, set, ctx->d_pl_all + lo * 2 * ctx->N, n, allow_partial ? 1 : 0, ctx->d_val_all + lo,
+                          ctx->d_st_all + lo, ks, fo, false, ctx->mode);
+    if (rc) return rc;
+    if (h_best) {
+      rc = argmax_on(ctx, set, ctx->d_val_all + lo, ctx->d_st_all + lo, n, lo, ctx->d_best + c, ctx->d_bidx + c, ks);
+      if (rc) return rc;
+    }
+    if (h_values) {
+      CK(cudaEventRecord(ctx->ev_out[c], ks));
+      CK(cudaStreamWaitEvent(os, ctx->ev_out[c], 0));
+      CK(cudaMemcpyAsync(h_values + lo, ctx->d_val_all + lo, sizeof(double) * n, cudaMemcpyDeviceToHost, os));
+      CK(cudaMemcpyAsync(h_status + lo, ctx->d_st_all + lo, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, os));
+    }
+  }
+  CK(cudaStreamSynchronize(ctx->pipe[0]));
+  CK(cudaStreamSynchronize(ctx->pipe[2]));
+  CK(cudaStreamSynchronize(os));
+  CK(cudaStreamSynchronize(ctx->copy));
+  if (h_best) {
+    std::vector<double> bv(nchunks);
+    std::vector<int64_t> bi(nchunks);
+    CK(cudaMemcpy(bv.data(), ctx->d_best, sizeof(double) * nchunks, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(bi.data(), ctx->d_bidx, sizeof(int64_t) * nchunks, cudaMemcpyDeviceToHost));
+    double best = 0.0;
+    int64_t idx = -1;
+    for (int64_t c = 0; c < nchunks; ++c)  // chunks in index order: strict '>' keeps the first max
+      if (bi[c] >= 0 && (idx < 0 || bv[c] > best)) {
+        best = bv[c];
+        idx = bi[c];
+      }
+    *h_best = best;
+    if (h_index) *h_index = idx;
+  }
+  return HELIO_OK;
+}
 
 // Host-buffer scoring, pipelined over two streams in chunks: H2D of chunk c+1
 // and D2H of chunk c-1 overlap the kernels of chunk c.  With pinned caller
@@ -818,8 +914,15 @@ int score_host_impl(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allo
     return HELIO_OK;
   }
   CK(cudaSetDevice(ctx->device));
+  // Chunks ramp up from 16k to 256k candidates: the first kernel starts after
+  // a short H2D instead of a full chunk's, then copies hide behind kernels.
   const int64_t chunk = std::min<int64_t>(B, 1 << 18);
-  const int64_t nchunks = (B + chunk - 1) / chunk;
+  std::vector<int64_t> clo, cn;
+  for (int64_t lo = 0, sz = std::min<int64_t>(chunk, 1 << 14); lo < B; lo += sz, sz = std::min(chunk, 2 * sz)) {
+    clo.push_back(lo);
+    cn.push_back(std::min(sz, B - lo));
+  }
+  const int64_t nchunks = (int64_t)clo.size();
   if (h_best && nchunks > 2 * 4096) return fail(ctx, HELIO_ERR_TOO_LARGE, "batch too large for the best reduction");
   int rc = ensure_stage(ctx, chunk);
   if (rc) return rc;
@@ -828,15 +931,17 @@ int score_host_impl(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allo
   const bool pin_out = want_vals && is_pinned(h_values) && is_pinned(h_status);
   const size_t row = sizeof(int16_t) * 2 * ctx->N;
   FlowOut fo{nullptr, nullptr, nullptr, 0};
+  if (pin_in && (!want_vals || pin_out) && (size_t)B * (row + 12) <= kResidentStageBytes)
+    return score_host_resident(ctx, h_pl, B, allow_partial, h_values, h_status, h_best, h_index, clo, cn);
   for (int64_t c = 0; c < nchunks; ++c) {
-    const int s = (int)(c & 1);
+    const int s = (int)(c % helio_gpu_ctx::kPipeSets);
     cudaStream_t st = ctx->pipe[s];
-    const int64_t lo = c * chunk, n = std::min(chunk, B - lo);
-    if (c >= 2 && (!pin_in || (want_vals && !pin_out))) {
-      // staging buffers of chunk c-2 are reused: retire it first
+    const int64_t lo = clo[c], n = cn[c];
+    if (c >= helio_gpu_ctx::kPipeSets && (!pin_in || (want_vals && !pin_out))) {
+      // staging buffers of chunk c-3 are reused: retire it first
       CK(cudaStreamSynchronize(st));
       if (want_vals && !pin_out) {
-        const int64_t plo = (c - 2) * chunk, pn = std::min(chunk, B - plo);
+        const int64_t plo = clo[c - helio_gpu_ctx::kPipeSets], pn = cn[c - helio_gpu_ctx::kPipeSets];
         std::memcpy(h_values + plo, ctx->h_val_pin[s], sizeof(double) * pn);
         std::memcpy(h_status + plo, ctx->h_st_pin[s], sizeof(int32_t) * pn);
       }
@@ -861,12 +966,12 @@ int score_host_impl(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allo
       CK(cudaMemcpyAsync(sdst, ctx->d_st[s], sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
     }
   }
-  const int64_t first_tail = (pin_in && (!want_vals || pin_out)) ? 0 : std::max<int64_t>(0, nchunks - 2);
+  const int64_t first_tail = (pin_in && (!want_vals || pin_out)) ? 0 : std::max<int64_t>(0, nchunks - helio_gpu_ctx::kPipeSets);
   for (int64_t c = first_tail; c < nchunks; ++c) {
-    const int s = (int)(c & 1);
+    const int s = (int)(c % helio_gpu_ctx::kPipeSets);
     CK(cudaStreamSynchronize(ctx->pipe[s]));
     if (want_vals && !pin_out) {
-      const int64_t lo = c * chunk, n = std::min(chunk, B - lo);
+      const int64_t lo = clo[c], n = cn[c];
       std::memcpy(h_values + lo, ctx->h_val_pin[s], sizeof(double) * n);
       std::memcpy(h_status + lo, ctx->h_st_pin[s], sizeof(int32_t) * n);
     }
@@ -931,7 +1036,8 @@ int helio_gpu_flows_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t K, int
     rc = fail(ctx, HELIO_ERR_CUDA, "H2D failed in flows");
   if (!rc) {
     FlowOut fo{d_ed, d_nv, d_ne, max_edges};
-    rc = launch_score(ctx, 0, d_pl, K, allow_partial ? 1 : 0, d_val, d_st, st, fo, false, HELIO_MODE_PARITY);
+    rc = launch_score(ctx, helio_gpu_ctx::kApiSet, d_pl, K, allow_partial ? 1 : 0, d_val, d_st, st, fo, false,
+                      HELIO_MODE_PARITY);
   }
   if (!rc) {
     bool ok = cudaMemcpyAsync(h_values, d_val, 8 * K, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
@@ -980,6 +1086,7 @@ int helio_gpu_maxflow_raw_host(helio_gpu_ctx* ctx, int64_t G, const int32_t* h_n
     return fail(ctx, HELIO_ERR_TOO_LARGE, "raw graph does not fit one SM's shared memory");
   int warps = (int)std::max<size_t>(1, std::min<size_t>(4, max_smem / lay.bytes));
   CK(cudaFuncSetAttribute(raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem));
+  CK(cudaFuncSetAttribute(raw_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raw_kernel, 32 * warps, lay.bytes * warps));
   if (per_sm < 1) per_sm = 1;
@@ -1045,7 +1152,7 @@ int helio_gpu_argmax(helio_gpu_ctx* ctx, const double* d_values, const int32_t* 
   if (!d_best || !d_index || (B > 0 && (!d_values || !d_status))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-  return argmax_on(ctx, 2, d_values, d_status, B, index_base, d_best, d_index, st);
+  return argmax_on(ctx, helio_gpu_ctx::kSets, d_values, d_status, B, index_base, d_best, d_index, st);
 }
 
 int helio_gpu_generate(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B, uint32_t ppm,

@@ -16,6 +16,7 @@ ap.add_argument("--config", default="het42-70b")
 ap.add_argument("--count", type=int, default=200_000)
 ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--mode", default="score", choices=["score", "parity"])
+ap.add_argument("--walk", action="store_true", help="link-walking generator (sparse topologies)")
 a = ap.parse_args()
 c = h.Cluster.from_json(json.dumps(clusters.CONFIGS[a.config]("float")))
 e = h.Engine(c)
@@ -23,7 +24,10 @@ e.mode = a.mode
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 pl = torch.empty((a.count, e.num_nodes, 2), dtype=torch.int16, device="cuda")
-e.generate_device(20240611, 0, a.count, 0, pl.data_ptr(), s.cuda_stream)
+if a.walk:
+    e.generate_walk_device(20240611, 0, a.count, pl.data_ptr(), s.cuda_stream)
+else:
+    e.generate_device(20240611, 0, a.count, 0, pl.data_ptr(), s.cuda_stream)
 v = torch.empty(a.count, dtype=torch.float64, device="cuda")
 st = torch.empty(a.count, dtype=torch.int32, device="cuda")
 for _ in range(a.repeat):
