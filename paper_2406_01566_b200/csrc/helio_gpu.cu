@@ -297,18 +297,29 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   // (12A + 27V + 8N bytes = 6.7 KB) lets 8 four-warp CTAs share an SM — the
   // register limit at 64 registers — instead of 7.
   int a_small = 8 * N;
+  // Sparse interconnects (< 16 links per node, e.g. syn256's 12 peers):
+  // link-walking placements carry ~2.6N edges (max seen 2.75N), so 6N arcs
+  // hold them and the smaller slot buys resident warps.
+  if (ctx->Mv < 16 * N) a_small = 6 * N;
   if (a_small < 2 * ctx->L + 2) a_small = 2 * ctx->L + 2;  // cover/start masks live in cap[]
   int a_struct = 2 * (N + ctx->Mv);
   if (a_small > a_struct) a_small = a_struct;
   if (a_small < 2) a_small = 2;
   ctx->small = make_layout(V, a_small, N, 0);
-  int warps = 4;
-  ctx->small_warps = warps;
   const size_t max_smem = 227 * 1024;
-  if ((size_t)ctx->small.bytes * warps > max_smem) {
-    warps = 1;
-    ctx->small_warps = 1;
+  // warps per CTA: the most resident warps per SM (228 KB, 1 KB reserved per
+  // CTA), preferring larger CTAs on ties
+  int warps = 1, best_res = -1;
+  for (int w : {4, 2, 1}) {
+    const size_t cta = (size_t)ctx->small.bytes * w;
+    if (cta > max_smem) continue;
+    const int res = w * (int)std::min<size_t>(32, (228 * 1024) / (cta + 1024));
+    if (res > best_res) {
+      best_res = res;
+      warps = w;
+    }
   }
+  ctx->small_warps = warps;
   // Big slot: structural maximum (every declared link valid).
   int a_big = a_struct < 2 ? 2 : a_struct;
   if (a_big > 32766) a_big = 32766;
