@@ -216,6 +216,37 @@ def syn256(capacity: str = "float", seed: int = 256) -> dict:
     return {"model": m, "coordinator": {"id": "coord"}, "nodes": nodes, "links": links}
 
 
+def mesh_cluster(n: int, model: str = "llama2-70b", capacity: str = "float", peers: int = 0,
+                 seed: int = 1) -> dict:
+    """n nodes cycling het42's type mix, coordinator <-> every node, and a full
+    mesh (peers == 0) or `peers` seeded random neighbours per node: the
+    size sweep behind the solver-boundary tests (V = 2n + 2 crosses 32, 64,
+    96 and 128)."""
+    m = _model(model, capacity)
+    mix = [t for t, c in HET42_MIX for _ in range(c)]
+    nodes = [_node(f"m{i:03d}", mix[i % len(mix)], m, capacity) for i in range(n)]
+    links: List[dict] = []
+    for x in nodes:
+        _biline(links, "coord", x["id"], 10e9, 0.0002)
+    if peers <= 0:
+        for i in range(n):
+            for j in range(i + 1, n):
+                _biline(links, nodes[i]["id"], nodes[j]["id"], 10e9, 0.001)
+    else:
+        seen = set()
+        state = seed
+        for i in range(n):
+            for _ in range(peers):
+                state = _splitmix64(state)
+                j = state % n
+                key = (min(i, j), max(i, j))
+                if j == i or key in seen:
+                    continue
+                seen.add(key)
+                _biline(links, nodes[i]["id"], nodes[j]["id"], 10e9, 0.001)
+    return {"model": m, "coordinator": {"id": "coord"}, "nodes": nodes, "links": links}
+
+
 def make_node(nid: str, hold_layers: int, peak: float, gtype: str = "gpu") -> dict:
     """test_support.hpp:11-20: k layers at 1 GB beside the KV half."""
     return {"id": nid, "type": gtype, "vram_gb": 2.0 * hold_layers + 1.0, "kv_reserve": 0.5,

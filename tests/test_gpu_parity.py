@@ -383,3 +383,35 @@ def test_concurrent_callers_on_one_engine():
     for (v, s), ((gv, gs), obj) in zip(want, got):
         assert np.array_equal(bits(v), bits(gv)) and np.array_equal(s, gs)
     assert len({obj for _, obj in got}) == 1
+
+
+# --- solver-boundary sweep: V = 2N + 2 crosses the bitset solver's word counts
+# (32 / 64 / 96 / 128 vertices), the N <= 64 cover-mask builders and the
+# general per-node-list builder --------------------------------------------------
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,peers", [(15, 0), (16, 0), (31, 0), (32, 0), (47, 0), (48, 0), (63, 0),
+                                     (64, 0), (65, 0), (100, 0), (100, 8)])
+def test_size_sweep_both_modes_match_oracle(n, peers):
+    model = "llama-30b" if n < 40 else "llama2-70b"  # small clusters must still cover the model
+    for cap in ("float", "int"):
+        d = clusters.mesh_cluster(n, model=model, capacity=cap, peers=peers)
+        c = h.Cluster.from_json(json.dumps(d))
+        e = h.Engine(c)
+        if peers:  # sparse: placements that walk existing links
+            rows = e.generate_walk_host(78 + n, 0, 800)
+        else:
+            rows = np.concatenate([h.generate_host(list(e.kmax), c.num_layers, 77 + n, 0, 600, 0),
+                                   h.generate_host(list(e.kmax), c.num_layers, 78 + n, 0, 200, 200000)])
+        want_v, want_s = Oracle(d).score(rows, True)
+        v, s = e.score(rows, True)
+        assert np.array_equal(s, want_s)
+        assert np.array_equal(bits(v), bits(want_v)), f"PARITY n={n} {cap}"
+        e.mode = "score"
+        vs_, ss_ = e.score(rows, True)
+        assert np.array_equal(ss_, want_s)
+        if cap == "int":
+            assert np.array_equal(bits(vs_), bits(want_v)), f"SCORE n={n} int"
+        else:
+            assert np.all(np.abs(vs_ - want_v) <= 1e-6 * np.maximum(1.0, np.abs(want_v))), f"SCORE n={n}"
+        assert (want_v > 0).mean() > 0.5, "sweep must exercise non-trivial flows"
