@@ -65,6 +65,19 @@ def ncu_traffic_per_eval(mode):
         return None, None
 
 
+def ncu_inst_per_eval(mode):
+    """Warp-instructions per candidate (smsp__inst_executed.sum) of the same
+    committed capture."""
+    import csv
+    path = os.path.join(ROOT, "profiles", f"r01_{mode}_mode_raw.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+        i = rows[0].index("smsp__inst_executed.sum")
+        return float(rows[2][i].replace(",", "")) / PROFILE_GRAPHS
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -609,6 +622,20 @@ def main():
         for r in search["runs"]:  # the same scoring on the reference, at the measured host rate
             r["reference_equivalent_seconds"] = r["scored"] / cpu["value"]
 
+    clocks = clk.summary()
+    # the roofline that binds this kernel: warp-instruction issue (4 schedulers
+    # per SM, one instruction per clock each) — see DESIGN.md §4
+    ipe = ncu_inst_per_eval(args.mode)
+    if ipe and clocks.get("sm_mhz"):
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        issue_peak = sms * 4 * clocks["sm_mhz"] * 1e6
+        issue_ach = ipe * B / (avg_kernel_ms / 1e3)
+        roofline["issue"] = {"bound": "warp-instruction issue", "warp_instr_per_eval": ipe,
+                             "achieved": issue_ach, "peak": issue_peak, "unit": "warp-instr/s",
+                             "frac": issue_ach / issue_peak,
+                             "source": "smsp__inst_executed.sum per candidate from the committed ncu capture; "
+                                       "peak = SMs x 4 schedulers x median SM clock under load"}
+
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
@@ -624,7 +651,7 @@ def main():
                        "best": {"value": win[0], "index": win[1]}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "routing": routing, "other_configs": cfg_table, "split_pipeline": split, "search": search,
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         print(json.dumps(out))
     if world > 1:
