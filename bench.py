@@ -337,30 +337,35 @@ def split_leg(eng, dev, sp, B=200_000):
 
 def search_leg(h, clusters, dev):
     """device local search (helio_gpu_local_search)
-    on het42-70b from the reference's three heuristics, in both modes; host
-    wall clock around each call (neighbour generation, scoring, argmax and the
-    per-move readback all inside)."""
+    on het42-70b from the reference's three heuristics, single-node moves with
+    and without interval swaps, both modes; best-of-three host wall clock
+    around each call (neighbour generation, scoring, argmax and the per-move
+    readback all inside)."""
     import numpy as np
 
     d = clusters.CONFIGS["het42-70b"]("float")
     c = h.Cluster.from_json(json.dumps(d))
     eng = h.Engine(c, dev)
-    out = {"workload": "het42-70b: best-improvement single-node moves from swarm / petals / sp seeds",
-           "neighbours_per_move": None, "runs": []}
+    N = eng.num_nodes
+    singles = sum(1 + sum(min(c.num_layers, s + k) - s for s in range(c.num_layers)) for k in eng.kmax)
+    out = {"workload": "het42-70b: best-improvement local search from swarm / petals / sp seeds",
+           "neighbourhood": {"single_node_moves": singles, "interval_swaps": N * (N - 1) // 2},
+           "runs": []}
     for method in ("swarm", "petals", "sp"):
         placement, _ = h.heuristic_placement(c, method)
         seed = h.placement_rows(c, [{k: tuple(v) for k, v in placement.items()}])[0]
-        for mode in ("score", "parity"):
+        for mode, swaps in (("score", False), ("score", True), ("parity", True)):
             eng.mode = mode
-            eng.local_search(seed, True, 1)  # warm (allocations, first launch)
-            t0 = time.perf_counter()
-            value, row, moves, scored = eng.local_search(seed, True, -1)
-            dt = time.perf_counter() - t0
+            eng.local_search(seed, True, 1, swaps)  # warm (allocations, first launch)
+            dt = float("inf")
+            for _ in range(3):  # best of three (host wall clock)
+                t0 = time.perf_counter()
+                value, row, moves, scored = eng.local_search(seed, True, -1, swaps)
+                dt = min(dt, time.perf_counter() - t0)
             v0, _ = eng.score(seed[None])
-            out["runs"].append({"seed": method, "mode": mode, "seed_value": float(v0[0]), "value": value,
-                                "moves": moves, "scored": scored, "seconds": dt,
+            out["runs"].append({"seed": method, "mode": mode, "swaps": swaps, "seed_value": float(v0[0]),
+                                "value": value, "moves": moves, "scored": scored, "seconds": dt,
                                 "evals_per_s": scored / dt if dt > 0 else None})
-    out["neighbours_per_move"] = int((out["runs"][0]["scored"] - 1) // max(1, out["runs"][0]["moves"] + 1))
     eng.mode = "score"
     return out
 

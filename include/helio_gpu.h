@@ -204,16 +204,25 @@ int helio_gpu_best_exhaustive(helio_gpu_ctx* ctx, int allow_partial, int64_t max
 
 /* Best-improvement local search from a seed placement (
  * seeds typically come from the heuristics of src/heuristics.cpp:12-131).
- * Each iteration scores, in the context's mode, every placement that differs
- * from the current one in exactly one node's interval (node-major; per node
- * the choices of enumerate.hpp:21-28: idle, then [s, e) with e - s <= k_i in
- * (s, e) order) and moves to the first strict maximum when it beats the
- * current value (enumerate.hpp:59).  Stops at a local optimum or after
- * max_moves moves (< 0: no limit).  The seed must pass validation
- * (HELIO_ERR_INVALID otherwise).  Outputs the final value and int16 [N][2]
- * row, the number of moves taken and the placements scored (seed included). */
+ * Each iteration scores, in the context's mode, the neighbourhood of the
+ * current placement and moves to its first strict maximum when that beats
+ * the current value (enumerate.hpp:59).  Neighbourhood bits:
+ *   HELIO_LS_MOVES  every placement that differs in exactly one node's
+ *                   interval, node-major; per node the choices of
+ *                   enumerate.hpp:21-28 (idle, then [s, e) with e - s <= k_i
+ *                   in (s, e) order);
+ *   HELIO_LS_SWAPS  then every exchange of two nodes' intervals, (i, j) with
+ *                   i < j in order (an exchange that breaks k_i scores as
+ *                   invalid and is never taken).
+ * Stops at a local optimum or after max_moves moves (< 0: no limit).  The
+ * seed must pass validation (HELIO_ERR_INVALID otherwise).  Outputs the final
+ * value and int16 [N][2] row, the moves taken and the placements scored
+ * (seed included). */
+#define HELIO_LS_MOVES 1
+#define HELIO_LS_SWAPS 2
 int helio_gpu_local_search(helio_gpu_ctx* ctx, const int16_t* h_seed, int allow_partial, int32_t max_moves,
-                           double* h_value, int16_t* h_row, int32_t* h_moves, int64_t* h_scored);
+                           int32_t neighbourhood, double* h_value, int16_t* h_row, int32_t* h_moves,
+                           int64_t* h_scored);
 
 /* Link-walking covering chains (gen.h hg_candidate_walk) for sparse
  * topologies, device and host (identical output). */

@@ -37,7 +37,8 @@ struct LocalSearchResult {
   int moves = 0;
   long long scored = 0;
 };
+// swaps: also exchange two nodes' intervals (HELIO_LS_SWAPS).
 LocalSearchResult local_search_placement(const ClusterSpec& c, const Placement& seed, bool allow_partial,
-                                         int max_moves = -1);
+                                         int max_moves = -1, bool swaps = true);
 
 }  // namespace helio

@@ -612,16 +612,17 @@ PYBIND11_MODULE(_helio, m) {
 
   m.def(
       "local_search",
-      [](const ClusterSpec& c, const py::dict& seed, bool allow_partial, int max_moves) {
+      [](const ClusterSpec& c, const py::dict& seed, bool allow_partial, int max_moves, bool swaps) {
         const Placement p = placement_from_dict(seed);
         LocalSearchResult r;
         {
           py::gil_scoped_release rel;
-          r = local_search_placement(c, p, allow_partial, max_moves);
+          r = local_search_placement(c, p, allow_partial, max_moves, swaps);
         }
         return py::make_tuple(placement_to_dict(r.placement), r.value, r.moves, r.scored);
       },
       py::arg("cluster"), py::arg("seed"), py::arg("allow_partial") = true, py::arg("max_moves") = -1,
+      py::arg("swaps") = true,
       "Device local search from a placement: (placement, value, moves, placements scored).");
 
   m.def(
@@ -921,7 +922,7 @@ PYBIND11_MODULE(_helio, m) {
       .def(
           "local_search",
           [](PyEngine& e, py::array_t<int16_t, py::array::c_style | py::array::forcecast> seed, bool allow_partial,
-             int32_t max_moves) {
+             int32_t max_moves, bool swaps) {
             const int N = e.eng->num_nodes();
             if (seed.ndim() != 2 || seed.shape(0) != N || seed.shape(1) != 2)
               throw py::value_error("seed must be int16 [num_nodes, 2]");
@@ -932,13 +933,15 @@ PYBIND11_MODULE(_helio, m) {
             int rc;
             {
               py::gil_scoped_release rel;
-              rc = helio_gpu_local_search(e.eng->ctx(), seed.data(), allow_partial ? 1 : 0, max_moves, &value,
+              rc = helio_gpu_local_search(e.eng->ctx(), seed.data(), allow_partial ? 1 : 0, max_moves,
+                                          HELIO_LS_MOVES | (swaps ? HELIO_LS_SWAPS : 0), &value,
                                           row.mutable_data(), &moves, &scored);
             }
             e.eng->check(rc, "helio_gpu_local_search");
             return py::make_tuple(value, row, moves, scored);
           },
-          py::arg("seed"), py::arg("allow_partial") = true, py::arg("max_moves") = -1,
-          "Best-improvement single-node-move local search: (value, row, moves, placements scored).")
+          py::arg("seed"), py::arg("allow_partial") = true, py::arg("max_moves") = -1, py::arg("swaps") = true,
+          "Best-improvement local search over single-node moves (+ interval swaps): "
+          "(value, row, moves, placements scored).")
       .def("sync", [](PyEngine& e) { e.eng->check(helio_gpu_sync(e.eng->ctx()), "helio_gpu_sync"); });
 }

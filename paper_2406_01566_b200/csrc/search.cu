@@ -215,6 +215,8 @@ extern "C" int helio_gpu_best_exhaustive(helio_gpu_ctx* ctx, int allow_partial, 
 // the current value (enumerate.hpp:59's strict '>' and first-wins rule).
 namespace {
 
+// Move t: node_of[t] >= 0 gives that node the packed interval choice[t];
+// node_of[t] < 0 exchanges the intervals of nodes ~node_of[t] and choice[t].
 __global__ void neighbour_rows(const int32_t* __restrict__ cur, int N, const int16_t* __restrict__ node_of,
                                const int32_t* __restrict__ choice, int64_t C, int32_t* __restrict__ rows) {
   const int64_t words = C * N;
@@ -222,35 +224,53 @@ __global__ void neighbour_rows(const int32_t* __restrict__ cur, int N, const int
        q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = q / N;
     const int k = (int)(q - t * N);
-    rows[q] = k == node_of[t] ? choice[t] : __ldg(cur + k);
+    const int a = node_of[t];
+    int32_t w = __ldg(cur + k);
+    if (a >= 0) {
+      if (k == a) w = choice[t];
+    } else {
+      const int i = ~a, j = choice[t];
+      if (k == i) w = __ldg(cur + j);
+      else if (k == j) w = __ldg(cur + i);
+    }
+    rows[q] = w;
   }
 }
 
 }  // namespace
 
 extern "C" int helio_gpu_local_search(helio_gpu_ctx* ctx, const int16_t* h_seed, int allow_partial,
-                                      int32_t max_moves, double* h_value, int16_t* h_row, int32_t* h_moves,
-                                      int64_t* h_scored) {
+                                      int32_t max_moves, int32_t neighbourhood, double* h_value, int16_t* h_row,
+                                      int32_t* h_moves, int64_t* h_scored) {
   if (!ctx) return HELIO_ERR_INVALID;
   std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
   if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
   if (!h_seed || !h_value || !h_row) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  if ((neighbourhood & (HELIO_LS_MOVES | HELIO_LS_SWAPS)) == 0 || (neighbourhood & ~(HELIO_LS_MOVES | HELIO_LS_SWAPS)))
+    return fail(ctx, HELIO_ERR_INVALID, "neighbourhood must be a non-empty set of HELIO_LS_* bits");
   const int N = ctx->N, L = ctx->L;
   CK(cudaSetDevice(ctx->device));
   // the move list: (node, packed interval) in neighbour order
   std::vector<int16_t> node_of;
   std::vector<int32_t> choice;
   auto pack = [](int s, int e) { return (int32_t)(uint16_t)s | (int32_t)((uint32_t)(uint16_t)e << 16); };
-  for (int i = 0; i < N; ++i) {
-    node_of.push_back((int16_t)i);
-    choice.push_back(0);
-    const int k = ctx->h_kmax[i];
-    for (int s = 0; s < L; ++s)
-      for (int e = s + 1; e <= L && e - s <= k; ++e) {
-        node_of.push_back((int16_t)i);
-        choice.push_back(pack(s, e));
+  if (neighbourhood & HELIO_LS_MOVES)
+    for (int i = 0; i < N; ++i) {
+      node_of.push_back((int16_t)i);
+      choice.push_back(0);
+      const int k = ctx->h_kmax[i];
+      for (int s = 0; s < L; ++s)
+        for (int e = s + 1; e <= L && e - s <= k; ++e) {
+          node_of.push_back((int16_t)i);
+          choice.push_back(pack(s, e));
+        }
+    }
+  if (neighbourhood & HELIO_LS_SWAPS)
+    for (int i = 0; i < N; ++i)
+      for (int j = i + 1; j < N; ++j) {
+        node_of.push_back((int16_t)~i);
+        choice.push_back(j);
       }
-  }
   const int64_t C = (int64_t)choice.size();
   cudaStream_t st = ctx->stream;
   int rc = HELIO_OK;
@@ -306,7 +326,11 @@ extern "C" int helio_gpu_local_search(helio_gpu_ctx* ctx, const int16_t* h_seed,
     scored += C;
     if (rc || bi < 0 || !(best > value)) break;
     value = best;
-    cur[node_of[bi]] = choice[bi];
+    if (node_of[bi] >= 0) {
+      cur[node_of[bi]] = choice[bi];
+    } else {
+      std::swap(cur[~node_of[bi]], cur[choice[bi]]);
+    }
     ++moves;
     if (cudaMemcpyAsync(d_cur, cur.data(), 4 * N, cudaMemcpyHostToDevice, st) != cudaSuccess)
       rc = fail(ctx, HELIO_ERR_CUDA, "local search upload");

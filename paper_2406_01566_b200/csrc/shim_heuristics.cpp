@@ -136,15 +136,16 @@ HeuristicResult separate_pipelines_placement(const ClusterSpec& c) {
 }
 
 LocalSearchResult local_search_placement(const ClusterSpec& c, const Placement& seed, bool allow_partial,
-                                         int max_moves) {
+                                         int max_moves, bool swaps) {
   const std::vector<int16_t> row = placement_row(c, seed);  // validates, reference messages
   auto eng = gpu::engine_for(c);                             // PARITY-mode engine
   std::vector<int16_t> out(row.size(), 0);
   LocalSearchResult r;
   int32_t moves = 0;
   int64_t scored = 0;
-  eng->check(helio_gpu_local_search(eng->ctx(), row.data(), allow_partial ? 1 : 0, max_moves, &r.value, out.data(),
-                                    &moves, &scored),
+  const int32_t hood = HELIO_LS_MOVES | (swaps ? HELIO_LS_SWAPS : 0);
+  eng->check(helio_gpu_local_search(eng->ctx(), row.data(), allow_partial ? 1 : 0, max_moves, hood, &r.value,
+                                    out.data(), &moves, &scored),
              "helio_gpu_local_search");
   for (size_t i = 0; i < c.nodes.size(); ++i)
     if (out[2 * i + 1] > out[2 * i]) r.placement[c.nodes[i].id] = Interval{out[2 * i], out[2 * i + 1]};

@@ -428,34 +428,46 @@ def bits(a):
     return np.ascontiguousarray(a, np.float64).view(np.uint64)
 
 
-def neighbour_moves(kmax, L):
-    """Single-node moves in helio_gpu_local_search's order: node-major, per node
-    the choices of enumerate.hpp:21-28 (idle, then [s, e) with e - s <= k_i in
-    (s, e) order).  -> (node int[C], start int[C], end int[C])."""
-    node, st, en = [], [], []
+def neighbour_moves(kmax, L, swaps=False):
+    """helio_gpu_local_search's neighbourhood in its order: single-node moves,
+    node-major, per node the choices of enumerate.hpp:21-28 (idle, then [s, e)
+    with e - s <= k_i in (s, e) order); then (swaps) every exchange of two
+    nodes' intervals, (i, j) with i < j in order.
+    -> (node int[C], start int16[C], end int16[C], partner int[C]): partner
+    >= 0 marks a swap of `node` and `partner` (start/end unused)."""
+    node, st, en, pa = [], [], [], []
     for i, k in enumerate(kmax):
-        node.append(i); st.append(0); en.append(0)
+        node.append(i); st.append(0); en.append(0); pa.append(-1)
         for s in range(L):
             for e in range(s + 1, min(L, s + k) + 1):
-                node.append(i); st.append(s); en.append(e)
-    return np.array(node), np.array(st, np.int16), np.array(en, np.int16)
+                node.append(i); st.append(s); en.append(e); pa.append(-1)
+    if swaps:
+        for i in range(len(kmax)):
+            for j in range(i + 1, len(kmax)):
+                node.append(i); st.append(0); en.append(0); pa.append(j)
+    return np.array(node), np.array(st, np.int16), np.array(en, np.int16), np.array(pa)
 
 
-def local_search_oracle(score, kmax, L, seed_row, max_moves=-1):
+def local_search_oracle(score, kmax, L, seed_row, max_moves=-1, swaps=True):
     """CPU statement of the device local search over any scorer
-    score(rows int16[B,N,2]) -> (values, status): best-improvement single-node
-    moves, first strict maximum over status-OK positive values
+    score(rows int16[B,N,2]) -> (values, status): best-improvement moves over
+    neighbour_moves(), first strict maximum over status-OK positive values
     (enumerate.hpp:59).  -> (value, row, moves, scored)."""
-    node, st, en = neighbour_moves(kmax, L)
+    node, st, en, pa = neighbour_moves(kmax, L, swaps)
     C_ = len(node)
+    single = pa < 0
     cur = np.array(seed_row, np.int16).copy()
     v, s = score(cur[None])
     assert s[0] == 0, "seed must validate"
     value, scored, moves = float(v[0]), 1, 0
+    idx = np.arange(C_)
     while max_moves < 0 or moves < max_moves:
         rows = np.repeat(cur[None], C_, axis=0)
-        rows[np.arange(C_), node, 0] = st
-        rows[np.arange(C_), node, 1] = en
+        rows[idx[single], node[single], 0] = st[single]
+        rows[idx[single], node[single], 1] = en[single]
+        sw = ~single
+        rows[idx[sw], node[sw]] = cur[pa[sw]]
+        rows[idx[sw], pa[sw]] = cur[node[sw]]
         vals, sts = score(rows)
         scored += C_
         ok = (sts == 0) & (vals > 0)
@@ -465,7 +477,7 @@ def local_search_oracle(score, kmax, L, seed_row, max_moves=-1):
         if not vals[bi] > value:
             break
         value = float(vals[bi])
-        cur[node[bi]] = (st[bi], en[bi])
+        cur = rows[bi].copy()
         moves += 1
     return value, cur, moves, scored
 

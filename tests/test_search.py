@@ -81,10 +81,13 @@ def test_separate_pipelines_needs_types():
 def test_neighbour_order_is_enumerate_choice_order():
     from _support import neighbour_moves
 
-    node, s, e = neighbour_moves([1, 2], 3)
+    node, s, e, pa = neighbour_moves([1, 2], 3)
     got = list(zip(node.tolist(), s.tolist(), e.tolist()))
     assert got == [(0, 0, 0), (0, 0, 1), (0, 1, 2), (0, 2, 3),
                    (1, 0, 0), (1, 0, 1), (1, 0, 2), (1, 1, 2), (1, 1, 3), (1, 2, 3)]
+    assert (pa == -1).all()
+    node, s, e, pa = neighbour_moves([1, 2, 1], 3, swaps=True)
+    assert list(zip(node[pa >= 0].tolist(), pa[pa >= 0].tolist())) == [(0, 1), (0, 2), (1, 2)]
 
 
 # --- device local search ------------------------------------------------------
@@ -97,18 +100,18 @@ def _ref_scorer(d, partial=True):
 
 @pytest.mark.gpu
 @needs_ref
-@pytest.mark.parametrize("name,seed_method,max_moves", [
-    ("geo24", "petals", -1), ("geo24", "swarm", -1), ("single24-30b", "petals", -1),
-    ("het42-70b", "petals", 2),
+@pytest.mark.parametrize("name,seed_method,max_moves,swaps", [
+    ("geo24", "petals", -1, True), ("geo24", "swarm", -1, False), ("geo24", "swarm", -1, True),
+    ("single24-30b", "petals", -1, True), ("het42-70b", "petals", 2, True),
 ])
-def test_local_search_matches_reference_driver(name, seed_method, max_moves):
+def test_local_search_matches_reference_driver(name, seed_method, max_moves, swaps):
     d = clusters.CONFIGS[name]()
     c = _cluster(d)
     seed = _row(c, h.heuristic_placement(c, seed_method)[0])
     e = h.Engine(c)  # PARITY: every value is the reference's double
-    value, row, moves, scored = e.local_search(seed, True, max_moves)
+    value, row, moves, scored = e.local_search(seed, True, max_moves, swaps)
     rc, score = _ref_scorer(d)
-    w_value, w_row, w_moves, w_scored = local_search_oracle(score, list(e.kmax), rc.L, seed, max_moves)
+    w_value, w_row, w_moves, w_scored = local_search_oracle(score, list(e.kmax), rc.L, seed, max_moves, swaps)
     assert value == w_value
     assert np.array_equal(row, w_row)
     assert (moves, scored) == (w_moves, w_scored)
