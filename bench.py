@@ -35,6 +35,24 @@ WORKLOAD = ("het42-70b: covering-chain placements (SURVEY.md §8(d) G(seed,i)) o
             "(4 A100-40, 6 V100-16, 8 L4-24, 10 T4-16, 4 2xL4, 6 2xT4, 4 4xT4), full mesh "
             "10 Gb/s (1,806 links), LLaMA-2-70B (80 layers), allow_partial=true")
 SEED = 20240611
+# --config other than the headline: the BASELINE configs as extra bench lines
+# (sparse topologies draw link-walking placements)
+WALK_CONFIGS = {"syn256-120l", "geo24-70b"}
+
+
+def workload_of(name):
+    if name == "het42-70b":
+        return WORKLOAD
+    gen = "link-walking" if name in WALK_CONFIGS else "covering-chain"
+    return f"{name}: {gen} placements (SURVEY.md §8(d)), paper_2406_01566_b200.clusters.{name}, allow_partial=true"
+
+
+def host_rows(h, name, kmax, L, first, n, ppm=0, eng=None):
+    """Candidate rows on the host: G(seed, i) chains, or link walks (which need
+    the compiled cluster's link lists, i.e. an engine)."""
+    if name in WALK_CONFIGS:
+        return eng.generate_walk_host(SEED, first, n)
+    return h.generate_host(kmax, L, SEED, first, n, ppm)
 
 
 def env_int(k, d):
@@ -144,22 +162,26 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def reference_rate(cluster_dict, kmax, L, budget_s, threads, first=0):
+def reference_rate(cluster_dict, kmax, L, budget_s, threads, first=0, rows_fn=None):
     """The unmodified reference (oracle/_ref) on the host cores: build_flow_graph
-    + max_flow per candidate on a std::thread pool.  Returns (evals/s, sample)."""
+    + max_flow per candidate on a std::thread pool.  Returns (evals/s, sample).
+    Inputs are prepared outside the timed call (rows_fn(first, n), default
+    G(seed, i) chains)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from _support import RefCluster, ref_available  # test infrastructure: reference arm only
     import paper_2406_01566_b200 as h
 
     if not ref_available():
         raise RuntimeError("oracle/_ref/libhelio_ref.so missing (build in the container with /root/reference)")
+    if rows_fn is None:
+        rows_fn = lambda f, n: h.generate_host(kmax, L, SEED, f, n, 0)  # noqa: E731
     rc = RefCluster(cluster_dict)
-    probe = h.generate_host(kmax, L, SEED, first, 64 * threads, 0)
+    probe = rows_fn(first, 64 * threads)
     t0 = time.perf_counter()
     rc.score(probe, True, threads)
     rate = len(probe) / max(time.perf_counter() - t0, 1e-6)
     n = int(min(max(rate * budget_s, 64 * threads), 400_000))
-    rows = h.generate_host(kmax, L, SEED, first, n, 0)
+    rows = rows_fn(first, n)
     t0 = time.perf_counter()
     rc.score(rows, True, threads)
     dt = time.perf_counter() - t0
@@ -381,10 +403,15 @@ def run_reference(args):
     c = h.Cluster.from_json(json.dumps(d))
     kmax = [c.max_layers(i) for i in c.node_ids]
     threads = os.cpu_count() or 1
+    rows_fn = None
+    if args.config in WALK_CONFIGS:  # link walks need the compiled link lists (input prep, untimed)
+        gen = h.Engine(c)
+        rows_fn = lambda f, n: host_rows(h, args.config, kmax, c.num_layers, f, n, eng=gen)  # noqa: E731
     rates = []
     samples = 0
     for step in range(args.warmup + args.steps):
-        r, n, dt = reference_rate(d, kmax, c.num_layers, args.ref_step_s, threads, first=step * 10_000_000)
+        r, n, dt = reference_rate(d, kmax, c.num_layers, args.ref_step_s, threads, first=step * 10_000_000,
+                                  rows_fn=rows_fn)
         if step >= args.warmup:
             rates.append(r)
             samples += n
@@ -394,7 +421,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "parallelism": "host threads", "candidates_per_step": samples // max(1, args.steps)},
+        "config": {"workload": workload_of(args.config), "parallelism": "host threads",
+                   "candidates_per_step": samples // max(1, args.steps)},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
                          "sample": f"median of {args.steps} steps, each ~{args.ref_step_s:.0f}s of "
                                    f"build_flow_graph+max_flow on the first candidates of the workload "
@@ -455,7 +483,10 @@ def main():
     sp = stream.cuda_stream
 
     pl = torch.empty((B, N, 2), dtype=torch.int16, device=dev)
-    eng.generate_device(SEED, first, B, args.ppm, pl.data_ptr(), sp)
+    if args.config in WALK_CONFIGS:
+        eng.generate_walk_device(SEED, first, B, pl.data_ptr(), sp)
+    else:
+        eng.generate_device(SEED, first, B, args.ppm, pl.data_ptr(), sp)
     vals = torch.empty(B, dtype=torch.float64, device=dev)
     st = torch.empty(B, dtype=torch.int32, device=dev)
     best = torch.empty(1, dtype=torch.float64, device=dev)
@@ -541,7 +572,8 @@ def main():
     avg_kernel_ms = sum(kms) / len(kms) if kms else ms_per_step
     achieved = bytes_per_eval * B / (avg_kernel_ms / 1e3) / 1e9
     peak, peak_src = load_peaks()
-    tpe, tsrc = ncu_traffic_per_eval(args.mode)
+    # the committed ncu captures are of the headline workload
+    tpe, tsrc = ncu_traffic_per_eval(args.mode) if args.config == "het42-70b" else (None, None)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak,
                 "traffic": (tpe * B) if tpe is not None else None,
@@ -557,7 +589,7 @@ def main():
     # e2e through the C ABI with host buffers (pinned), timed on the host
     e2e = None
     if not args.no_e2e:
-        host = torch.from_numpy(h.generate_host(list(eng.kmax), L, SEED, first, B, args.ppm)).pin_memory()
+        host = torch.from_numpy(host_rows(h, args.config, list(eng.kmax), L, first, B, args.ppm, eng)).pin_memory()
         hv = torch.empty(B, dtype=torch.float64).pin_memory()
         hs = torch.empty(B, dtype=torch.int32).pin_memory()
         for _ in range(2):
@@ -616,7 +648,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            r, n, dt = reference_rate(d, list(eng.kmax), L, args.cpu_seconds, threads)
+            r, n, dt = reference_rate(d, list(eng.kmax), L, args.cpu_seconds, threads,
+                                      rows_fn=lambda f, n: host_rows(h, args.config, list(eng.kmax), L, f, n,
+                                                                     eng=eng))
             cpu = {"value": r, "unit": "evals/s", "cores": threads, "kind": "reference",
                    "sample": f"first {n} candidates of the workload, {dt:.1f}s wall, unmodified reference "
                              f"build_flow_graph+max_flow on a {threads}-thread std::thread pool"}
@@ -630,7 +664,7 @@ def main():
     clocks = clk.summary()
     # the roofline that binds this kernel: warp-instruction issue (4 schedulers
     # per SM, one instruction per clock each) — see DESIGN.md §4
-    ipe = ncu_inst_per_eval(args.mode)
+    ipe = ncu_inst_per_eval(args.mode) if args.config == "het42-70b" else None
     if ipe and clocks.get("sm_mhz"):
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         issue_peak = sms * 4 * clocks["sm_mhz"] * 1e6
@@ -646,7 +680,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "candidates_per_gpu": B, "global_batch": B * world,
+            "config": {"workload": workload_of(args.config), "candidates_per_gpu": B, "global_batch": B * world,
                        "parallelism": f"dp{world} (candidate shards; NCCL all-gather of the 16 B argmax record)",
                        "mode": args.mode, "p_uniform_ppm": args.ppm,
                        "other_mode": {"mode": other, "value": other_rate, "unit": "evals/s",
