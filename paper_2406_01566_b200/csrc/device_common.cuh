@@ -37,6 +37,40 @@ Layout make_layout(int V, int A, int N, int M) {
   return l;
 }
 
+// SCORE layout for the general path (N > 64: per-node-list builder + queue
+// BFS), which touches only cap/to/rv/abeg/cur/q/h/ex/ps/pe: 12A + 16V + 4N
+// bytes instead of 12A + 27V + 8N, so more graphs stay resident per SM.  The
+// regions that path never touches alias live ones.
+Layout make_layout_score_general(int V, int A, int N) {
+  Layout l;
+  l.V = V; l.A = A; l.N = N; l.M = 0;
+  int o = 0;
+  auto take = [&](int bytes, int align) {
+    o = (o + align - 1) / align * align;
+    int r = o;
+    o += bytes;
+    return r;
+  };
+  l.o_cap = take(8 * A, 16);
+  l.o_ex = take(8 * V, 16);  // builder: int fill counters; BFS: bottleneck per vertex
+  l.o_vs = l.o_ex;
+  l.o_to = take(2 * A, 2);
+  l.o_rv = take(2 * A, 2);
+  l.o_abeg = take(2 * (V + 1), 2);
+  l.o_h = take(2 * V, 2);
+  l.o_cur = take(2 * V, 2);
+  l.o_q = take(2 * V, 2);
+  l.o_ps = take(2 * N, 4);
+  l.o_pe = take(2 * N, 2);
+  l.o_cnt = l.o_q;
+  l.o_inq = l.o_q;
+  l.o_vin = l.o_ps;
+  l.o_unode = l.o_ps;
+  l.o_efwd = l.o_ps;
+  l.bytes = (o + 15) / 16 * 16;
+  return l;
+}
+
 // PARITY per-vertex solver state, one 16-byte shared-memory record so a
 // discharge loads it with a single LDS.128.
 struct __align__(16) VState {

@@ -68,8 +68,12 @@ struct helio_gpu_ctx {
   helio_engine::ClusterDev cd{};
   void* d_cluster = nullptr;  // one allocation for all constant arrays
   int32_t* d_kmax32 = nullptr;
-  helio_engine::Layout small{}, big{};
+  helio_engine::Layout small{}, big{};  // PARITY slots (also the split pipeline's)
   int small_warps = 4, small_blocks[2] = {0, 0}, big_blocks[2] = {0, 0};
+  // per-mode slots for score_kernel<MODE> (SCORE uses a compact layout when N > 64)
+  helio_engine::Layout slot_small[2]{}, slot_big[2]{};
+  int slot_warps[2] = {4, 4};
+  bool slot_big_ok[2] = {false, false};
   int mode = 0;  // HELIO_MODE_PARITY
   bool big_ok = false;
 

@@ -305,39 +305,51 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   int a_struct = 2 * (N + ctx->Mv);
   if (a_small > a_struct) a_small = a_struct;
   if (a_small < 2) a_small = 2;
-  ctx->small = make_layout(V, a_small, N, 0);
   const size_t max_smem = 227 * 1024;
-  // warps per CTA: the most resident warps per SM (228 KB, 1 KB reserved per
-  // CTA), preferring larger CTAs on ties
-  int warps = 1, best_res = -1;
-  for (int w : {4, 2, 1}) {
-    const size_t cta = (size_t)ctx->small.bytes * w;
-    if (cta > max_smem) continue;
-    const int res = w * (int)std::min<size_t>(32, (228 * 1024) / (cta + 1024));
-    if (res > best_res) {
-      best_res = res;
-      warps = w;
+  // One mode's slots: the small one with the warps per CTA that keep the most
+  // warps resident per SM (228 KB, 1 KB reserved per CTA; larger CTAs on
+  // ties), and the big one for the structural maximum (every declared link
+  // valid) or the largest arc count that still fits one CTA.
+  auto plan = [&](bool compact, Layout& small, Layout& big, int& warps_out, bool& big_ok) {
+    auto mk = [&](int a) { return compact ? make_layout_score_general(V, a, N) : make_layout(V, a, N, 0); };
+    small = mk(a_small);
+    int warps = 1, best_res = -1;
+    for (int w : {4, 2, 1}) {
+      const size_t cta = (size_t)small.bytes * w;
+      if (cta > max_smem) continue;
+      const int res = w * (int)std::min<size_t>(32, (228 * 1024) / (cta + 1024));
+      if (res > best_res) {
+        best_res = res;
+        warps = w;
+      }
     }
-  }
-  ctx->small_warps = warps;
-  // Big slot: structural maximum (every declared link valid).
-  int a_big = a_struct < 2 ? 2 : a_struct;
-  if (a_big > 32766) a_big = 32766;
-  ctx->big = make_layout(V, a_big, N, 0);
-  ctx->big_ok = (size_t)ctx->big.bytes <= max_smem;
-  if (!ctx->big_ok) {
-    // largest arc count that still fits one CTA
-    int lo = 2, hi = a_big;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) / 2;
-      if ((size_t)make_layout(V, mid, N, 0).bytes <= max_smem) lo = mid;
-      else hi = mid - 1;
+    warps_out = warps;
+    int a_big = a_struct < 2 ? 2 : a_struct;
+    if (a_big > 32766) a_big = 32766;
+    big = mk(a_big);
+    big_ok = (size_t)big.bytes <= max_smem;
+    if (!big_ok) {
+      int lo = 2, hi = a_big;
+      while (lo < hi) {
+        int mid = (lo + hi + 1) / 2;
+        if ((size_t)mk(mid).bytes <= max_smem) lo = mid;
+        else hi = mid - 1;
+      }
+      big = mk(lo);
+      big_ok = (size_t)big.bytes <= max_smem;
     }
-    ctx->big = make_layout(V, lo, N, 0);
-    ctx->big_ok = (size_t)ctx->big.bytes <= max_smem;
-  }
+  };
+  plan(false, ctx->small, ctx->big, ctx->small_warps, ctx->big_ok);
   if ((size_t)ctx->small.bytes * ctx->small_warps > max_smem)
     return fail(ctx, HELIO_ERR_TOO_LARGE, "cluster too large: one graph slot exceeds shared memory");
+  ctx->slot_small[HELIO_MODE_PARITY] = ctx->small;
+  ctx->slot_big[HELIO_MODE_PARITY] = ctx->big;
+  ctx->slot_warps[HELIO_MODE_PARITY] = ctx->small_warps;
+  ctx->slot_big_ok[HELIO_MODE_PARITY] = ctx->big_ok;
+  // SCORE: N <= 64 runs the cover-mask builder and bitset solver on the full
+  // layout (residual rows in the VState bytes); larger clusters the compact one
+  plan(N > 64, ctx->slot_small[HELIO_MODE_SCORE], ctx->slot_big[HELIO_MODE_SCORE],
+       ctx->slot_warps[HELIO_MODE_SCORE], ctx->slot_big_ok[HELIO_MODE_SCORE]);
   // occupancy of both instantiations (PARITY / SCORE)
   void* fns[2] = {reinterpret_cast<void*>(score_kernel<HELIO_MODE_PARITY>),
                   reinterpret_cast<void*>(score_kernel<HELIO_MODE_SCORE>)};
@@ -346,14 +358,14 @@ int configure_layouts(helio_gpu_ctx* ctx) {
     // the whole unified L1/shared array as shared memory: the driver's default
     // carveout (200 KB here) would cap het42 at 7 four-warp CTAs per SM
     CK(cudaFuncSetAttribute(fns[m], cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    const int w = ctx->slot_warps[m];
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[m], 32 * ctx->small_warps,
-                                                     ctx->small.bytes * ctx->small_warps));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[m], 32 * w, ctx->slot_small[m].bytes * w));
     if (per_sm < 1) per_sm = 1;
     ctx->small_blocks[m] = per_sm * ctx->sm_count;
     int per_sm_big = 1;
-    if (ctx->big_ok) {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_big, fns[m], 32, ctx->big.bytes));
+    if (ctx->slot_big_ok[m]) {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_big, fns[m], 32, ctx->slot_big[m].bytes));
       if (per_sm_big < 1) per_sm_big = 1;
     }
     ctx->big_blocks[m] = per_sm_big * ctx->sm_count;
@@ -376,12 +388,14 @@ void launch_score_mode(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t
   unsigned long long* work = ctx->d_work + 2 * set;
   unsigned int* oc = ctx->d_ovf_count + set;
   if (timed) cudaEventRecord(ctx->ev0, st);
-  const int grid = (int)std::min<int64_t>(ctx->small_blocks[MODE], (B + ctx->small_warps - 1) / ctx->small_warps);
-  score_kernel<MODE><<<grid, 32 * ctx->small_warps, ctx->small.bytes * ctx->small_warps, st>>>(
-      ctx->cd, ctx->small, d_pl, B, partial, d_val, d_st, work, ctx->d_ovf[set], oc, 0, fo);
+  const Layout& sl = ctx->slot_small[MODE];
+  const int warps = ctx->slot_warps[MODE];
+  const int grid = (int)std::min<int64_t>(ctx->small_blocks[MODE], (B + warps - 1) / warps);
+  score_kernel<MODE><<<grid, 32 * warps, sl.bytes * warps, st>>>(ctx->cd, sl, d_pl, B, partial, d_val, d_st, work,
+                                                                 ctx->d_ovf[set], oc, 0, fo);
   if (timed) cudaEventRecord(ctx->ev1, st);
   // graphs that overflowed the small slot: same kernel, one warp per CTA, big slot
-  const Layout& bl = ctx->big_ok ? ctx->big : ctx->small;
+  const Layout& bl = ctx->slot_big_ok[MODE] ? ctx->slot_big[MODE] : sl;
   score_kernel<MODE><<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
                                                                    work + 1, ctx->d_ovf[set], oc, 1, fo);
 }
