@@ -562,6 +562,21 @@ def main():
     from paper_2406_01566_b200.dist import reduce_best, unpack_records
     recs = unpack_records(gathered) if world > 1 else [(float(best.item()), int(bidx.item()))]
     win = reduce_best(recs)
+    # the winner's plan reaches every rank: its owner
+    # computes the PARITY per-edge flows and broadcasts row + flows over NCCL
+    winner_plan = None
+    if world > 1 and win[1] >= 0:
+        from paper_2406_01566_b200.dist import share_winner
+        row_w = flows_w = None
+        if win[1] // B == rank:
+            row_w = pl[win[1] - first].cpu().numpy()
+            _, _, _, ne_w, _, dbl_w = eng.flows(row_w[None], True)
+            flows_w = dbl_w[0, :int(ne_w[0]), 1]
+        t_share = time.perf_counter()
+        row_s, flows_s = share_winner(win[1], B, row_w, flows_w)
+        winner_plan = {"owner_rank": win[1] // B, "edges": int(flows_s.size),
+                       "bytes": int(row_s.nbytes + flows_s.nbytes),
+                       "ms": (time.perf_counter() - t_share) * 1e3}
     st_host = st.cpu().numpy()
     nonzero = float((vals.cpu().numpy() > 0).mean())
 
@@ -687,7 +702,7 @@ def main():
                                       "max_rel_diff_vs_headline": rel},
                        "l2": "L2 flushed (256 MB write) between timed steps; inputs 168 MB/GPU",
                        "nonzero_fraction": nonzero, "status_nonzero": int((st_host != 0).sum()),
-                       "best": {"value": win[0], "index": win[1]}},
+                       "best": {"value": win[0], "index": win[1]}, "winner_plan_broadcast": winner_plan},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "routing": routing, "other_configs": cfg_table, "split_pipeline": split, "search": search,
             "clocks": clocks,

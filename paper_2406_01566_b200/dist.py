@@ -53,3 +53,31 @@ def gather_best(rec, world: int, group=None) -> Tuple[float, int]:
     out = torch.empty(2 * world, dtype=torch.int64, device=rec.device)
     dist.all_gather_into_tensor(out, rec, group=group)
     return reduce_best(unpack_records(out))
+
+
+def share_winner(index: int, per_rank: int, row=None, flows=None, group=None):
+    """after the argmax, the rank that owns global
+    candidate `index` broadcasts the winning placement row (int16 [N][2]) and
+    its PARITY per-edge flows (float64 [E], reference edge order) so that every
+    rank can materialise the plan and route without re-scoring.  `row` and
+    `flows` are read on the owner only.  -> (row int16 [N][2], flows float64 [E])
+    on every rank, as CPU numpy arrays."""
+    import torch
+    import torch.distributed as dist
+    owner = index // per_rank
+    me = dist.get_rank(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    meta = torch.zeros(2, dtype=torch.int64, device=dev)
+    if me == owner:
+        meta[0] = int(np.asarray(row).size)
+        meta[1] = int(np.asarray(flows).size)
+    dist.broadcast(meta, src=owner, group=group)
+    nr, ne = int(meta[0]), int(meta[1])
+    r = torch.zeros(nr, dtype=torch.int32, device=dev)  # gloo has no int16 collectives
+    f = torch.zeros(ne, dtype=torch.float64, device=dev)
+    if me == owner:
+        r.copy_(torch.from_numpy(np.ascontiguousarray(row, np.int32).reshape(-1)))
+        f.copy_(torch.from_numpy(np.ascontiguousarray(flows, np.float64).reshape(-1)))
+    dist.broadcast(r, src=owner, group=group)
+    dist.broadcast(f, src=owner, group=group)
+    return r.cpu().numpy().astype(np.int16).reshape(-1, 2), f.cpu().numpy()

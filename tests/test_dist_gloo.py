@@ -77,3 +77,35 @@ def test_reduce_best_rules():
     assert reduce_best([(3.0, 5), (3.0, 2), (1.0, 0)]) == (3.0, 2)
     assert reduce_best([(0.0, -1), (0.0, -1)]) == (0.0, -1)
     assert shard_range(1000, 3) == (3000, 4000)
+
+
+def _share_worker(rank, world, port, q):
+    from paper_2406_01566_b200.dist import share_winner
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    per = 100
+    index = 137  # owned by rank 1
+    row = flows = None
+    if rank == 1:
+        row = np.arange(2 * 7, dtype=np.int16).reshape(7, 2)
+        flows = np.linspace(0.5, 3.5, 11)
+    r, f = share_winner(index, per, row, flows)
+    q.put((rank, (r.tolist(), f.tolist())))
+    dist.destroy_process_group()
+
+
+def test_winner_plan_is_broadcast_from_its_owner():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_share_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = (np.arange(14).reshape(7, 2).tolist(), np.linspace(0.5, 3.5, 11).tolist())
+    assert res[0] == want and res[1] == want
