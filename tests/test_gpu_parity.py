@@ -391,7 +391,7 @@ def test_concurrent_callers_on_one_engine():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,peers", [(15, 0), (16, 0), (31, 0), (32, 0), (47, 0), (48, 0), (63, 0),
-                                     (64, 0), (65, 0), (100, 0), (100, 8)])
+                                     (64, 0), (65, 0), (100, 0), (100, 8), (400, 6)])
 def test_size_sweep_both_modes_match_oracle(n, peers):
     model = "llama-30b" if n < 40 else "llama2-70b"  # small clusters must still cover the model
     for cap in ("float", "int"):
