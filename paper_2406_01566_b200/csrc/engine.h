@@ -15,6 +15,10 @@ namespace helio_engine {
 // Device-side cluster constants (K0 output).
 struct ClusterDev {
   int N, L, Mv;
+  // SCORE solver for graphs with more than 128 vertices: 0 = push-relabel
+  // with global relabels every pr_gr pulses (default), 1 = Edmonds-Karp with
+  // the batched queue BFS (HELIO_LARGE_SOLVER / HELIO_PR_GR, tuning knobs)
+  int large_solver, pr_gr;
   const int16_t* kmax;      // [N]
   const int32_t* lexrank;   // [N]
   const int16_t* lexnode;   // [N] node at lex rank r

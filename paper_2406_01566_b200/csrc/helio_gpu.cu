@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <mutex>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -92,7 +93,9 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     }
     double value = 0.0;
     if (st == 0 && MODE == HELIO_MODE_SCORE) {
-      value = V <= 128 ? solve_ek_bits(g, V, 0, 1, lane) : solve_ek_batched(g, V, 0, 1, lane);
+      value = V <= 128          ? solve_ek_bits(g, V, 0, 1, lane)
+              : cd.large_solver ? solve_ek_batched(g, V, 0, 1, lane)
+                                : solve_pr(g, V, 0, 1, lane, cd.pr_gr);
     } else if (st == 0) {
       solve_fifo2(g, V, 0, 1, lane);
       value = built_value(cd, g, lane);
@@ -296,21 +299,25 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   // (het42: mean 140, p99 159, max seen 165 of 168), and at N = 42 the slot
   // (12A + 27V + 8N bytes = 6.7 KB) lets 8 four-warp CTAs share an SM — the
   // register limit at 64 registers — instead of 7.
-  int a_small = 8 * N;
-  // Sparse interconnects (< 16 links per node, e.g. syn256's 12 peers):
-  // link-walking placements carry ~2.6N edges (max seen 2.75N), so 6N arcs
-  // hold them and the smaller slot buys resident warps.
-  if (ctx->Mv < 16 * N) a_small = 6 * N;
-  if (a_small < 2 * ctx->L + 2) a_small = 2 * ctx->L + 2;  // cover/start masks live in cap[]
-  int a_struct = 2 * (N + ctx->Mv);
-  if (a_small > a_struct) a_small = a_struct;
-  if (a_small < 2) a_small = 2;
+  // Sparse interconnects: link-walking placements carry ~2.6N edges (max
+  // seen 2.75N on syn256), so 6N arcs hold them and the smaller slot buys
+  // resident warps.  PARITY (and the split pipeline's slab) switches below 16
+  // declared links per node; SCORE's compact general layout below 32 (both
+  // directions and the coordinator's count: syn256's 12 peers give ~25).
+  auto small_arcs = [&](int sparse_below) {
+    int a = ctx->Mv < sparse_below * N ? 6 * N : 8 * N;
+    if (a < 2 * ctx->L + 2) a = 2 * ctx->L + 2;  // cover/start masks live in cap[]
+    const int a_struct = 2 * (N + ctx->Mv);
+    if (a > a_struct) a = a_struct;
+    return a < 2 ? 2 : a;
+  };
+  const int a_struct = 2 * (N + ctx->Mv);
   const size_t max_smem = 227 * 1024;
   // One mode's slots: the small one with the warps per CTA that keep the most
   // warps resident per SM (228 KB, 1 KB reserved per CTA; larger CTAs on
   // ties), and the big one for the structural maximum (every declared link
   // valid) or the largest arc count that still fits one CTA.
-  auto plan = [&](bool compact, Layout& small, Layout& big, int& warps_out, bool& big_ok) {
+  auto plan = [&](bool compact, int a_small, Layout& small, Layout& big, int& warps_out, bool& big_ok) {
     auto mk = [&](int a) { return compact ? make_layout_score_general(V, a, N) : make_layout(V, a, N, 0); };
     small = mk(a_small);
     int warps = 1, best_res = -1;
@@ -339,7 +346,7 @@ int configure_layouts(helio_gpu_ctx* ctx) {
       big_ok = (size_t)big.bytes <= max_smem;
     }
   };
-  plan(false, ctx->small, ctx->big, ctx->small_warps, ctx->big_ok);
+  plan(false, small_arcs(16), ctx->small, ctx->big, ctx->small_warps, ctx->big_ok);
   if ((size_t)ctx->small.bytes * ctx->small_warps > max_smem)
     return fail(ctx, HELIO_ERR_TOO_LARGE, "cluster too large: one graph slot exceeds shared memory");
   ctx->slot_small[HELIO_MODE_PARITY] = ctx->small;
@@ -348,7 +355,7 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   ctx->slot_big_ok[HELIO_MODE_PARITY] = ctx->big_ok;
   // SCORE: N <= 64 runs the cover-mask builder and bitset solver on the full
   // layout (residual rows in the VState bytes); larger clusters the compact one
-  plan(N > 64, ctx->slot_small[HELIO_MODE_SCORE], ctx->slot_big[HELIO_MODE_SCORE],
+  plan(N > 64, small_arcs(N > 64 ? 32 : 16), ctx->slot_small[HELIO_MODE_SCORE], ctx->slot_big[HELIO_MODE_SCORE],
        ctx->slot_warps[HELIO_MODE_SCORE], ctx->slot_big_ok[HELIO_MODE_SCORE]);
   // occupancy of both instantiations (PARITY / SCORE)
   void* fns[2] = {reinterpret_cast<void*>(score_kernel<HELIO_MODE_PARITY>),
@@ -758,6 +765,12 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   ctx->cd.N = N;
   ctx->cd.L = L;
   ctx->cd.Mv = Mv;
+  {
+    const char* ls = getenv("HELIO_LARGE_SOLVER");
+    const char* gr = getenv("HELIO_PR_GR");
+    ctx->cd.large_solver = (ls && atoi(ls) == 1) ? 1 : 0;
+    ctx->cd.pr_gr = gr && atoi(gr) > 0 ? atoi(gr) : 16;
+  }
   ctx->cd.kmax = reinterpret_cast<const int16_t*>(base + o_kmax);
   ctx->cd.lexrank = reinterpret_cast<const int32_t*>(base + o_lexrank);
   ctx->cd.lexnode = reinterpret_cast<const int16_t*>(base + o_lexnode);

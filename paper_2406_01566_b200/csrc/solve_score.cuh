@@ -135,6 +135,212 @@ __device__ double solve_ek_batched(const Gs& g, const int n, const int s, const 
   return value;
 }
 
+// ---------------------------------------------------------------------------
+// SCORE solver for n > 128 (deep sparse networks such as syn256's link walks,
+// ~500 vertices, ~40 augmenting paths of ~60 arcs each): synchronous
+// push-relabel, preflow phase only, with periodic global relabels.  The
+// preflow phase ends with a minimum cut and the sink's excess equals the
+// max-flow value, so the excess-return phase is never run.
+//
+// Pulse: the active vertices (excess > 0, height < n, not s/t) in vertex
+// order, 32 per batch, one lane each.  Push rounds: every lane pushes along
+// its next admissible arc (h[u] == h[v] + 1, residual > eps, current-arc
+// order).  Lanes whose target another lower lane also pushes to this round
+// wait one round, so every vertex receives at most one deposit per round and
+// no FP addition order depends on timing; pushes into the sink accumulate in
+// the pushing lane's register and are reduced at the end.  Then every batch
+// vertex with excess left relabels to 1 + min height over its residual arcs
+// (capped at n = dead: it cannot reach the sink).  Global relabel: backward
+// BFS from the sink over residual arcs (warp-cooperative, arc-parallel over
+// the queue, lowest lane wins = exact BFS distances); unreached vertices get
+// n.  Everything is deterministic; on integer capacities every intermediate
+// is an integer-valued double, so the value is exact.
+// Global relabel: exact BFS distances to t over residual arcs into h.  The
+// BFS stops as soon as every live vertex holding excess is labelled: at that
+// point every vertex at distance <= hd (the level of the queue head) is
+// labelled, so hd + 1 is a valid (lower-bound) label for the rest.  Dead
+// vertices (h >= n: distance >= n, i.e. unreachable) stay dead; anything the
+// exhausted BFS never reached becomes dead.  q: n-entry queue scratch.
+__device__ void pr_global_relabel(const Gs& g, int16_t* q, const int n, const int s, const int t, const int lane) {
+  const unsigned lt = lanemask_lt();
+  const unsigned le = lt | (1u << lane);
+  int need = 0;
+  for (int x = lane; x < n; x += 32) {
+    const int hx = g.h[x];
+    const bool dead = x == s || hx >= n;
+    if (!dead && x != t && g.ex[x] > 0.0) ++need;
+    g.h[x] = (int16_t)(dead ? n : -1);
+  }
+  need = __reduce_add_sync(FULL, need);
+  __syncwarp();
+  if (lane == 0) {
+    g.h[t] = 0;
+    q[0] = (int16_t)t;
+  }
+  __syncwarp();
+  // the queue's arcs form one stream; each step gives lane j stream arc j.
+  // off = arcs of q[qh] already scanned (a vertex with > 32 arcs spans steps)
+  int qh = 0, qt = 1, off = 0;
+  while (qh < qt) {
+    const int avail = min(32, qt - qh);
+    int vi = 0, bi = 0, di = 0;
+    if (lane < avail) {
+      vi = q[qh + lane];
+      bi = g.abeg[vi];
+      di = g.abeg[vi + 1] - bi;
+      if (lane == 0) {
+        bi += off;
+        di -= off;
+      }
+    }
+    int incl = di;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int start = incl - di;
+    const unsigned sm = __reduce_or_sync(FULL, (lane < avail && di > 0 && start < 32) ? (1u << start) : 0u);
+    const int total = min(32, __shfl_sync(FULL, incl, avail - 1));
+    const int slot = __popc(sm & le) - 1;
+    const int su = slot < 0 ? 0 : slot;
+    const int u_b = __shfl_sync(FULL, bi, su);
+    const int u_st = __shfl_sync(FULL, start, su);
+    const int u_v = __shfl_sync(FULL, vi, su);
+    const int kfull = __popc(__ballot_sync(FULL, lane < avail && incl <= 32));
+    const int p_st = __shfl_sync(FULL, start, kfull & 31);
+    bool ok = false;
+    int x = 0;
+    if (lane < total) {
+      const int a = u_b + (lane - u_st);
+      x = g.to[a];
+      // arc x -> u_v is residual (the reverse of a); x not yet labelled
+      ok = g.h[x] == -1 && g.cap[g.rv[a]] > FLOW_EPS;
+    }
+    const unsigned cand = __ballot_sync(FULL, ok);
+    if (ok) ok = (__match_any_sync(cand, x) & lt) == 0u;
+    const unsigned m = __ballot_sync(FULL, ok);
+    if (ok) {
+      g.h[x] = (int16_t)(g.h[u_v] + 1);
+      q[qt + __popc(m & lt)] = (int16_t)x;
+    }
+    qt += __popc(m);
+    need -= __popc(__ballot_sync(FULL, ok && g.ex[x] > 0.0));
+    if (kfull < avail) {  // q[qh + kfull] continues into the next step
+      off = (kfull == 0 ? off : 0) + (32 - p_st);
+    } else {
+      off = 0;
+    }
+    qh += kfull;
+    __syncwarp();
+    if (need == 0 && qh < qt) break;
+  }
+  const int rest = qh < qt ? g.h[q[qh]] + 1 : n;
+  for (int x = lane; x < n; x += 32)
+    if (g.h[x] == -1) g.h[x] = (int16_t)rest;
+  __syncwarp();
+}
+
+__device__ double solve_pr(const Gs& g, const int n, const int s, const int t, const int lane, const int gr_every) {
+  const unsigned lt = lanemask_lt();
+  int16_t* act = g.q;    // active list of the pulse
+  int16_t* bq = g.cur;   // global-relabel queue
+  for (int x = lane; x < n; x += 32) {
+    g.ex[x] = 0.0;
+    g.h[x] = 0;  // live until the first global relabel
+  }
+  __syncwarp();
+  if (lane == 0) {  // saturate the source's arcs in adjacency order
+    for (int a = g.abeg[s], e = g.abeg[s + 1]; a < e; ++a) {
+      const double c = g.cap[a];
+      if (c > 0.0) {
+        const int v = g.to[a];
+        g.cap[a] = 0.0;
+        g.cap[g.rv[a]] += c;
+        g.ex[v] += c;
+      }
+    }
+  }
+  __syncwarp();
+  double sink = 0.0;  // this lane's pushes into t
+  int since = gr_every;
+  for (;;) {
+    if (since >= gr_every) {
+      pr_global_relabel(g, bq, n, s, t, lane);
+      since = 0;
+    }
+    ++since;
+    int nact = 0;
+    for (int x0 = 0; x0 < n; x0 += 32) {
+      const int x = x0 + lane;
+      const bool a = x < n && x != s && x != t && g.ex[x] > 0.0 && g.h[x] < n;
+      const unsigned m = __ballot_sync(FULL, a);
+      if (a) act[nact + __popc(m & lt)] = (int16_t)x;
+      nact += __popc(m);
+    }
+    if (nact == 0) break;
+    __syncwarp();
+    for (int base = 0; base < nact; base += 32) {
+      const int u = base + lane < nact ? act[base + lane] : -1;
+      int a = 0, ae = 0, hu = 0;
+      if (u >= 0) {
+        a = g.abeg[u];
+        ae = g.abeg[u + 1];
+        hu = g.h[u];
+      }
+      for (;;) {
+        double e = 0.0, c = 0.0;
+        int v = -1;
+        if (u >= 0) {
+          e = g.ex[u];
+          if (e > 0.0)
+            for (; a < ae; ++a) {
+              const int w = g.to[a];
+              if (g.h[w] == hu - 1) {
+                c = g.cap[a];
+                if (c > FLOW_EPS) {
+                  v = w;
+                  break;
+                }
+              }
+            }
+        }
+        const unsigned pm = __ballot_sync(FULL, v >= 0);
+        if (pm == 0u) break;
+        const unsigned nm = __ballot_sync(FULL, v >= 0 && v != t);
+        bool go = v >= 0;
+        if (v >= 0 && v != t) go = (__match_any_sync(nm, v) & lt) == 0u;  // lowest lane per target
+        double d = 0.0;
+        if (go) {
+          d = ref_min(e, c);
+          g.cap[a] = c - d;
+          g.cap[g.rv[a]] += d;
+          g.ex[u] = e - d;
+          if (v == t) sink += d;
+          if (d == c) ++a;  // saturated (else u is drained)
+        }
+        __syncwarp();
+        if (go && v != t) g.ex[v] += d;
+        __syncwarp();
+      }
+      // relabel what still has excess: every arc was scanned, none admissible
+      int nl = -1;
+      if (u >= 0 && g.ex[u] > 0.0) {
+        int best = n;
+        for (int b = g.abeg[u]; b < ae; ++b)
+          if (g.cap[b] > FLOW_EPS) best = min(best, g.h[g.to[b]] + 1);
+        nl = best;
+      }
+      __syncwarp();
+      if (nl >= 0) g.h[u] = (int16_t)nl;
+      __syncwarp();
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sink += __shfl_xor_sync(FULL, sink, o);
+  return g.ex[t] + sink;
+}
+
 // SCORE solver for n <= 128: Edmonds-Karp with a level-synchronous bitset
 // BFS.  Vertex sets are four 32-bit words (vertex v = bit v & 31 of word
 // v >> 5), so lane l owns vertices l, l+32, l+64, l+96 and its bit in every
