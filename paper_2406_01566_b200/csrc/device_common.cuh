@@ -63,7 +63,7 @@ Layout make_layout_score_general(int V, int A, int N) {
   l.o_ps = take(2 * N, 4);
   l.o_pe = take(2 * N, 2);
   l.o_cnt = l.o_q;
-  l.o_inq = l.o_q;
+  l.o_inq = l.o_ps;  // push-relabel FIFO flags (V <= 4N bytes) over the builder's ps/pe
   l.o_vin = l.o_ps;
   l.o_unode = l.o_ps;
   l.o_efwd = l.o_ps;

@@ -769,7 +769,7 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
     const char* ls = getenv("HELIO_LARGE_SOLVER");
     const char* gr = getenv("HELIO_PR_GR");
     ctx->cd.large_solver = (ls && atoi(ls) == 1) ? 1 : 0;
-    ctx->cd.pr_gr = gr && atoi(gr) > 0 ? atoi(gr) : 16;
+    ctx->cd.pr_gr = gr && atoi(gr) > 0 ? atoi(gr) : 20;
   }
   ctx->cd.kmax = reinterpret_cast<const int16_t*>(base + o_kmax);
   ctx->cd.lexrank = reinterpret_cast<const int32_t*>(base + o_lexrank);

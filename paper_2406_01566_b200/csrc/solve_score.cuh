@@ -142,15 +142,16 @@ __device__ double solve_ek_batched(const Gs& g, const int n, const int s, const 
 // preflow phase ends with a minimum cut and the sink's excess equals the
 // max-flow value, so the excess-return phase is never run.
 //
-// Pulse: the active vertices (excess > 0, height < n, not s/t) in vertex
-// order, 32 per batch, one lane each.  Push rounds: every lane pushes along
+// Batches: live vertices with excess (height < n, not s/t) wait in a FIFO
+// (each at most once); a batch pops up to 32 of them, one lane each.  Push rounds: every lane pushes along
 // its next admissible arc (h[u] == h[v] + 1, residual > eps, current-arc
 // order).  Lanes whose target another lower lane also pushes to this round
 // wait one round, so every vertex receives at most one deposit per round and
 // no FP addition order depends on timing; pushes into the sink accumulate in
-// the pushing lane's register and are reduced at the end.  Then every batch
-// vertex with excess left relabels to 1 + min height over its residual arcs
-// (capped at n = dead: it cannot reach the sink).  Global relabel: backward
+// the pushing lane's register and are reduced at the end; receivers join the
+// FIFO tail in lane order.  Then every batch vertex with excess left relabels to 1 + min height over its residual arcs
+// (capped at n = dead: it cannot reach the sink) and rejoins the FIFO.
+// Every gr_every batches a global relabel runs: backward
 // BFS from the sink over residual arcs (warp-cooperative, arc-parallel over
 // the queue, lowest lane wins = exact BFS distances); unreached vertices get
 // n.  Everything is deterministic; on integer capacities every intermediate
@@ -243,13 +244,16 @@ __device__ void pr_global_relabel(const Gs& g, int16_t* q, const int n, const in
 
 __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, const int lane, const int gr_every) {
   const unsigned lt = lanemask_lt();
-  int16_t* act = g.q;    // active list of the pulse
+  int16_t* fq = g.q;     // circular FIFO of live vertices with excess (<= n entries)
+  uint8_t* inq = g.inq;  // FIFO membership
   int16_t* bq = g.cur;   // global-relabel queue
   for (int x = lane; x < n; x += 32) {
     g.ex[x] = 0.0;
     g.h[x] = 0;  // live until the first global relabel
+    inq[x] = 0;
   }
   __syncwarp();
+  int head = 0, cnt = 0;
   if (lane == 0) {  // saturate the source's arcs in adjacency order
     for (int a = g.abeg[s], e = g.abeg[s + 1]; a < e; ++a) {
       const double c = g.cap[a];
@@ -258,83 +262,111 @@ __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, c
         g.cap[a] = 0.0;
         g.cap[g.rv[a]] += c;
         g.ex[v] += c;
+        if (v != t && v != s && !inq[v]) {
+          inq[v] = 1;
+          fq[cnt++] = (int16_t)v;
+        }
       }
     }
   }
+  cnt = __shfl_sync(FULL, cnt, 0);
   __syncwarp();
   double sink = 0.0;  // this lane's pushes into t
   int since = gr_every;
-  for (;;) {
+  while (cnt > 0) {
     if (since >= gr_every) {
       pr_global_relabel(g, bq, n, s, t, lane);
       since = 0;
     }
     ++since;
-    int nact = 0;
-    for (int x0 = 0; x0 < n; x0 += 32) {
-      const int x = x0 + lane;
-      const bool a = x < n && x != s && x != t && g.ex[x] > 0.0 && g.h[x] < n;
-      const unsigned m = __ballot_sync(FULL, a);
-      if (a) act[nact + __popc(m & lt)] = (int16_t)x;
-      nact += __popc(m);
-    }
-    if (nact == 0) break;
-    __syncwarp();
-    for (int base = 0; base < nact; base += 32) {
-      const int u = base + lane < nact ? act[base + lane] : -1;
-      int a = 0, ae = 0, hu = 0;
-      if (u >= 0) {
+    // pop up to 32 (FIFO order); entries that died since they were queued drop out
+    const int take = min(32, cnt);
+    int u = -1, a = 0, ae = 0, hu = 0;
+    if (lane < take) {
+      int p = head + lane;
+      if (p >= n) p -= n;
+      u = fq[p];
+      inq[u] = 0;
+      hu = g.h[u];
+      if (hu < n && g.ex[u] > 0.0) {
         a = g.abeg[u];
         ae = g.abeg[u + 1];
-        hu = g.h[u];
+      } else {
+        u = -1;
       }
-      for (;;) {
-        double e = 0.0, c = 0.0;
-        int v = -1;
-        if (u >= 0) {
-          e = g.ex[u];
-          if (e > 0.0)
-            for (; a < ae; ++a) {
-              const int w = g.to[a];
-              if (g.h[w] == hu - 1) {
-                c = g.cap[a];
-                if (c > FLOW_EPS) {
-                  v = w;
-                  break;
-                }
+    }
+    head += take;
+    if (head >= n) head -= n;
+    cnt -= take;
+    int tail = head + cnt;
+    if (tail >= n) tail -= n;
+    __syncwarp();
+    for (;;) {
+      double e = 0.0, c = 0.0;
+      int v = -1;
+      if (u >= 0) {
+        e = g.ex[u];
+        if (e > 0.0)
+          for (; a < ae; ++a) {
+            const int w = g.to[a];
+            if (g.h[w] == hu - 1) {
+              c = g.cap[a];
+              if (c > FLOW_EPS) {
+                v = w;
+                break;
               }
             }
-        }
-        const unsigned pm = __ballot_sync(FULL, v >= 0);
-        if (pm == 0u) break;
-        const unsigned nm = __ballot_sync(FULL, v >= 0 && v != t);
-        bool go = v >= 0;
-        if (v >= 0 && v != t) go = (__match_any_sync(nm, v) & lt) == 0u;  // lowest lane per target
-        double d = 0.0;
-        if (go) {
-          d = ref_min(e, c);
-          g.cap[a] = c - d;
-          g.cap[g.rv[a]] += d;
-          g.ex[u] = e - d;
-          if (v == t) sink += d;
-          if (d == c) ++a;  // saturated (else u is drained)
-        }
-        __syncwarp();
-        if (go && v != t) g.ex[v] += d;
-        __syncwarp();
+          }
       }
-      // relabel what still has excess: every arc was scanned, none admissible
-      int nl = -1;
-      if (u >= 0 && g.ex[u] > 0.0) {
-        int best = n;
-        for (int b = g.abeg[u]; b < ae; ++b)
-          if (g.cap[b] > FLOW_EPS) best = min(best, g.h[g.to[b]] + 1);
-        nl = best;
+      const unsigned pm = __ballot_sync(FULL, v >= 0);
+      if (pm == 0u) break;
+      const unsigned nm = __ballot_sync(FULL, v >= 0 && v != t);
+      bool go = v >= 0;
+      if (v >= 0 && v != t) go = (__match_any_sync(nm, v) & lt) == 0u;  // lowest lane per target
+      double d = 0.0;
+      if (go) {
+        d = ref_min(e, c);
+        g.cap[a] = c - d;
+        g.cap[g.rv[a]] += d;
+        g.ex[u] = e - d;
+        if (v == t) sink += d;
+        if (d == c) ++a;  // saturated (else u is drained)
       }
       __syncwarp();
-      if (nl >= 0) g.h[u] = (int16_t)nl;
+      const bool app = go && v != t && !inq[v];
+      if (go && v != t) g.ex[v] += d;
+      const unsigned am = __ballot_sync(FULL, app);
+      if (app) {
+        int p = tail + __popc(am & lt);
+        if (p >= n) p -= n;
+        fq[p] = (int16_t)v;
+        inq[v] = 1;
+      }
+      tail += __popc(am);
+      if (tail >= n) tail -= n;
+      cnt += __popc(am);
       __syncwarp();
     }
+    // relabel what still has excess: every arc was scanned, none admissible
+    int nl = -1;
+    if (u >= 0 && g.ex[u] > 0.0) {
+      int best = n;
+      for (int b2 = g.abeg[u]; b2 < ae; ++b2)
+        if (g.cap[b2] > FLOW_EPS) best = min(best, g.h[g.to[b2]] + 1);
+      nl = best;
+    }
+    __syncwarp();
+    const bool app = nl >= 0 && nl < n && !inq[u];
+    if (nl >= 0) g.h[u] = (int16_t)nl;
+    const unsigned am = __ballot_sync(FULL, app);
+    if (app) {
+      int p = tail + __popc(am & lt);
+      if (p >= n) p -= n;
+      fq[p] = (int16_t)u;
+      inq[u] = 1;
+    }
+    cnt += __popc(am);
+    __syncwarp();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sink += __shfl_xor_sync(FULL, sink, o);
