@@ -415,3 +415,39 @@ def test_size_sweep_both_modes_match_oracle(n, peers):
         else:
             assert np.all(np.abs(vs_ - want_v) <= 1e-6 * np.maximum(1.0, np.abs(want_v))), f"SCORE n={n}"
         assert (want_v > 0).mean() > 0.5, "sweep must exercise non-trivial flows"
+
+
+def test_push_relabel_solver_on_deep_sparse_graphs():
+    """SCORE on graphs over 128 vertices runs the push-relabel solver
+    (solve_score.cuh solve_pr): on syn256 link walks it must be bit-exact
+    against the reference on integer capacities, within 1e-6 on float ones,
+    deterministic run to run, and agree with the Edmonds-Karp solver it
+    replaced (HELIO_LARGE_SOLVER=1)."""
+    import os
+    for cap in ("int", "float"):
+        d = clusters.CONFIGS["syn256-120l"](cap)
+        c = h.Cluster.from_json(json.dumps(d))
+        e = h.Engine(c)
+        rows = e.generate_walk_host(4242, 0, 3000)
+        vo, so = Oracle(d).score(rows[:600])
+        e.mode = "score"
+        v1, s1 = e.score(rows)
+        v2, s2 = e.score(rows)
+        assert np.array_equal(bits(v1), bits(v2)) and np.array_equal(s1, s2), "not deterministic"
+        assert np.array_equal(s1[:600], so)
+        if cap == "int":
+            assert np.array_equal(bits(v1[:600]), bits(vo))
+        else:
+            assert np.all(np.abs(v1[:600] - vo) <= SCORE_REL_TOL * np.maximum(1.0, np.abs(vo)))
+        os.environ["HELIO_LARGE_SOLVER"] = "1"
+        try:
+            e_ek = h.Engine(h.Cluster.from_json(json.dumps(d)))
+        finally:
+            del os.environ["HELIO_LARGE_SOLVER"]
+        e_ek.mode = "score"
+        vk, sk = e_ek.score(rows)
+        assert np.array_equal(sk, s1)
+        if cap == "int":
+            assert np.array_equal(bits(vk), bits(v1))
+        else:
+            assert np.all(np.abs(vk - v1) <= SCORE_REL_TOL * np.maximum(1.0, np.abs(v1)))
