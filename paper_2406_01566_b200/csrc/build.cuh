@@ -225,40 +225,38 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
   if (V > lay.V) return ST_OVERFLOW;
   __syncwarp();
   // degrees: in_k = compute + valid in-links + source arc; out_k = compute +
-  // valid out-links + sink arc.
+  // valid out-links + sink arc.  One pass over the out-lists: a valid link
+  // k -> j adds to out_k here and to in_j through a shared atomic.
   int nedges = 0, dsrc = 0, dsink = 0;
   int* fill = reinterpret_cast<int*>(g.ex);  // int counters per vertex during the build
+  for (int x = lane; x < V; x += 32) fill[x] = 0;
+  __syncwarp();
   for (int k = lane; k < N; k += 32) {
     const int s = g.ps[k], e = g.pe[k];
-    int din = 0, dout = 0;
-    if (e > s) {
-      din = 1;
-      dout = 1;
-      ++nedges;
-      for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
-        const int j = __ldg(&cd.out_list[p].x);
-        const int sj = g.ps[j], ej = g.pe[j];
-        if (ej > sj && edge_ok(e, sj, ej, partial)) ++dout;
-      }
-      for (int p = __ldg(cd.in_beg + k), pe_ = __ldg(cd.in_beg + k + 1); p < pe_; ++p) {
-        const int i = __ldg(&cd.in_list[p].x);
-        const int si = g.ps[i], ei = g.pe[i];
-        if (ei > si && edge_ok(ei, s, e, partial)) ++din;
-      }
-      nedges += dout - 1;  // each link edge counted once, at its source
-      if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
-        ++din;
-        ++dsrc;
-        ++nedges;
-      }
-      if (e == L && __ldg(cd.cin_link + k) >= 0) {
+    if (e <= s) continue;
+    int din = 1, dout = 1;
+    ++nedges;
+    for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
+      const int j = __ldg(&cd.out_list[p].x);
+      const int sj = g.ps[j], ej = g.pe[j];
+      if (ej > sj && edge_ok(e, sj, ej, partial)) {
         ++dout;
-        ++dsink;
-        ++nedges;
+        atomicAdd(&fill[2 + 2 * j], 1);
       }
     }
-    g.cur[2 + 2 * k] = (int16_t)din;
-    g.cur[3 + 2 * k] = (int16_t)dout;
+    nedges += dout - 1;  // each link edge counted once, at its source
+    if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
+      ++din;
+      ++dsrc;
+      ++nedges;
+    }
+    if (e == L && __ldg(cd.cin_link + k) >= 0) {
+      ++dout;
+      ++dsink;
+      ++nedges;
+    }
+    atomicAdd(&fill[2 + 2 * k], din);
+    fill[3 + 2 * k] = dout;  // only this lane touches an out-vertex's count
   }
   nedges = __reduce_add_sync(FULL, nedges);
   dsrc = __reduce_add_sync(FULL, dsrc);
@@ -266,14 +264,16 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
   E = nedges;
   if (2 * E > lay.A) return ST_OVERFLOW;
   if (lane == 0) {
-    g.cur[0] = (int16_t)dsrc;
-    g.cur[1] = (int16_t)dsink;
+    fill[0] = dsrc;
+    fill[1] = dsink;
   }
   __syncwarp();
+  // arc ranges; each used node's compute pair takes slot 0 of both its
+  // vertices (so the pair arc of x >= 2 is arc abeg[x]), the rest fill in.
   int run = 0;
   for (int x0 = 0; x0 < V; x0 += 32) {
     const int x = x0 + lane;
-    const int d = x < V ? g.cur[x] : 0;
+    const int d = x < V ? fill[x] : 0;
     int incl = d;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -282,7 +282,7 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
     }
     if (x < V) {
       g.abeg[x] = (int16_t)(run + incl - d);
-      fill[x] = 0;
+      fill[x] = (x >= 2 && d > 0) ? 1 : 0;
     }
     run += __shfl_sync(FULL, incl, 31);
   }
@@ -294,8 +294,8 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
     const int s = g.ps[k], e = g.pe[k];
     if (e <= s) continue;
     const int vi = 2 + 2 * k, vo = vi + 1;
-    const int ai = g.abeg[vi] + atomicAdd(&fill[vi], 1);
-    const int ao = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+    const int ai = g.abeg[vi];
+    const int ao = g.abeg[vo];
     g.to[ai] = (int16_t)vo;
     g.rv[ai] = (int16_t)ao;
     g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
@@ -440,7 +440,8 @@ __device__ int build_graph_score_small(const ClusterDev& cd, const Gs& g, const 
   }
   if (lane == 0) g.abeg[V] = (int16_t)run;
   __syncwarp();
-  for (int x = lane; x < V; x += 32) fill[x] = 0;
+  // each used node's compute pair takes slot 0 of both its vertices
+  for (int x = lane; x < V; x += 32) fill[x] = (x >= 2 && g.abeg[x + 1] > g.abeg[x]) ? 1 : 0;
   __syncwarp();
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
@@ -449,8 +450,8 @@ __device__ int build_graph_score_small(const ClusterDev& cd, const Gs& g, const 
     const int s = g.ps[k], e = g.pe[k];
     if (e <= s) continue;
     const int vi = 2 + 2 * k, vo = vi + 1;
-    const int ai = g.abeg[vi] + atomicAdd(&fill[vi], 1);
-    const int ao = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+    const int ai = g.abeg[vi];
+    const int ao = g.abeg[vo];
     g.to[ai] = (int16_t)vo;
     g.rv[ai] = (int16_t)ao;
     g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);

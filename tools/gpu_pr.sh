@@ -1,5 +1,5 @@
 set -x
-for v in "HELIO_PR_GR=8" "HELIO_PR_GR=12" "HELIO_PR_GR=16" "HELIO_PR_GR=24" "HELIO_PR_GR=32" "HELIO_PR_GR=48"; do
+for v in "HELIO_PR_GR=20"; do
   env $v timeout 300 python tools/profile_score.py --config syn256-120l --walk --count 20000 --repeat 2 2>&1 | tail -1 | sed "s/^/$v /"
 done
 timeout 300 python tools/profile_score.py --count 200000 --repeat 2 2>&1 | tail -1
