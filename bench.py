@@ -62,14 +62,27 @@ def env_int(k, d):
         return d
 
 
-PROFILE_GRAPHS = 200_000  # tools/profile_score.py default: candidates in the profiled launch
+# committed ncu --set full captures of one score_kernel launch (tools/profile_score.py):
+# (config, mode) -> (file under profiles/, candidates in the profiled launch)
+PROFILES = {
+    ("het42-70b", "score"): ("r01_score_mode_raw.csv", 200_000),
+    ("het42-70b", "parity"): ("r01_parity_mode_raw.csv", 200_000),
+    ("syn256-120l", "score"): ("r01_syn256_score_raw.csv", 20_000),
+}
 
 
-def ncu_traffic_per_eval(mode):
+def _profile(config, mode):
+    f, n = PROFILES.get((config, mode), (None, 0))
+    return (os.path.join(ROOT, "profiles", f), n) if f else (None, 0)
+
+
+def ncu_traffic_per_eval(config, mode):
     """DRAM bytes (read + write) per candidate of the committed ncu --set full
-    capture of score_kernel in this mode (profiles/r01_<mode>_mode_raw.csv)."""
+    capture of score_kernel for this config and mode (PROFILES)."""
     import csv
-    path = os.path.join(ROOT, "profiles", f"r01_{mode}_mode_raw.csv")
+    path, graphs = _profile(config, mode)
+    if path is None:
+        return None, None, 0
     try:
         rows = list(csv.reader(open(path)))
         h, u, v = rows[0], rows[1], rows[2]
@@ -78,20 +91,22 @@ def ncu_traffic_per_eval(mode):
         for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             i = h.index(name)
             tot += float(v[i].replace(",", "")) * scale.get(u[i], 1.0)
-        return tot / PROFILE_GRAPHS, os.path.relpath(path, ROOT)
+        return tot / graphs, os.path.relpath(path, ROOT), graphs
     except Exception:
-        return None, None
+        return None, None, 0
 
 
-def ncu_inst_per_eval(mode):
+def ncu_inst_per_eval(config, mode):
     """Warp-instructions per candidate (smsp__inst_executed.sum) of the same
     committed capture."""
     import csv
-    path = os.path.join(ROOT, "profiles", f"r01_{mode}_mode_raw.csv")
+    path, graphs = _profile(config, mode)
+    if path is None:
+        return None
     try:
         rows = list(csv.reader(open(path)))
         i = rows[0].index("smsp__inst_executed.sum")
-        return float(rows[2][i].replace(",", "")) / PROFILE_GRAPHS
+        return float(rows[2][i].replace(",", "")) / graphs
     except Exception:
         return None
 
@@ -125,6 +140,11 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            # nvidia-smi takes a moment to start: wait for its first sample so a
+            # short timed region (e.g. 5 syn256 steps) is still covered
+            t0 = time.time()
+            while time.time() - t0 < 5.0 and os.path.getsize(self.path) == 0:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
@@ -587,13 +607,13 @@ def main():
     avg_kernel_ms = sum(kms) / len(kms) if kms else ms_per_step
     achieved = bytes_per_eval * B / (avg_kernel_ms / 1e3) / 1e9
     peak, peak_src = load_peaks()
-    # the committed ncu captures are of the headline workload
-    tpe, tsrc = ncu_traffic_per_eval(args.mode) if args.config == "het42-70b" else (None, None)
+    tpe, tsrc, tgraphs = ncu_traffic_per_eval(args.config, args.mode)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak,
                 "traffic": (tpe * B) if tpe is not None else None,
                 "traffic_unit": "bytes per launch (DRAM read + write)",
-                "traffic_source": f"{tsrc}: ncu --set full of one {PROFILE_GRAPHS}-candidate launch, per candidate x {B}",
+                "traffic_source": (f"{tsrc}: ncu --set full of one {tgraphs}-candidate launch, per candidate x {B}"
+                                   if tsrc else "no committed capture for this config/mode"),
                 "algorithmic_bytes_per_launch": bytes_per_eval * B,
                 "kernel": f"score_kernel<{args.mode}> (fused K1 build + K2 solve, one warp per graph)",
                 "kernel_ms": avg_kernel_ms, "kernel_share_of_step": avg_kernel_ms / ms_per_step,
@@ -679,7 +699,7 @@ def main():
     clocks = clk.summary()
     # the roofline that binds this kernel: warp-instruction issue (4 schedulers
     # per SM, one instruction per clock each) — see DESIGN.md §4
-    ipe = ncu_inst_per_eval(args.mode) if args.config == "het42-70b" else None
+    ipe = ncu_inst_per_eval(args.config, args.mode)
     if ipe and clocks.get("sm_mhz"):
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         issue_peak = sms * 4 * clocks["sm_mhz"] * 1e6

@@ -61,8 +61,9 @@ extern "C" {
  *            (flow_graph.cpp:138-229): values and per-edge flows are
  *            bit-identical to the reference.  Default; used for every
  *            per-edge-flow entry point.
- *   SCORE  — value only (Edmonds-Karp shortest augmenting paths).  Exact on
- *            integer capacities; within rounding (<= 1e-6 relative, asserted
+ *   SCORE  — value only (Edmonds-Karp over a bitset BFS for graphs of at
+ *            most 128 vertices; push-relabel with global relabels above).
+ *            Exact on integer capacities; within rounding (<= 1e-6 relative, asserted
  *            by the tests) on float capacities.  For bulk placement search. */
 #define HELIO_MODE_PARITY 0
 #define HELIO_MODE_SCORE 1
