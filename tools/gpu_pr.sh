@@ -1,6 +1,6 @@
 set -x
-for v in "HELIO_PR_GR=20"; do
-  env $v timeout 300 python tools/profile_score.py --config syn256-120l --walk --count 20000 --repeat 2 2>&1 | tail -1 | sed "s/^/$v /"
-done
+timeout 300 python tools/profile_score.py --config syn256-120l --walk --count 20000 --repeat 2 2>&1 | tail -1
 timeout 300 python tools/profile_score.py --count 200000 --repeat 2 2>&1 | tail -1
+timeout 300 python tools/profile_score.py --count 200000 --repeat 2 --mode parity 2>&1 | tail -1
+timeout 300 python tools/profile_score.py --config syn256-120l --walk --count 20000 --repeat 2 --mode parity 2>&1 | tail -1
 timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu --timeout 600 -x > gpurun_out/pytest_parity.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_parity.log
