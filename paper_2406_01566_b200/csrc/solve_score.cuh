@@ -492,7 +492,7 @@ __device__ double solve_ek_bits_w(const Gs& g, const int n, const int s, const i
       const int x = lane + 32 * i;
       const int dx = dl[i];
       if (x >= n || dx <= 0) continue;
-      int pick = -1, pu = -1, pair_arc = -1;
+      int pick = -1, pu = -1;
       for (int a = g.abeg[x], e = g.abeg[x + 1]; a < e; ++a) {
         const int u = g.to[a];
         const int r = g.rv[a];
@@ -501,16 +501,9 @@ __device__ double solve_ek_bits_w(const Gs& g, const int n, const int s, const i
           pu = u;
           break;
         }
-        if (u == (x ^ 1) && x >= 2) pair_arc = r;
       }
       if (pick < 0) {  // reached through its partner's pair arc at the same level
-        if (pair_arc < 0)
-          for (int a = g.abeg[x], e = g.abeg[x + 1]; a < e; ++a)
-            if (g.to[a] == (x ^ 1)) {
-              pair_arc = g.rv[a];
-              break;
-            }
-        pick = pair_arc;
+        pick = g.rv[g.abeg[x]];  // the builder puts the compute pair in slot 0
         pu = x ^ 1;
       }
       par[x] = (int32_t)(uint16_t)pick | (pu << 16);
