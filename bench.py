@@ -408,7 +408,22 @@ def search_leg(h, clusters, dev):
             out["runs"].append({"seed": method, "mode": mode, "swaps": swaps, "seed_value": float(v0[0]),
                                 "value": value, "moves": moves, "scored": scored, "seconds": dt,
                                 "evals_per_s": scored / dt if dt > 0 else None})
+    # past the local optimum: sampled multi-node search (helio_gpu_sampled_search)
+    # from the petals seed's local optimum, then one more local search
     eng.mode = "score"
+    placement, _ = h.heuristic_placement(c, "petals")
+    seed = h.placement_rows(c, [{k: tuple(v) for k, v in placement.items()}])[0]
+    lv, lrow, _, _ = eng.local_search(seed)
+    rounds, batch, changes = 10, 1 << 20, 2
+    t0 = time.perf_counter()
+    sv, srow, imp, sscored = eng.sampled_search(lrow, True, rounds, batch, changes, 7)
+    dt = time.perf_counter() - t0
+    fv, _, fmoves, _ = eng.local_search(srow)
+    out["sampled"] = {"from": "petals local optimum", "mode": "score", "rounds": rounds, "batch": batch,
+                      "max_changes": changes, "start_value": lv, "value": sv, "improving_rounds": imp,
+                      "scored": sscored, "seconds": dt, "evals_per_s": sscored / dt if dt > 0 else None,
+                      "local_search_after": fv,
+                      "note": "mutants with overlapping intervals are denser graphs (some take the big-slot path)"}
     return out
 
 

@@ -225,6 +225,20 @@ int helio_gpu_local_search(helio_gpu_ctx* ctx, const int16_t* h_seed, int allow_
                            int32_t neighbourhood, double* h_value, int16_t* h_row, int32_t* h_moves,
                            int64_t* h_scored);
 
+/* Sampled multi-node search from a seed placement (SURVEY.md §8(f) rank 1,
+ * past the local optima of helio_gpu_local_search).  Each of `iterations`
+ * rounds scores, in the context's mode, `batch` mutants of the incumbent —
+ * each re-assigns 1..max_changes random nodes (keep start / keep end / start
+ * where another node ends / idle / uniform; lengths within k_i, so every
+ * mutant validates) — and moves to the first strict best when it beats the
+ * incumbent (enumerate.hpp:59).  Draws are counter-based over (rng_seed,
+ * round, mutant): the result is deterministic.  The seed must validate.
+ * Outputs the final value and int16 [N][2] row, the number of improving
+ * rounds and the placements scored (seed included). */
+int helio_gpu_sampled_search(helio_gpu_ctx* ctx, const int16_t* h_seed, int allow_partial, int32_t iterations,
+                             int64_t batch, int32_t max_changes, uint64_t rng_seed, double* h_value,
+                             int16_t* h_row, int32_t* h_improvements, int64_t* h_scored);
+
 /* Link-walking covering chains (gen.h hg_candidate_walk) for sparse
  * topologies, device and host (identical output). */
 int helio_gpu_generate_walk(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B,

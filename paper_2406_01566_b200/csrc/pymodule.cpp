@@ -943,5 +943,30 @@ PYBIND11_MODULE(_helio, m) {
           py::arg("seed"), py::arg("allow_partial") = true, py::arg("max_moves") = -1, py::arg("swaps") = true,
           "Best-improvement local search over single-node moves (+ interval swaps): "
           "(value, row, moves, placements scored).")
+      .def(
+          "sampled_search",
+          [](PyEngine& e, py::array_t<int16_t, py::array::c_style | py::array::forcecast> seed, bool allow_partial,
+             int32_t iterations, int64_t batch, int32_t max_changes, uint64_t rng_seed) {
+            const int N = e.eng->num_nodes();
+            if (seed.ndim() != 2 || seed.shape(0) != N || seed.shape(1) != 2)
+              throw py::value_error("seed must be int16 [num_nodes, 2]");
+            py::array_t<int16_t> row({(py::ssize_t)N, (py::ssize_t)2});
+            double value = 0;
+            int32_t improvements = 0;
+            int64_t scored = 0;
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = helio_gpu_sampled_search(e.eng->ctx(), seed.data(), allow_partial ? 1 : 0, iterations, batch,
+                                            max_changes, rng_seed, &value, row.mutable_data(), &improvements,
+                                            &scored);
+            }
+            e.eng->check(rc, "helio_gpu_sampled_search");
+            return py::make_tuple(value, row, improvements, scored);
+          },
+          py::arg("seed"), py::arg("allow_partial") = true, py::arg("iterations") = 20,
+          py::arg("batch") = 1 << 20, py::arg("max_changes") = 3, py::arg("rng_seed") = 1,
+          "Sampled multi-node search: `iterations` rounds of `batch` mutants (1..max_changes nodes "
+          "re-assigned) of the incumbent, first strict best kept: (value, row, improving rounds, scored).")
       .def("sync", [](PyEngine& e) { e.eng->check(helio_gpu_sync(e.eng->ctx()), "helio_gpu_sync"); });
 }

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "gen.h"
 
 using namespace helio_engine;
 
@@ -345,6 +346,155 @@ extern "C" int helio_gpu_local_search(helio_gpu_ctx* ctx, const int16_t* h_seed,
     h_row[2 * i + 1] = (int16_t)((uint32_t)cur[i] >> 16);
   }
   if (h_moves) *h_moves = moves;
+  if (h_scored) *h_scored = scored;
+  return HELIO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Sampled multi-node search (beyond the 1-move local
+// search): every iteration scores `batch` mutants of the incumbent, each
+// changing 1..max_changes random nodes, and moves to the first strict best if
+// it beats the incumbent.  Local optima of the single-node neighbourhood are
+// usually one 2-3-node change away from something better; the full 2-move
+// neighbourhood of het42 has ~3e8 members, so it is sampled — at ~60M
+// evals/s a 1M-mutant iteration costs ~17 ms.  A change re-assigns one node
+// (any node with k_i >= 1) to an interval built from the incumbent:
+//   25% keep its start, new length; 25% keep its end, new length;
+//   30% start where a random other node ends (wrapping at L) — extend a chain;
+//   10% idle; 10% uniform interval.
+// Lengths are U[1, k_i] truncated to [0, L], so every mutant validates.
+// Counter-based draws (gen.h) over (seed, iteration, mutant): deterministic.
+namespace {
+
+__global__ void copy_rows(const int32_t* __restrict__ cur, int N, int64_t B, int32_t* __restrict__ rows) {
+  const int64_t words = B * N;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < words; q += (int64_t)gridDim.x * blockDim.x)
+    rows[q] = __ldg(cur + (q % N));
+}
+
+__global__ void mutate_rows(const int32_t* __restrict__ cur, const int32_t* __restrict__ kmax, int N, int L,
+                            uint64_t seed, int64_t B, int max_changes, int32_t* __restrict__ rows) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = hg_key(seed, (uint64_t)b);
+    const int c = 1 + (int)hg_uniform(hg_draw(key, 0), (uint32_t)max_changes);
+    for (int j = 0; j < c; ++j) {
+      const uint64_t d0 = hg_draw(key, 1 + 4 * j), d1 = hg_draw(key, 2 + 4 * j), d2 = hg_draw(key, 3 + 4 * j),
+                     d3 = hg_draw(key, 4 + 4 * j);
+      const int node = (int)hg_uniform(d0, (uint32_t)N);
+      const int k = __ldg(kmax + node);
+      if (k < 1) continue;
+      const int32_t w = __ldg(cur + node);
+      int s = (int16_t)(w & 0xffff), e = (int16_t)(w >> 16);
+      const bool used = e > s;
+      const int len = 1 + (int)hg_uniform(d2, (uint32_t)k);
+      const uint32_t op = hg_uniform(d1, 100);
+      if (op < 25) {  // keep start
+        if (!used) s = (int)hg_uniform(d3, (uint32_t)L);
+        e = min(s + len, L);
+      } else if (op < 50) {  // keep end
+        if (!used) e = 1 + (int)hg_uniform(d3, (uint32_t)L);
+        s = max(e - len, 0);
+      } else if (op < 80) {  // attach after another node's end
+        const int32_t a = __ldg(cur + hg_uniform(d3, (uint32_t)N));
+        const int as = (int16_t)(a & 0xffff), ae = (int16_t)(a >> 16);
+        s = (ae > as && ae < L) ? ae : 0;
+        e = min(s + len, L);
+      } else if (op < 90) {  // idle
+        s = e = 0;
+      } else {  // uniform
+        const int ln = min(len, L);
+        s = (int)hg_uniform(d3, (uint32_t)(L - ln + 1));
+        e = s + ln;
+      }
+      rows[b * N + node] = (int32_t)(uint16_t)s | (int32_t)((uint32_t)(uint16_t)e << 16);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int helio_gpu_sampled_search(helio_gpu_ctx* ctx, const int16_t* h_seed, int allow_partial,
+                                        int32_t iterations, int64_t batch, int32_t max_changes, uint64_t rng_seed,
+                                        double* h_value, int16_t* h_row, int32_t* h_improvements,
+                                        int64_t* h_scored) {
+  if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
+  if (!ctx->has_cluster) return fail(ctx, HELIO_ERR_NO_CLUSTER, "no cluster set");
+  if (!h_seed || !h_value || !h_row) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  if (iterations < 0 || batch < 1 || max_changes < 1)
+    return fail(ctx, HELIO_ERR_INVALID, "need iterations >= 0, batch >= 1, max_changes >= 1");
+  const int N = ctx->N, L = ctx->L;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  int rc = HELIO_OK;
+  int32_t *d_cur = nullptr, *d_rows = nullptr, *d_st = nullptr, *d_kmax = nullptr;
+  double *d_val = nullptr, *d_best = nullptr;
+  int64_t* d_bidx = nullptr;
+  auto A = [&](void** p, size_t bytes) {
+    if (!rc && cudaMalloc(p, std::max<size_t>(bytes, 8)) != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "sampled search alloc");
+  };
+  A((void**)&d_cur, 4 * N);
+  A((void**)&d_kmax, 4 * N);
+  A((void**)&d_rows, 4 * (size_t)N * batch);
+  A((void**)&d_val, 8 * batch);
+  A((void**)&d_st, 4 * batch);
+  A((void**)&d_best, 8);
+  A((void**)&d_bidx, 8);
+  auto sync_read = [&](void* dst, const void* src, size_t bytes) {
+    if (!rc && (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess))
+      rc = fail(ctx, HELIO_ERR_CUDA, std::string("sampled search readback: ") + cudaGetErrorString(cudaGetLastError()));
+  };
+  double value = 0.0;
+  int32_t improvements = 0;
+  int64_t scored = 0;
+  if (!rc) {
+    std::vector<int32_t> cur(N);
+    for (int i = 0; i < N; ++i)
+      cur[i] = (int32_t)(uint16_t)h_seed[2 * i] | (int32_t)((uint32_t)(uint16_t)h_seed[2 * i + 1] << 16);
+    cudaMemcpyAsync(d_cur, cur.data(), 4 * N, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_kmax, ctx->h_kmax.data(), 4 * N, cudaMemcpyHostToDevice, st);
+    rc = helio_gpu_score(ctx, reinterpret_cast<const int16_t*>(d_cur), 1, allow_partial, d_val, d_st, st);
+    int32_t s0 = 0;
+    sync_read(&value, d_val, 8);
+    sync_read(&s0, d_st, 4);
+    scored = 1;
+    if (!rc && s0 != 0) rc = fail(ctx, HELIO_ERR_INVALID, "seed placement fails validation (status " + std::to_string(s0) + ")");
+  }
+  const int grid_w = (int)std::min<int64_t>(((int64_t)N * batch + 255) / 256, 16 * ctx->sm_count);
+  const int grid_b = (int)std::min<int64_t>((batch + 255) / 256, 16 * ctx->sm_count);
+  for (int32_t it = 0; !rc && it < iterations; ++it) {
+    copy_rows<<<grid_w, 256, 0, st>>>(d_cur, N, batch, d_rows);
+    mutate_rows<<<grid_b, 256, 0, st>>>(d_cur, d_kmax, N, L, hg_key(rng_seed, (uint64_t)it), batch, max_changes,
+                                        d_rows);
+    ctx->launches += 2;
+    rc = helio_gpu_score(ctx, reinterpret_cast<const int16_t*>(d_rows), batch, allow_partial, d_val, d_st, st);
+    if (rc) break;
+    rc = helio_gpu_argmax(ctx, d_val, d_st, batch, 0, d_best, d_bidx, st);
+    if (rc) break;
+    double best = 0.0;
+    int64_t bi = -1;
+    sync_read(&best, d_best, 8);
+    sync_read(&bi, d_bidx, 8);
+    scored += batch;
+    if (!rc && bi >= 0 && best > value) {
+      value = best;
+      ++improvements;
+      if (cudaMemcpyAsync(d_cur, d_rows + bi * N, 4 * N, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        rc = fail(ctx, HELIO_ERR_CUDA, "sampled search update");
+    }
+  }
+  std::vector<int32_t> out(N);
+  sync_read(out.data(), d_cur, 4 * N);
+  cudaFree(d_cur); cudaFree(d_kmax); cudaFree(d_rows); cudaFree(d_val); cudaFree(d_st); cudaFree(d_best);
+  cudaFree(d_bidx);
+  if (rc) return rc;
+  *h_value = value;
+  for (int i = 0; i < N; ++i) {
+    h_row[2 * i] = (int16_t)(out[i] & 0xffff);
+    h_row[2 * i + 1] = (int16_t)((uint32_t)out[i] >> 16);
+  }
+  if (h_improvements) *h_improvements = improvements;
   if (h_scored) *h_scored = scored;
   return HELIO_OK;
 }

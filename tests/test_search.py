@@ -170,3 +170,40 @@ def test_local_search_rejects_invalid_seed():
         e.local_search(bad)
     with pytest.raises(h.ValidationError):
         h.local_search(c, {d["nodes"][0]["id"]: (0, 24)})
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_sampled_search_escapes_the_local_optimum():
+    """helio_gpu_sampled_search: multi-node mutants of the incumbent, first
+    strict best kept.  From geo24's swarm seed the single-node local optimum
+    (866.7) is left behind; the result is reproducible, never below its seed,
+    and its PARITY value is the reference's value of the returned row."""
+    d = clusters.CONFIGS["geo24"]()
+    c = _cluster(d)
+    e = h.Engine(c)  # PARITY
+    seed = _row(c, h.heuristic_placement(c, "swarm")[0])
+    lv, lrow, _, _ = e.local_search(seed)
+    v1, r1, imp, scored = e.sampled_search(lrow, True, 8, 200_000, 3, 7)
+    v2, r2, imp2, scored2 = e.sampled_search(lrow, True, 8, 200_000, 3, 7)
+    assert v1 == v2 and np.array_equal(r1, r2) and (imp, scored) == (imp2, scored2)
+    assert scored == 1 + 8 * 200_000
+    assert v1 > lv and imp >= 1
+    rc, score = _ref_scorer(d)
+    ref_v, ref_st = score(np.ascontiguousarray(r1[None]))
+    assert ref_st[0] == 0 and ref_v[0] == v1
+    # zero rounds return the seed untouched
+    v0, r0, imp0, sc0 = e.sampled_search(lrow, True, 0, 1000, 3, 7)
+    assert v0 == lv and np.array_equal(r0, lrow) and imp0 == 0 and sc0 == 1
+
+
+@pytest.mark.gpu
+def test_sampled_search_score_mode_integer_capacities_equal_parity():
+    d = clusters.CONFIGS["het42-70b"]("int")
+    c = _cluster(d)
+    e = h.Engine(c)
+    seed = _row(c, h.heuristic_placement(c, "petals")[0])
+    par = e.sampled_search(seed, True, 3, 100_000, 2, 11)
+    e.mode = "score"
+    sco = e.sampled_search(seed, True, 3, 100_000, 2, 11)
+    assert par[0] == sco[0] and np.array_equal(par[1], sco[1]) and par[2:] == sco[2:]
