@@ -76,6 +76,11 @@ struct helio_gpu_ctx {
   int small_warps = 4, small_blocks[2] = {0, 0}, big_blocks[2] = {0, 0};
   // per-mode slots for score_kernel<MODE> (SCORE uses a compact layout when N > 64)
   helio_engine::Layout slot_small[2]{}, slot_big[2]{};
+  // middle tier between the small and the big slot (dense placements, e.g. the
+  // heuristics' replicated stages, which overflow the small slot)
+  helio_engine::Layout slot_mid[2]{};
+  int mid_warps[2] = {1, 1}, mid_blocks[2] = {0, 0};
+  bool slot_mid_ok[2] = {false, false};
   int slot_warps[2] = {4, 4};
   bool slot_big_ok[2] = {false, false};
   int mode = 0;  // HELIO_MODE_PARITY
@@ -86,9 +91,10 @@ struct helio_gpu_ctx {
   // to release the SMs, never holds up the following H2D), plus kApiSet for
   // the device-pointer entries and search.cu
   static constexpr int kPipeSets = 3, kApiSet = 3, kSets = 4;
-  unsigned long long* d_work = nullptr;  // [16]: set k uses [2k, 2k+1], split.cu [8]/[9]
-  unsigned int* d_ovf_count = nullptr;   // [kSets]
-  int64_t* d_ovf[kSets] = {nullptr, nullptr, nullptr, nullptr};
+  unsigned long long* d_work = nullptr;  // [32]: raw [0], split.cu [8]/[9], set k [16+3k, 16+3k+2]
+  unsigned int* d_ovf_count = nullptr;   // [2 * kSets]: small -> mid, mid -> big
+  int64_t* d_ovf[kSets] = {nullptr, nullptr, nullptr, nullptr};   // small-slot overflows
+  int64_t* d_ovf2[kSets] = {nullptr, nullptr, nullptr, nullptr};  // mid-slot overflows
   int64_t ovf_cap[kSets] = {0, 0, 0, 0};
   double* d_pv = nullptr;      // argmax partials: kSets + 1 scratch rows of 4096
   long long* d_pi = nullptr;

@@ -59,24 +59,26 @@ struct FlowOut {
   int max_e;
 };
 
-// Persistent: every warp loops fetching candidate indices.  big == 0: all B
-// candidates, overflowing graphs appended to ovf; big == 1: the ovf list.
+// Persistent: every warp loops fetching candidate indices.  tier 0: all B
+// candidates, graphs whose arcs exceed the slot appended to ovf; tier 1: the
+// ovf list, overflows appended to ovf2 when it is given (middle slot) or
+// reported HELIO_CAND_TOO_LARGE (big slot); tier 2: the ovf2 list (big slot).
 template <int MODE>
 __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restrict__ pl, int64_t B,
                              int partial, double* __restrict__ values, int32_t* __restrict__ status,
-                             unsigned long long* work, int64_t* ovf, unsigned int* ovf_count,
-                             int big, FlowOut fo) {
+                             unsigned long long* work, int64_t* ovf, int64_t* ovf2, unsigned int* ovf_count,
+                             int tier, FlowOut fo) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const Gs g = slot_view(smem + wib * lay.bytes, lay);
-  const int64_t total = big ? (int64_t)(*ovf_count) : B;
+  const int64_t total = tier ? (int64_t)ovf_count[tier - 1] : B;
   for (;;) {
     unsigned long long w = 0;
     if (lane == 0) w = atomicAdd(work, 1ull);
     w = __shfl_sync(FULL, w, 0);
     if ((int64_t)w >= total) break;
-    const int64_t b = big ? ovf[w] : (int64_t)w;
+    const int64_t b = tier == 0 ? (int64_t)w : (tier == 1 ? ovf : ovf2)[w];
     int V = 0, E = 0;
     int st = MODE == HELIO_MODE_SCORE
                  ? (cd.out_mask ? build_graph_score_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
@@ -85,8 +87,8 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
                         ? build_graph_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
                         : build_graph(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E));
     if (st == ST_OVERFLOW) {
-      if (!big) {
-        if (lane == 0) ovf[atomicAdd(ovf_count, 1u)] = b;
+      if (tier == 0 || (tier == 1 && ovf2)) {
+        if (lane == 0) (tier == 0 ? ovf : ovf2)[atomicAdd(ovf_count + tier, 1u)] = b;
         continue;
       }
       st = HELIO_CAND_TOO_LARGE;
@@ -107,7 +109,7 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     if (lane == 0) {
       values[b] = value;
       status[b] = st;
-      if (fo.nv) {
+      if (MODE == HELIO_MODE_PARITY && fo.nv) {  // SCORE calls never carry FlowOut
         fo.nv[b] = V;
         fo.ne[b] = E;
       }
@@ -317,12 +319,10 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   // warps resident per SM (228 KB, 1 KB reserved per CTA; larger CTAs on
   // ties), and the big one for the structural maximum (every declared link
   // valid) or the largest arc count that still fits one CTA.
-  auto plan = [&](bool compact, int a_small, Layout& small, Layout& big, int& warps_out, bool& big_ok) {
-    auto mk = [&](int a) { return compact ? make_layout_score_general(V, a, N) : make_layout(V, a, N, 0); };
-    small = mk(a_small);
+  auto best_warps = [&](const Layout& l) {
     int warps = 1, best_res = -1;
     for (int w : {4, 2, 1}) {
-      const size_t cta = (size_t)small.bytes * w;
+      const size_t cta = (size_t)l.bytes * w;
       if (cta > max_smem) continue;
       const int res = w * (int)std::min<size_t>(32, (228 * 1024) / (cta + 1024));
       if (res > best_res) {
@@ -330,7 +330,12 @@ int configure_layouts(helio_gpu_ctx* ctx) {
         warps = w;
       }
     }
-    warps_out = warps;
+    return warps;
+  };
+  auto plan = [&](bool compact, int a_small, Layout& small, Layout& big, int& warps_out, bool& big_ok) {
+    auto mk = [&](int a) { return compact ? make_layout_score_general(V, a, N) : make_layout(V, a, N, 0); };
+    small = mk(a_small);
+    warps_out = best_warps(small);
     int a_big = a_struct < 2 ? 2 : a_struct;
     if (a_big > 32766) a_big = 32766;
     big = mk(a_big);
@@ -357,6 +362,20 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   // layout (residual rows in the VState bytes); larger clusters the compact one
   plan(N > 64, small_arcs(N > 64 ? 32 : 16), ctx->slot_small[HELIO_MODE_SCORE], ctx->slot_big[HELIO_MODE_SCORE],
        ctx->slot_warps[HELIO_MODE_SCORE], ctx->slot_big_ok[HELIO_MODE_SCORE]);
+  // middle tier: twice the small slot's arcs (placements with replicated
+  // stages — the heuristics' petals/swarm layouts carry ~5N edges on het42),
+  // with its own warps per CTA; skipped when it would not beat the big slot
+  for (int m = 0; m < 2; ++m) {
+    const bool compact = m == HELIO_MODE_SCORE && N > 64;
+    const int a_small = ctx->slot_small[m].A;
+    const int a_mid = std::min(2 * a_small, ctx->slot_big[m].A);
+    ctx->slot_mid_ok[m] = false;
+    if (ctx->slot_big_ok[m] && a_mid > a_small && a_mid < ctx->slot_big[m].A) {
+      ctx->slot_mid[m] = compact ? make_layout_score_general(V, a_mid, N) : make_layout(V, a_mid, N, 0);
+      ctx->mid_warps[m] = best_warps(ctx->slot_mid[m]);
+      ctx->slot_mid_ok[m] = (size_t)ctx->slot_mid[m].bytes * ctx->mid_warps[m] <= max_smem;
+    }
+  }
   // occupancy of both instantiations (PARITY / SCORE)
   void* fns[2] = {reinterpret_cast<void*>(score_kernel<HELIO_MODE_PARITY>),
                   reinterpret_cast<void*>(score_kernel<HELIO_MODE_SCORE>)};
@@ -376,6 +395,13 @@ int configure_layouts(helio_gpu_ctx* ctx) {
       if (per_sm_big < 1) per_sm_big = 1;
     }
     ctx->big_blocks[m] = per_sm_big * ctx->sm_count;
+    int per_sm_mid = 1;
+    if (ctx->slot_mid_ok[m]) {
+      const int wm = ctx->mid_warps[m];
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_mid, fns[m], 32 * wm, ctx->slot_mid[m].bytes * wm));
+      if (per_sm_mid < 1) per_sm_mid = 1;
+    }
+    ctx->mid_blocks[m] = per_sm_mid * ctx->sm_count;
   }
   return HELIO_OK;
 }
@@ -383,8 +409,12 @@ int configure_layouts(helio_gpu_ctx* ctx) {
 int ensure_ovf(helio_gpu_ctx* ctx, int set, int64_t B) {
   if (ctx->ovf_cap[set] >= B) return HELIO_OK;
   if (ctx->d_ovf[set]) cudaFree(ctx->d_ovf[set]);
+  if (ctx->d_ovf2[set]) cudaFree(ctx->d_ovf2[set]);
+  ctx->d_ovf[set] = ctx->d_ovf2[set] = nullptr;
+  ctx->ovf_cap[set] = 0;
   int64_t cap = std::max<int64_t>(B, 1 << 16);
   CK(cudaMalloc(&ctx->d_ovf[set], sizeof(int64_t) * cap));
+  CK(cudaMalloc(&ctx->d_ovf2[set], sizeof(int64_t) * cap));
   ctx->ovf_cap[set] = cap;
   return HELIO_OK;
 }
@@ -392,19 +422,32 @@ int ensure_ovf(helio_gpu_ctx* ctx, int set, int64_t B) {
 template <int MODE>
 void launch_score_mode(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, int partial, double* d_val,
                        int32_t* d_st, cudaStream_t st, FlowOut fo, bool timed) {
-  unsigned long long* work = ctx->d_work + 2 * set;
-  unsigned int* oc = ctx->d_ovf_count + set;
+  unsigned long long* work = ctx->d_work + 16 + 3 * set;
+  unsigned int* oc = ctx->d_ovf_count + 2 * set;
+  int64_t* l1 = ctx->d_ovf[set];
+  int64_t* l2 = ctx->d_ovf2[set];
   if (timed) cudaEventRecord(ctx->ev0, st);
   const Layout& sl = ctx->slot_small[MODE];
   const int warps = ctx->slot_warps[MODE];
   const int grid = (int)std::min<int64_t>(ctx->small_blocks[MODE], (B + warps - 1) / warps);
   score_kernel<MODE><<<grid, 32 * warps, sl.bytes * warps, st>>>(ctx->cd, sl, d_pl, B, partial, d_val, d_st, work,
-                                                                 ctx->d_ovf[set], oc, 0, fo);
+                                                                 l1, l2, oc, 0, fo);
   if (timed) cudaEventRecord(ctx->ev1, st);
-  // graphs that overflowed the small slot: same kernel, one warp per CTA, big slot
+  // graphs that overflowed the small slot: the same kernel with the middle
+  // slot, then whatever overflows that with the big slot (one warp per CTA)
   const Layout& bl = ctx->slot_big_ok[MODE] ? ctx->slot_big[MODE] : sl;
-  score_kernel<MODE><<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
-                                                                   work + 1, ctx->d_ovf[set], oc, 1, fo);
+  if (ctx->slot_mid_ok[MODE]) {
+    const Layout& ml = ctx->slot_mid[MODE];
+    const int wm = ctx->mid_warps[MODE];
+    score_kernel<MODE><<<ctx->mid_blocks[MODE], 32 * wm, ml.bytes * wm, st>>>(
+        ctx->cd, ml, d_pl, B, partial, d_val, d_st, work + 1, l1, l2, oc, 1, fo);
+    score_kernel<MODE><<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
+                                                                     work + 2, l1, l2, oc, 2, fo);
+    ctx->launches += 1;
+  } else {
+    score_kernel<MODE><<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
+                                                                     work + 2, l1, nullptr, oc, 1, fo);
+  }
 }
 
 int launch_score(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, int partial,
@@ -412,9 +455,9 @@ int launch_score(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, in
   if (B <= 0) return HELIO_OK;
   int rc = ensure_ovf(ctx, set, B);
   if (rc) return rc;
-  CK(cudaMemsetAsync(ctx->d_work + 2 * set, 0, 2 * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(ctx->d_ovf_count + set, 0, sizeof(unsigned int), st));
-  if (mode == HELIO_MODE_SCORE && fo.edges == nullptr)
+  CK(cudaMemsetAsync(ctx->d_work + 16 + 3 * set, 0, 3 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(ctx->d_ovf_count + 2 * set, 0, 2 * sizeof(unsigned int), st));
+  if (mode == HELIO_MODE_SCORE && fo.edges == nullptr && fo.nv == nullptr)
     launch_score_mode<HELIO_MODE_SCORE>(ctx, set, d_pl, B, partial, d_val, d_st, st, fo, timed);
   else
     launch_score_mode<HELIO_MODE_PARITY>(ctx, set, d_pl, B, partial, d_val, d_st, st, fo, timed);
@@ -493,8 +536,8 @@ int helio_gpu_create(int device, helio_gpu_ctx** out) {
       cudaStreamCreateWithFlags(&ctx->pipe[2], cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
-      cudaMalloc(&ctx->d_work, 16 * sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMalloc(&ctx->d_ovf_count, helio_gpu_ctx::kSets * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_work, 32 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_ovf_count, 2 * helio_gpu_ctx::kSets * sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc(&ctx->d_pv, (helio_gpu_ctx::kSets + 1) * 4096 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&ctx->d_pi, (helio_gpu_ctx::kSets + 1) * 4096 * sizeof(long long)) != cudaSuccess ||
       cudaMalloc(&ctx->d_best, 2 * 4096 * sizeof(double)) != cudaSuccess ||
@@ -522,7 +565,10 @@ void helio_gpu_destroy(helio_gpu_ctx* ctx) {
     cudaFreeHost(ctx->h_val_pin[i]);
     cudaFreeHost(ctx->h_st_pin[i]);
   }
-  for (int i = 0; i < helio_gpu_ctx::kSets; ++i) cudaFree(ctx->d_ovf[i]);
+  for (int i = 0; i < helio_gpu_ctx::kSets; ++i) {
+    cudaFree(ctx->d_ovf[i]);
+    cudaFree(ctx->d_ovf2[i]);
+  }
   if (ctx->copy) {
     cudaStreamSynchronize(ctx->copy);
     cudaStreamDestroy(ctx->copy);

@@ -451,3 +451,51 @@ def test_push_relabel_solver_on_deep_sparse_graphs():
             assert np.array_equal(bits(vk), bits(v1))
         else:
             assert np.all(np.abs(vk - v1) <= SCORE_REL_TOL * np.maximum(1.0, np.abs(v1)))
+
+
+def test_dense_placements_take_the_middle_and_big_slots():
+    """Placements with replicated stages (the heuristics' petals layout has
+    ~5N edges on het42) overflow the small slot (4N edges) into the middle
+    tier (8N); fully replicated stages go on to the big slot.  Both tiers must
+    match the oracle like the small one."""
+    from _support import RefCluster, ref_available, ref_heuristic
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    d = clusters.CONFIGS["het42-70b"]("float")
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    o = Oracle(d)
+    N, L = len(d["nodes"]), c.num_layers
+    kmax = list(e.kmax)
+    petals, _ = ref_heuristic(RefCluster(d), "petals")
+    rng = np.random.default_rng(5)
+    rows = [petals]
+    for _ in range(600):  # 1-2 node re-assignments of the petals row
+        r = petals.copy()
+        for _ in range(int(rng.integers(1, 3))):
+            k = int(rng.integers(N))
+            ln = 1 + int(rng.integers(kmax[k]))
+            s = int(rng.integers(0, L - ln + 1))
+            r[k] = (s, s + ln)
+        rows.append(r)
+    for groups in (3, 4, 6):  # every node of a stage on the same 4-layer interval
+        r = np.zeros((N, 2), np.int16)
+        for k in range(N):
+            g = k % groups
+            r[k] = (4 * g, 4 * g + 4)
+        rows.append(r)
+    rows = np.stack(rows).astype(np.int16)
+    edges = []
+    for r in rows:
+        st, nv, E, val = o.graph(r, True)
+        edges.append(len(E["u"]) if st == 0 else 0)
+    edges = np.array(edges)
+    assert (edges > 4 * N).sum() > 100 and (edges > 8 * N).sum() >= 2, "must exercise both tiers"
+    want_v, want_s = o.score(rows, True)
+    v, s = e.score(rows, True)
+    assert np.array_equal(s, want_s) and np.array_equal(bits(v), bits(want_v))
+    e.mode = "score"
+    vs_, ss_ = e.score(rows, True)
+    e.mode = "parity"
+    assert np.array_equal(ss_, want_s)
+    assert np.all(np.abs(vs_ - want_v) <= SCORE_REL_TOL * np.maximum(1.0, np.abs(want_v)))
