@@ -712,6 +712,11 @@ def main():
             r["reference_equivalent_seconds"] = r["scored"] / cpu["value"]
 
     clocks = clk.summary()
+    if world > 1:  # every rank sampled its own GPU: report them all (the step is as slow as the slowest)
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, {"sm_mhz": clocks.get("sm_mhz"), "reasons": clocks.get("reasons"),
+                                          "kernel_ms": sum(k for k in kernel_ms if k) / max(1, len(kernel_ms))})
+        clocks["per_rank"] = per_rank
     # the roofline that binds this kernel: warp-instruction issue (4 schedulers
     # per SM, one instruction per clock each) — see DESIGN.md §4
     ipe = ncu_inst_per_eval(args.config, args.mode)
