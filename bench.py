@@ -444,18 +444,21 @@ def run_reference(args):
         rows_fn = lambda f, n: host_rows(h, args.config, kmax, c.num_layers, f, n, eng=gen)  # noqa: E731
     rates = []
     samples = 0
+    step_ms = []
     for step in range(args.warmup + args.steps):
         r, n, dt = reference_rate(d, kmax, c.num_layers, args.ref_step_s, threads, first=step * 10_000_000,
                                   rows_fn=rows_fn)
         if step >= args.warmup:
             rates.append(r)
             samples += n
+            step_ms.append(n / r * 1e3 if r else None)
     value = sorted(rates)[len(rates) // 2]
+    ms = [x for x in step_ms if x]
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
+        "ms_per_step": sum(ms) / len(ms) if ms else None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_of(args.config), "parallelism": "host threads",
                    "candidates_per_step": samples // max(1, args.steps)},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
