@@ -12,12 +12,14 @@
 //   score_kernel<MODE>  placement rows -> graph -> max-flow value, one warp per
 //                       graph, persistent CTAs pulling work from an atomic
 //                       counter; graphs whose arcs exceed the small slot are
-//                       queued and finished by the same kernel launched with one
-//                       warp per CTA and a large slot.
+//                       queued for the same kernel with a middle slot (twice
+//                       the arcs), and what overflows that for one warp per CTA
+//                       with a slot for every declared link.
 //   raw_kernel          max_flow on caller-supplied raw graphs (AC1 style).
 //   argmax_*            (max value, min index) reduction (enumerate.hpp:59).
 //   gen_kernel / gen_walk_kernel   counter-based candidate generators (gen.h).
-// route.cu holds K3 (IWRR routing), search.cu the exhaustive search.
+// route.cu holds K3 (IWRR routing), search.cu the exhaustive, local and
+// sampled placement searches, split.cu the split K1 -> HBM -> K2 pipeline.
 //
 // Everything is compiled with -fmad=false; the only FP operations on the path
 // are min / + / - / compare on doubles, in the reference's order.
