@@ -349,7 +349,7 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
 // (flow_graph.cpp:121: s_j <= e_i < e_j, resp. e_i == s_j), so each node
 // visits only its ~2-3 actual edges instead of every link of the cluster.
 __device__ int build_graph_score_small(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
-                                       int partial, int lane, int& V, int& E) {
+                                       int partial, int lane, int& V, int& E, double& cut) {
   const int N = cd.N, L = cd.L;
   unsigned long long* cover = reinterpret_cast<unsigned long long*>(g.cap);  // [L] then start[L]; scratch
   unsigned long long* start = cover + L;
@@ -382,6 +382,24 @@ __device__ int build_graph_score_small(const ClusterDev& cd, const Gs& g, const 
     for (int l = s; l < e; ++l) atomicOr(&cover[l], bit);
   }
   __syncwarp();
+  // Layer cut: every source -> sink path crosses the compute edge of some node
+  // covering layer l (intervals chain from 0 to L), so those compute edges are
+  // an s-t cut for each l; cut = the smallest one (summed in node order) bounds
+  // the max-flow value, and a solver that reaches it can stop.
+  {
+    double c = 1.0e300;
+    for (int l = lane; l < L; l += 32) {
+      double sum = 0.0;
+      for (unsigned long long m = cover[l]; m; m &= m - 1) {
+        const int k = __ffsll(m) - 1;
+        sum += __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (g.pe[k] - g.ps[k]) - 1);
+      }
+      c = ref_min(c, sum);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c = ref_min(c, __shfl_xor_sync(FULL, c, o));
+    cut = c;
+  }
   // successor sets (kept in registers; lanes own nodes lane, lane+32)
   unsigned long long T[2] = {0ull, 0ull};
   int* fill = reinterpret_cast<int*>(g.vs);

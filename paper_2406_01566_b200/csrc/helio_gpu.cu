@@ -82,8 +82,9 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     if ((int64_t)w >= total) break;
     const int64_t b = tier == 0 ? (int64_t)w : (tier == 1 ? ovf : ovf2)[w];
     int V = 0, E = 0;
+    double cut = 1.0e300;  // SCORE, N <= 64: the builder's layer cut (an upper bound to stop at)
     int st = MODE == HELIO_MODE_SCORE
-                 ? (cd.out_mask ? build_graph_score_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
+                 ? (cd.out_mask ? build_graph_score_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E, cut)
                                 : build_graph_score(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E))
                  : (cd.less_cout && !fo.edges
                         ? build_graph_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
@@ -97,7 +98,7 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     }
     double value = 0.0;
     if (st == 0 && MODE == HELIO_MODE_SCORE) {
-      value = V <= 128          ? solve_ek_bits(g, V, 0, 1, lane)
+      value = V <= 128          ? solve_ek_bits(g, V, 0, 1, lane, cut)
               : cd.large_solver ? solve_ek_batched(g, V, 0, 1, lane)
                                 : solve_pr(g, V, 0, 1, lane, cd.pr_gr);
     } else if (st == 0) {

@@ -399,7 +399,8 @@ __device__ __forceinline__ unsigned swap_pairs32(unsigned x) {
 // NW = 32-bit words per vertex set = ceil(n / 32): lane l owns vertices l + 32i
 // for i < NW, so every loop below is unrolled to exactly the words in use.
 template <int NW>
-__device__ double solve_ek_bits_w(const Gs& g, const int n, const int s, const int t, const int lane) {
+__device__ double solve_ek_bits_w(const Gs& g, const int n, const int s, const int t, const int lane,
+                                  const double cut) {
   // R in the VState region; BFS level per vertex (int8, n <= 128 levels) in
   // the in-queue bytes; parent arc | parent vertex << 16 per vertex in the
   // count region (4V + 2 bytes); the augmenting path in the queue region.
@@ -538,15 +539,18 @@ __device__ double solve_ek_bits_w(const Gs& g, const int n, const int s, const i
     }
     value += f;
     __syncwarp();
+    if (value >= cut) break;  // a flow as large as a cut is maximum: skip the proving BFS
   }
   return value;
 }
 
-__device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int t, const int lane) {
-  if (n <= 32) return solve_ek_bits_w<1>(g, n, s, t, lane);
-  if (n <= 64) return solve_ek_bits_w<2>(g, n, s, t, lane);
-  if (n <= 96) return solve_ek_bits_w<3>(g, n, s, t, lane);
-  return solve_ek_bits_w<4>(g, n, s, t, lane);
+// cut: the capacity of any s-t cut (the builder's layer cut), or +inf
+__device__ double solve_ek_bits(const Gs& g, const int n, const int s, const int t, const int lane,
+                                const double cut) {
+  if (n <= 32) return solve_ek_bits_w<1>(g, n, s, t, lane, cut);
+  if (n <= 64) return solve_ek_bits_w<2>(g, n, s, t, lane, cut);
+  if (n <= 96) return solve_ek_bits_w<3>(g, n, s, t, lane, cut);
+  return solve_ek_bits_w<4>(g, n, s, t, lane, cut);
 }
 
 }  // namespace
