@@ -309,12 +309,15 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   // resident warps.  PARITY (and the split pipeline's slab) switches below 16
   // declared links per node; SCORE's compact general layout below 32 (both
   // directions and the coordinator's count: syn256's 12 peers give ~25).
+  // The N <= 64 builders keep per-layer cover/start masks in cap[] while they
+  // run, so every slot holds at least 2L + 2 arcs (tiny sparse clusters with
+  // many layers have fewer structural arcs than that).
+  const int a_masks = 2 * ctx->L + 2;
   auto small_arcs = [&](int sparse_below) {
     int a = ctx->Mv < sparse_below * N ? 6 * N : 8 * N;
-    if (a < 2 * ctx->L + 2) a = 2 * ctx->L + 2;  // cover/start masks live in cap[]
     const int a_struct = 2 * (N + ctx->Mv);
     if (a > a_struct) a = a_struct;
-    return a < 2 ? 2 : a;
+    return std::max(a, a_masks);
   };
   const int a_struct = 2 * (N + ctx->Mv);
   const size_t max_smem = 227 * 1024;
@@ -339,7 +342,7 @@ int configure_layouts(helio_gpu_ctx* ctx) {
     auto mk = [&](int a) { return compact ? make_layout_score_general(V, a, N) : make_layout(V, a, N, 0); };
     small = mk(a_small);
     warps_out = best_warps(small);
-    int a_big = a_struct < 2 ? 2 : a_struct;
+    int a_big = std::max(a_struct, a_masks);
     if (a_big > 32766) a_big = 32766;
     big = mk(a_big);
     big_ok = (size_t)big.bytes <= max_smem;

@@ -499,3 +499,28 @@ def test_dense_placements_take_the_middle_and_big_slots():
     e.mode = "parity"
     assert np.array_equal(ss_, want_s)
     assert np.all(np.abs(vs_ - want_v) <= SCORE_REL_TOL * np.maximum(1.0, np.abs(want_v)))
+
+
+@pytest.mark.parametrize("cap", ["float", "int"])
+def test_tiny_sparse_cluster_with_many_layers(cap):
+    """8 nodes, 3 peers each, 60 layers: fewer structural arcs (2(N + links))
+    than the 2L + 2 the N <= 64 builders' cover/start masks need in cap[] —
+    every slot is sized for the masks (found by tools/fuzz_parity.py)."""
+    d = clusters.mesh_cluster(8, model="llama-30b", capacity=cap, peers=3, seed=5)
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    rows = np.concatenate([e.generate_walk_host(11, 0, 500),
+                           h.generate_host(list(e.kmax), c.num_layers, 12, 0, 500, 300000)])
+    o = Oracle(d)
+    for partial in (True, False):
+        want_v, want_s = o.score(rows, partial)
+        v, s = e.score(rows, partial)
+        assert np.array_equal(s, want_s) and np.array_equal(bits(v), bits(want_v))
+        e.mode = "score"
+        vs_, ss_ = e.score(rows, partial)
+        e.mode = "parity"
+        assert np.array_equal(ss_, want_s)
+        if cap == "int":
+            assert np.array_equal(bits(vs_), bits(want_v))
+        else:
+            assert np.all(np.abs(vs_ - want_v) <= SCORE_REL_TOL * np.maximum(1.0, np.abs(want_v)))
