@@ -228,13 +228,16 @@ int helio_gpu_local_search(helio_gpu_ctx* ctx, const int16_t* h_seed, int allow_
 /* Sampled multi-node search from a seed placement (SURVEY.md §8(f) rank 1,
  * past the local optima of helio_gpu_local_search).  Each of `iterations`
  * rounds scores, in the context's mode, `batch` mutants of the incumbent —
- * each re-assigns 1..max_changes random nodes (keep start / keep end / start
- * where another node ends / idle / uniform; lengths within k_i, so every
- * mutant validates) — and moves to the first strict best when it beats the
- * incumbent (enumerate.hpp:59).  Draws are counter-based over (rng_seed,
- * round, mutant): the result is deterministic.  The seed must validate.
- * Outputs the final value and int16 [N][2] row, the number of improving
- * rounds and the placements scored (seed included). */
+ * each re-assigns 1..max_changes random nodes (keep start / keep end / shift
+ * the stage boundary shared with a chain successor / start where another node
+ * ends / idle / uniform; lengths within k_i, so every mutant validates) — and
+ * moves to the round's first maximum (enumerate.hpp:59 order) when it is at
+ * least the incumbent's value: equal values are sideways moves along a
+ * plateau.  The best placement seen (first strict improvement kept) is
+ * returned.  Draws are counter-based over (rng_seed, round, mutant): the
+ * result is deterministic.  The seed must validate.  Outputs the best value
+ * and int16 [N][2] row, the number of rounds that raised the best value and
+ * the placements scored (seed included). */
 int helio_gpu_sampled_search(helio_gpu_ctx* ctx, const int16_t* h_seed, int allow_partial, int32_t iterations,
                              int64_t batch, int32_t max_changes, uint64_t rng_seed, double* h_value,
                              int16_t* h_row, int32_t* h_improvements, int64_t* h_scored);

@@ -967,6 +967,7 @@ PYBIND11_MODULE(_helio, m) {
           py::arg("seed"), py::arg("allow_partial") = true, py::arg("iterations") = 20,
           py::arg("batch") = 1 << 20, py::arg("max_changes") = 3, py::arg("rng_seed") = 1,
           "Sampled multi-node search: `iterations` rounds of `batch` mutants (1..max_changes nodes "
-          "re-assigned) of the incumbent, first strict best kept: (value, row, improving rounds, scored).")
+          "re-assigned) of the incumbent; the round's first maximum is taken when >= the incumbent (plateau "
+          "moves), the best seen is returned: (value, row, rounds that raised it, scored).")
       .def("sync", [](PyEngine& e) { e.eng->check(helio_gpu_sync(e.eng->ctx()), "helio_gpu_sync"); });
 }

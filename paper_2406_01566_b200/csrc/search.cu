@@ -359,8 +359,10 @@ extern "C" int helio_gpu_local_search(helio_gpu_ctx* ctx, const int16_t* h_seed,
 // neighbourhood of het42 has ~3e8 members, so it is sampled — at ~60M
 // evals/s a 1M-mutant iteration costs ~17 ms.  A change re-assigns one node
 // (any node with k_i >= 1) to an interval built from the incumbent:
-//   25% keep its start, new length; 25% keep its end, new length;
-//   30% start where a random other node ends (wrapping at L) — extend a chain;
+//   20% keep its start, new length; 20% keep its end, new length;
+//   15% move the stage boundary it shares with a chain successor (a node
+//       starting where it ends) by 1-4 layers, both nodes re-assigned;
+//   25% start where a random other node ends (wrapping at L) — extend a chain;
 //   10% idle; 10% uniform interval.
 // Lengths are U[1, k_i] truncated to [0, L], so every mutant validates.
 // Counter-based draws (gen.h) over (seed, iteration, mutant): deterministic.
@@ -388,12 +390,33 @@ __global__ void mutate_rows(const int32_t* __restrict__ cur, const int32_t* __re
       const bool used = e > s;
       const int len = 1 + (int)hg_uniform(d2, (uint32_t)k);
       const uint32_t op = hg_uniform(d1, 100);
-      if (op < 25) {  // keep start
+      if (op < 20) {  // keep start
         if (!used) s = (int)hg_uniform(d3, (uint32_t)L);
         e = min(s + len, L);
-      } else if (op < 50) {  // keep end
+      } else if (op < 40) {  // keep end
         if (!used) e = 1 + (int)hg_uniform(d3, (uint32_t)L);
         s = max(e - len, 0);
+      } else if (op < 55) {  // shift the stage boundary to a chain successor
+        if (!used || e >= L) continue;
+        int m = -1;
+        const int off = (int)hg_uniform(d3, (uint32_t)N);
+        for (int q = 0; q < N && m < 0; ++q) {
+          const int cand = off + q < N ? off + q : off + q - N;
+          const int32_t a = __ldg(cur + cand);
+          const int as = (int16_t)(a & 0xffff), ae = (int16_t)(a >> 16);
+          if (cand != node && ae > as && as == e) m = cand;
+        }
+        if (m < 0) continue;
+        const int32_t a = __ldg(cur + m);
+        const int me = (int16_t)(a >> 16), km = __ldg(kmax + m);
+        const int delta = 1 + (int)((d2 >> 1) & 3);
+        int ne = (d2 & 1) ? e + delta : e - delta;
+        ne = max(max(ne, s), me - km);
+        ne = min(min(ne, s + k), me);
+        if (ne == e) continue;
+        rows[b * N + node] = ne > s ? (int32_t)(uint16_t)s | (int32_t)((uint32_t)(uint16_t)ne << 16) : 0;
+        rows[b * N + m] = me > ne ? (int32_t)(uint16_t)ne | (int32_t)((uint32_t)(uint16_t)me << 16) : 0;
+        continue;
       } else if (op < 80) {  // attach after another node's end
         const int32_t a = __ldg(cur + hg_uniform(d3, (uint32_t)N));
         const int as = (int16_t)(a & 0xffff), ae = (int16_t)(a >> 16);
@@ -427,13 +450,14 @@ extern "C" int helio_gpu_sampled_search(helio_gpu_ctx* ctx, const int16_t* h_see
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
   int rc = HELIO_OK;
-  int32_t *d_cur = nullptr, *d_rows = nullptr, *d_st = nullptr, *d_kmax = nullptr;
+  int32_t *d_cur = nullptr, *d_keep = nullptr, *d_rows = nullptr, *d_st = nullptr, *d_kmax = nullptr;
   double *d_val = nullptr, *d_best = nullptr;
   int64_t* d_bidx = nullptr;
   auto A = [&](void** p, size_t bytes) {
     if (!rc && cudaMalloc(p, std::max<size_t>(bytes, 8)) != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "sampled search alloc");
   };
   A((void**)&d_cur, 4 * N);
+  A((void**)&d_keep, 4 * N);
   A((void**)&d_kmax, 4 * N);
   A((void**)&d_rows, 4 * (size_t)N * batch);
   A((void**)&d_val, 8 * batch);
@@ -445,7 +469,7 @@ extern "C" int helio_gpu_sampled_search(helio_gpu_ctx* ctx, const int16_t* h_see
                 cudaStreamSynchronize(st) != cudaSuccess))
       rc = fail(ctx, HELIO_ERR_CUDA, std::string("sampled search readback: ") + cudaGetErrorString(cudaGetLastError()));
   };
-  double value = 0.0;
+  double value = 0.0, best_value = 0.0;
   int32_t improvements = 0;
   int64_t scored = 0;
   if (!rc) {
@@ -453,12 +477,14 @@ extern "C" int helio_gpu_sampled_search(helio_gpu_ctx* ctx, const int16_t* h_see
     for (int i = 0; i < N; ++i)
       cur[i] = (int32_t)(uint16_t)h_seed[2 * i] | (int32_t)((uint32_t)(uint16_t)h_seed[2 * i + 1] << 16);
     cudaMemcpyAsync(d_cur, cur.data(), 4 * N, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_keep, cur.data(), 4 * N, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(d_kmax, ctx->h_kmax.data(), 4 * N, cudaMemcpyHostToDevice, st);
     rc = helio_gpu_score(ctx, reinterpret_cast<const int16_t*>(d_cur), 1, allow_partial, d_val, d_st, st);
     int32_t s0 = 0;
     sync_read(&value, d_val, 8);
     sync_read(&s0, d_st, 4);
     scored = 1;
+    best_value = value;
     if (!rc && s0 != 0) rc = fail(ctx, HELIO_ERR_INVALID, "seed placement fails validation (status " + std::to_string(s0) + ")");
   }
   const int grid_w = (int)std::min<int64_t>(((int64_t)N * batch + 255) / 256, 16 * ctx->sm_count);
@@ -477,15 +503,22 @@ extern "C" int helio_gpu_sampled_search(helio_gpu_ctx* ctx, const int16_t* h_see
     sync_read(&best, d_best, 8);
     sync_read(&bi, d_bidx, 8);
     scored += batch;
-    if (!rc && bi >= 0 && best > value) {
+    if (!rc && bi >= 0 && best >= value) {  // equal values: a sideways move along the plateau
+      if (best > best_value) {
+        best_value = best;
+        ++improvements;
+        if (cudaMemcpyAsync(d_keep, d_rows + bi * N, 4 * N, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+          rc = fail(ctx, HELIO_ERR_CUDA, "sampled search update");
+      }
       value = best;
-      ++improvements;
       if (cudaMemcpyAsync(d_cur, d_rows + bi * N, 4 * N, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         rc = fail(ctx, HELIO_ERR_CUDA, "sampled search update");
     }
   }
   std::vector<int32_t> out(N);
-  sync_read(out.data(), d_cur, 4 * N);
+  sync_read(out.data(), d_keep, 4 * N);
+  value = best_value;
+  cudaFree(d_keep);
   cudaFree(d_cur); cudaFree(d_kmax); cudaFree(d_rows); cudaFree(d_val); cudaFree(d_st); cudaFree(d_best);
   cudaFree(d_bidx);
   if (rc) return rc;
