@@ -40,5 +40,11 @@ struct LocalSearchResult {
 // swaps: also exchange two nodes' intervals (HELIO_LS_SWAPS).
 LocalSearchResult local_search_placement(const ClusterSpec& c, const Placement& seed, bool allow_partial,
                                          int max_moves = -1, bool swaps = true);
+// local search -> sampled multi-node search (helio_gpu_sampled_search, SCORE
+// mode) -> local search again (PARITY: the value is reference-exact);
+// `scored` counts every placement scored.
+LocalSearchResult sampled_search_placement(const ClusterSpec& c, const Placement& seed, bool allow_partial,
+                                           int rounds = 30, long long batch = 1 << 20, int max_changes = 3,
+                                           unsigned long long rng_seed = 7);
 
 }  // namespace helio

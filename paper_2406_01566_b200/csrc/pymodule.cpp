@@ -567,7 +567,7 @@ PYBIND11_MODULE(_helio, m) {
           for (const std::string& w : h.warnings) plan.warnings.push_back(w);
           return plan;
         }
-        if (method == "local") {
+        if (method == "local" || method == "sampled") {
           // seeds as the reference's MILP warm starts (placement.cpp:491-498)
           std::vector<HeuristicResult> seeds{swarm_placement(c), petals_placement(c)};
           if (std::all_of(c.nodes.begin(), c.nodes.end(), [](const NodeSpec& n) { return !n.type.empty(); }))
@@ -580,14 +580,15 @@ PYBIND11_MODULE(_helio, m) {
             LocalSearchResult r;
             {
               py::gil_scoped_release rel;
-              r = local_search_placement(c, h.placement, allow_partial, max_moves);
+              r = method == "local" ? local_search_placement(c, h.placement, allow_partial, max_moves)
+                                    : sampled_search_placement(c, h.placement, allow_partial);
             }
             if (r.value > best_value) {
               best_value = r.value;
               best = r.placement;
             }
           }
-          PlacementPlan plan = plan_from_placement(c, best, allow_partial, "local");
+          PlacementPlan plan = plan_from_placement(c, best, allow_partial, method);
           for (const std::string& w : warnings) plan.warnings.push_back(w);
           return plan;
         }
@@ -596,7 +597,8 @@ PYBIND11_MODULE(_helio, m) {
         throw ValidationError("unknown method '" + method + "'");
       },
       py::arg("cluster"), py::arg("method") = "local", py::arg("allow_partial") = true, py::arg("max_moves") = -1,
-      "Compute a placement plan (method: swarm, petals, sp, or local = device local search from those seeds).");
+      "Compute a placement plan (method: swarm, petals, sp; local = device local search from those seeds; "
+      "sampled = local search, sampled multi-node search, local search again from each seed).");
 
   m.def(
       "heuristic_placement",

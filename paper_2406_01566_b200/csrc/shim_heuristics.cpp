@@ -154,5 +154,31 @@ LocalSearchResult local_search_placement(const ClusterSpec& c, const Placement& 
   return r;
 }
 
+LocalSearchResult sampled_search_placement(const ClusterSpec& c, const Placement& seed, bool allow_partial,
+                                           int rounds, long long batch, int max_changes,
+                                           unsigned long long rng_seed) {
+  LocalSearchResult a = local_search_placement(c, seed, allow_partial);
+  const std::vector<int16_t> row = placement_row(c, a.placement);
+  // a private SCORE-mode context (the cached engine stays PARITY for its
+  // other callers); the closing local search re-scores in PARITY
+  auto eng = std::make_unique<gpu::Engine>(gpu::engine_for(c)->device());
+  eng->set_cluster(c);
+  eng->check(helio_gpu_set_mode(eng->ctx(), HELIO_MODE_SCORE), "helio_gpu_set_mode");
+  std::vector<int16_t> out(row.size(), 0);
+  double value = 0;
+  int32_t improvements = 0;
+  int64_t scored = 0;
+  eng->check(helio_gpu_sampled_search(eng->ctx(), row.data(), allow_partial ? 1 : 0, rounds, batch, max_changes,
+                                      rng_seed, &value, out.data(), &improvements, &scored),
+             "helio_gpu_sampled_search");
+  Placement mid;
+  for (size_t i = 0; i < c.nodes.size(); ++i)
+    if (out[2 * i + 1] > out[2 * i]) mid[c.nodes[i].id] = Interval{out[2 * i], out[2 * i + 1]};
+  LocalSearchResult r = local_search_placement(c, mid, allow_partial);
+  r.moves += a.moves + improvements;
+  r.scored += a.scored + scored;
+  return r;
+}
+
 }  // namespace helio
 

@@ -160,6 +160,20 @@ def test_plan_local_beats_its_seeds():
 
 
 @pytest.mark.gpu
+def test_plan_sampled_at_least_local():
+    """plan(c, "sampled"): each seed's local optimum, then the sampled
+    multi-node search, then local search again; never below plan(c, "local"),
+    deterministic, and its objective is the reference-exact max-flow value."""
+    for name in ("geo24", "geo24-70b"):
+        c = _cluster(clusters.CONFIGS[name]())
+        p = h.plan(c, "sampled")
+        assert p.method == "sampled"
+        assert p.objective >= h.plan(c, "local").objective
+        assert p.objective == h.max_flow_value(c, p.placement)
+        assert h.plan(c, "sampled").objective == p.objective
+
+
+@pytest.mark.gpu
 def test_local_search_rejects_invalid_seed():
     d = clusters.CONFIGS["geo24"]()
     c = _cluster(d)
