@@ -581,7 +581,11 @@ PYBIND11_MODULE(_helio, m) {
             {
               py::gil_scoped_release rel;
               r = method == "local" ? local_search_placement(c, h.placement, allow_partial, max_moves)
-                                    : sampled_search_placement(c, h.placement, allow_partial);
+                                    : c.nodes.size() <= 64
+                                        ? sampled_search_placement(c, h.placement, allow_partial)
+                                        // large sparse clusters score ~40x slower per graph
+                                        // (syn256): more, smaller rounds
+                                        : sampled_search_placement(c, h.placement, allow_partial, 60, 1 << 16);
             }
             if (r.value > best_value) {
               best_value = r.value;

@@ -138,7 +138,17 @@ HeuristicResult separate_pipelines_placement(const ClusterSpec& c) {
 LocalSearchResult local_search_placement(const ClusterSpec& c, const Placement& seed, bool allow_partial,
                                          int max_moves, bool swaps) {
   const std::vector<int16_t> row = placement_row(c, seed);  // validates, reference messages
-  auto eng = gpu::engine_for(c);                             // PARITY-mode engine
+  // N <= 64: the cached PARITY engine.  Larger (sparse) clusters: PARITY's
+  // exact FIFO replay costs ~40x SCORE per graph there (syn256: minutes per
+  // search), so the moves are scored in SCORE mode on a private context and
+  // the final placement's value is re-solved in PARITY below.
+  const bool score_moves = c.nodes.size() > 64;
+  std::shared_ptr<gpu::Engine> eng = gpu::engine_for(c);
+  if (score_moves) {
+    eng = std::make_shared<gpu::Engine>(eng->device());
+    eng->set_cluster(c);
+    eng->check(helio_gpu_set_mode(eng->ctx(), HELIO_MODE_SCORE), "helio_gpu_set_mode");
+  }
   std::vector<int16_t> out(row.size(), 0);
   LocalSearchResult r;
   int32_t moves = 0;
@@ -149,6 +159,7 @@ LocalSearchResult local_search_placement(const ClusterSpec& c, const Placement& 
              "helio_gpu_local_search");
   for (size_t i = 0; i < c.nodes.size(); ++i)
     if (out[2 * i + 1] > out[2 * i]) r.placement[c.nodes[i].id] = Interval{out[2 * i], out[2 * i + 1]};
+  if (score_moves) r.value = detail::solve_one(c, r.placement, allow_partial).value;
   r.moves = moves;
   r.scored = scored;
   return r;

@@ -3,7 +3,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import json,time,paper_2406_01566_b200 as h
 from paper_2406_01566_b200 import clusters
-for n in ("het42-70b","geo24","geo24-70b","single24-70b","syn256-120l"):
+for n in sys.argv[1:] or ("het42-70b","geo24","geo24-70b","single24-70b","syn256-120l"):
     c=h.Cluster.from_json(json.dumps(clusters.CONFIGS[n]()))
     out={"config":n}
     for m in ("swarm","petals","sp","local","sampled"):
