@@ -182,30 +182,121 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def reference_rate(cluster_dict, kmax, L, budget_s, threads, first=0, rows_fn=None):
-    """The unmodified reference (oracle/_ref) on the host cores: build_flow_graph
-    + max_flow per candidate on a std::thread pool.  Returns (evals/s, sample).
-    Inputs are prepared outside the timed call (rows_fn(first, n), default
-    G(seed, i) chains)."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from _support import RefCluster, ref_available  # test infrastructure: reference arm only
-    import paper_2406_01566_b200 as h
+def load_workloads():
+    """The workload clusters (paper_2406_01566_b200/clusters.py: builders of
+    dicts in the reference's cluster JSON schema, stdlib only) loaded by file
+    path, so the reference arm never imports the package (whose import loads
+    the CUDA extension)."""
+    import importlib.util
 
-    if not ref_available():
-        raise RuntimeError("oracle/_ref/libhelio_ref.so missing (build in the container with /root/reference)")
-    if rows_fn is None:
-        rows_fn = lambda f, n: h.generate_host(kmax, L, SEED, f, n, 0)  # noqa: E731
-    rc = RefCluster(cluster_dict)
-    probe = rows_fn(first, 64 * threads)
-    t0 = time.perf_counter()
-    rc.score(probe, True, threads)
-    rate = len(probe) / max(time.perf_counter() - t0, 1e-6)
-    n = int(min(max(rate * budget_s, 64 * threads), 400_000))
-    rows = rows_fn(first, n)
-    t0 = time.perf_counter()
-    rc.score(rows, True, threads)
-    dt = time.perf_counter() - t0
-    return n / dt, n, dt
+    spec = importlib.util.spec_from_file_location(
+        "helio_workloads", os.path.join(ROOT, "paper_2406_01566_b200", "clusters.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+class RefArm:
+    """The unmodified reference (oracle/_ref/libhelio_ref.so, compiled from
+    /root/reference by oracle/Makefile) through ctypes: the reference's own
+    parse_cluster, ClusterSpec::max_layers, build_flow_graph + max_flow, and the
+    workload generator restated over its ClusterSpec (refh_generate).  Nothing
+    from paper_2406_01566_b200 is loaded on this path."""
+
+    SO = os.path.join(ROOT, "oracle", "_ref", "libhelio_ref.so")
+
+    def __init__(self, cluster_dict):
+        import ctypes as C
+
+        import numpy as np
+
+        if not os.path.exists(self.SO):
+            raise RuntimeError("oracle/_ref/libhelio_ref.so missing (built in the container from /root/reference)")
+        self.np, self.C = np, C
+        lib = C.CDLL(self.SO)
+        i16 = np.ctypeslib.ndpointer(np.int16, flags="C_CONTIGUOUS")
+        i32 = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+        f64 = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        lib.refh_cluster_from_json.restype = C.c_void_p
+        lib.refh_cluster_from_json.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        lib.refh_cluster_free.argtypes = [C.c_void_p]
+        lib.refh_cluster_num_nodes.argtypes = [C.c_void_p]
+        lib.refh_max_layers.argtypes = [C.c_void_p, C.c_int]
+        lib.refh_score.argtypes = [C.c_void_p, i16, C.c_int64, C.c_int, C.c_int, f64, i32]
+        lib.refh_solve_only.argtypes = [C.c_void_p, i16, C.c_int64, C.c_int, C.c_int,
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        lib.refh_solve_only.restype = C.c_int64
+        lib.refh_generate.argtypes = [C.c_void_p, C.c_uint64, C.c_int64, C.c_int64, C.c_uint32, C.c_int,
+                                      C.c_int, i16]
+        self.lib = lib
+        err = C.create_string_buffer(512)
+        self.h = lib.refh_cluster_from_json(json.dumps(cluster_dict).encode(), err, 512)
+        if not self.h:
+            raise RuntimeError(f"reference parse_cluster failed: {err.value.decode()}")
+        self.N = lib.refh_cluster_num_nodes(self.h)
+        self.kmax = [lib.refh_max_layers(self.h, k) for k in range(self.N)]
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.refh_cluster_free(self.h)
+
+    def rows(self, first, n, walk, ppm=0, threads=None):
+        out = self.np.zeros((n, self.N, 2), self.np.int16)
+        self.lib.refh_generate(self.h, SEED, first, n, ppm, int(walk), threads or (os.cpu_count() or 1), out)
+        return out
+
+    def score(self, rows, threads):
+        n = rows.shape[0]
+        v = self.np.zeros(n, self.np.float64)
+        st = self.np.zeros(n, self.np.int32)
+        t0 = time.perf_counter()
+        self.lib.refh_score(self.h, rows, n, 1, threads, v, st)
+        return v, st, time.perf_counter() - t0
+
+    def solve_only(self, rows, threads):
+        s, chk = self.C.c_double(0), self.C.c_double(0)
+        g = self.lib.refh_solve_only(self.h, rows, rows.shape[0], 1, threads, self.C.byref(s), self.C.byref(chk))
+        return g, s.value
+
+    def rate(self, first, budget_s, threads, walk, ppm=0):
+        """evals/s of build_flow_graph + max_flow over the workload's rows
+        [first, first + n), n sized for ~budget_s; generation untimed."""
+        probe = self.rows(first, 32 * threads, walk, ppm)
+        for _ in range(2):  # the first call pays page faults and allocator warm-up
+            _, _, dt = self.score(probe, threads)
+        n = int(min(max(len(probe) / max(dt, 1e-6) * budget_s, 32 * threads), 2_000_000))
+        rows = self.rows(first, n, walk, ppm)
+        _, _, dt = self.score(rows, threads)
+        return n / dt, n, dt
+
+
+def reference_baseline(cluster_dict, walk, budget_s, ppm=0, arm=None):
+    """SURVEY.md §8(d) "CPU reference timing": the unmodified reference on every
+    host thread (the headline baseline), plus one core, plus max_flow alone on
+    pre-built graphs, on the first candidates of the workload."""
+    ra = arm or RefArm(cluster_dict)
+    threads = os.cpu_count() or 1
+    rate, n, dt = ra.rate(0, budget_s, threads, walk, ppm)
+    r1, n1, _ = ra.rate(0, max(1.0, budget_s / 4), 1, walk, ppm)
+    rows = ra.rows(0, min(n, 200_000), walk, ppm)
+    g, solve_s = ra.solve_only(rows, threads)
+    return {"value": rate, "unit": "evals/s", "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(),
+            "sample": f"first {n} candidates of the workload ({dt:.1f} s wall): unmodified reference "
+                      f"build_flow_graph + max_flow (enumerate.hpp:56-57) on a {threads}-thread std::thread pool",
+            "single_core": {"value": r1, "unit": "evals/s", "sample": f"first {n1} candidates, 1 thread"},
+            "solve_only": {"value": g / solve_s if solve_s > 0 else None, "unit": "max_flow/s",
+                           "sample": f"max_flow on {g} pre-built FlowGraphs, {threads} threads"}}
 
 
 def routing_leg(h, clusters, dev, sp, requests, with_reference):
@@ -427,48 +518,93 @@ def search_leg(h, clusters, dev):
     return out
 
 
+# default global batch per config (BASELINE.json configs): het42 1M sharded
+# over N (configs[2]), syn256 10M (configs[4]), the rest 100k (configs[1], [3])
+DEFAULT_BATCH = {"het42-70b": 1_000_000, "syn256-120l": 10_000_000}
+
+
+def shard(args, world, rank):
+    """(first global index, candidates on this rank, global batch).  strong:
+    the global batch is split into contiguous ranges [r*G/N, (r+1)*G/N);
+    weak: every rank scores its own --per-gpu candidates."""
+    if args.scaling == "strong":
+        G = args.global_batch
+        lo, hi = rank * G // world, (rank + 1) * G // world
+        return lo, hi - lo, G
+    return rank * args.per_gpu, args.per_gpu, args.per_gpu * world
+
+
+def bench_config(args, world):
+    """The `config` object — identical on both arms (static workload facts only;
+    measured details live in other keys)."""
+    _, n0, G = shard(args, world, 0)
+    return {"workload": workload_of(args.config), "global_batch": G, "candidates_per_gpu": n0,
+            "parallelism": f"dp{world} (candidate shards; NCCL all-gather of the 16 B argmax record)",
+            "capacity": "float", "allow_partial": True, "generator_seed": SEED, "p_uniform_ppm": args.ppm,
+            "l2": "GPU arm: L2 flushed (256 MB write) between timed steps"}
+
+
 def run_reference(args):
-    rank = env_int("RANK", 0)
+    """--impl reference: the unmodified reference on the host cores, on this
+    run's workload (RefArm: oracle/_ref only — no package import).  Each step
+    scores a bounded sample of the global batch (rows rotate through it)."""
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", args.gpus)
     if rank != 0:
         return 0
-    import paper_2406_01566_b200 as h
-    from paper_2406_01566_b200 import clusters
-
-    d = clusters.CONFIGS[args.config]("float")
-    c = h.Cluster.from_json(json.dumps(d))
-    kmax = [c.max_layers(i) for i in c.node_ids]
+    wl = load_workloads()
+    d = wl.CONFIGS[args.config]("float")
+    walk = args.config in WALK_CONFIGS
+    ra = RefArm(d)
     threads = os.cpu_count() or 1
-    rows_fn = None
-    if args.config in WALK_CONFIGS:  # link walks need the compiled link lists (input prep, untimed)
-        gen = h.Engine(c)
-        rows_fn = lambda f, n: host_rows(h, args.config, kmax, c.num_layers, f, n, eng=gen)  # noqa: E731
-    rates = []
-    samples = 0
-    step_ms = []
+    _, _, G = shard(args, world, 0)
+    # size one step for ~ref_step_s of host work (bounded: the whole run stays
+    # within a few minutes), from a probe
+    probe = ra.rows(0, 32 * threads, walk, args.ppm)
+    for _ in range(2):  # the first call pays page faults and allocator warm-up
+        _, _, dt = ra.score(probe, threads)
+    n = int(min(max(len(probe) / max(dt, 1e-6) * args.ref_step_s, 32 * threads), G))
+    evals, secs, step_ms = 0, 0.0, []
     for step in range(args.warmup + args.steps):
-        r, n, dt = reference_rate(d, kmax, c.num_layers, args.ref_step_s, threads, first=step * 10_000_000,
-                                  rows_fn=rows_fn)
+        first = (step * n) % max(1, G - n + 1)
+        rows = ra.rows(first, n, walk, args.ppm)  # input preparation, untimed
+        _, _, dt = ra.score(rows, threads)
         if step >= args.warmup:
-            rates.append(r)
-            samples += n
-            step_ms.append(n / r * 1e3 if r else None)
-    value = sorted(rates)[len(rates) // 2]
-    ms = [x for x in step_ms if x]
+            evals += n
+            secs += dt
+            step_ms.append(dt * 1e3)
+    value = evals / secs
+    base = reference_baseline(d, walk, max(2.0, args.ref_step_s), args.ppm, arm=ra)
+    base.update({"value": value,
+                 "sample": f"{args.steps} timed steps (+{args.warmup} warm-up) of {n} candidates each, rotating "
+                           f"through the {G}-candidate workload: unmodified reference build_flow_graph + max_flow "
+                           f"on a {threads}-thread std::thread pool"})
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sum(ms) / len(ms) if ms else None, "higher_is_better": True, "scaling": "weak",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sum(step_ms) / len(step_ms), "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_of(args.config), "parallelism": "host threads",
-                   "candidates_per_step": samples // max(1, args.steps)},
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
-                         "sample": f"median of {args.steps} steps, each ~{args.ref_step_s:.0f}s of "
-                                   f"build_flow_graph+max_flow on the first candidates of the workload "
-                                   f"(std::thread pool, {threads} threads)"},
+        "config": bench_config(args, world),
+        "cpu_baseline": base,
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
     }
     print(json.dumps(out))
     return 0
+
+
+def time_steps(step, flush, stream, steps, dev):
+    """CUDA events on the launching stream around each step, L2 flushed between
+    steps (outside the events); returns total ms."""
+    import torch
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    return sum(a.elapsed_time(b) for a, b in ev)
 
 
 def main():
@@ -478,6 +614,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="het42-70b")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: --global-batch split over the ranks (BASELINE configs[2]); "
+                         "weak: --per-gpu candidates on every rank")
+    ap.add_argument("--global-batch", type=int, default=None)
     ap.add_argument("--per-gpu", type=int, default=1_000_000)
     ap.add_argument("--ppm", type=int, default=0, help="uniform-interval mix, parts per million")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -486,12 +626,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-routing", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--no-weak", action="store_true")
     ap.add_argument("--route-requests", type=int, default=1_000_000)
     ap.add_argument("--mode", default="score", choices=["score", "parity"],
                     help="headline scoring mode (the other mode is timed too and reported beside it)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.global_batch is None:
+        args.global_batch = DEFAULT_BATCH.get(args.config, 100_000)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -508,23 +651,28 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     d = clusters.CONFIGS[args.config]("float")
+    walk = args.config in WALK_CONFIGS
+    headline = args.config == "het42-70b"
     c = h.Cluster.from_json(json.dumps(d))
     eng = h.Engine(c, device=local)
     eng.mode = args.mode
     N, L = eng.num_nodes, eng.num_layers
-    B = args.per_gpu
-    first = rank * B
+    first, B, G = shard(args, world, rank)
     # a dedicated stream: its handle is what the engine launches on, and the
     # CUDA events below are recorded on the same stream
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
     sp = stream.cuda_stream
 
-    pl = torch.empty((B, N, 2), dtype=torch.int16, device=dev)
-    if args.config in WALK_CONFIGS:
-        eng.generate_walk_device(SEED, first, B, pl.data_ptr(), sp)
-    else:
-        eng.generate_device(SEED, first, B, args.ppm, pl.data_ptr(), sp)
+    def make_rows(first_, n_):
+        t = torch.empty((n_, N, 2), dtype=torch.int16, device=dev)
+        if walk:
+            eng.generate_walk_device(SEED, first_, n_, t.data_ptr(), sp)
+        else:
+            eng.generate_device(SEED, first_, n_, args.ppm, t.data_ptr(), sp)
+        return t
+
+    pl = make_rows(first, B)
     vals = torch.empty(B, dtype=torch.float64, device=dev)
     st = torch.empty(B, dtype=torch.int32, device=dev)
     best = torch.empty(1, dtype=torch.float64, device=dev)
@@ -533,13 +681,16 @@ def main():
     gathered = torch.empty(2 * world, dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
 
-    def step():
-        eng.score_device(pl.data_ptr(), B, vals.data_ptr(), st.data_ptr(), True, sp)
-        eng.argmax_device(vals.data_ptr(), st.data_ptr(), B, first, best.data_ptr(), bidx.data_ptr(), sp)
+    def step_on(rows, n, base, v, s):
+        eng.score_device(rows.data_ptr(), n, v.data_ptr(), s.data_ptr(), True, sp)
+        eng.argmax_device(v.data_ptr(), s.data_ptr(), n, base, best.data_ptr(), bidx.data_ptr(), sp)
         if world > 1:
             rec[0:1].copy_(best.view(torch.int64))
             rec[1:2].copy_(bidx)
             dist.all_gather_into_tensor(gathered, rec)
+
+    def step():
+        step_on(pl, B, first, vals, st)
 
     for _ in range(args.warmup):
         step()
@@ -567,149 +718,147 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = (B * world) / (ms_per_step / 1e3)
-
-    # the other mode, same batch, same timing rules (reported beside the headline)
-    other = "parity" if args.mode == "score" else "score"
-    eng.mode = other
-    oth = []
-    for i in range(args.steps + 1):
-        flush.zero_()
-        a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        step()
-        b2.record(stream)
-        torch.cuda.synchronize(dev)
-        if i > 0:
-            oth.append(a.elapsed_time(b2))
-    eng.mode = args.mode
-    ot = torch.tensor([sum(oth)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ot, op=dist.ReduceOp.MAX)
-    other_rate = (B * world) / (float(ot.item()) / len(oth) / 1e3)
-    eng.mode = other
-    step()
-    torch.cuda.synchronize(dev)
-    other_vals = vals.clone()
-    eng.mode = args.mode
-    step()
-    torch.cuda.synchronize(dev)
-    rel = ((vals - other_vals).abs() / other_vals.abs().clamp(min=1.0)).max().item()
-
-    # winner (deterministic: max value, then min global index)
+    value = G / (ms_per_step / 1e3)  # every candidate of the global batch, over the slowest rank's time
+    recs = unpack = None
     from paper_2406_01566_b200.dist import reduce_best, unpack_records
     recs = unpack_records(gathered) if world > 1 else [(float(best.item()), int(bidx.item()))]
     win = reduce_best(recs)
+    st_host = st.cpu().numpy()
+    head_vals = vals.clone()
+    nonzero = float((head_vals > 0).double().mean().item())
+
+    # the other mode on (a bounded prefix of) the same rows, same timing rules
+    other = "parity" if args.mode == "score" else "score"
+    ob = min(B, 1_000_000 if headline else 100_000)
+    osteps = min(args.steps, 5)
+    eng.mode = other
+    ov = torch.empty(ob, dtype=torch.float64, device=dev)
+    os_ = torch.empty(ob, dtype=torch.int32, device=dev)
+    ostep = lambda: step_on(pl, ob, first, ov, os_)  # noqa: E731
+    ostep()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ot = torch.tensor([time_steps(ostep, flush, stream, osteps, dev)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ot, op=dist.ReduceOp.MAX)
+    other_rate = (ob * world) / (float(ot.item()) / osteps / 1e3)
+    eng.mode = args.mode
+    hv_ = head_vals[:ob]
+    rel = ((hv_ - ov).abs() / ov.abs().clamp(min=1.0)).max().item() if ob else 0.0
+
+    # weak scaling beside the strong headline: --per-gpu candidates on every rank
+    weak = None
+    if args.scaling == "strong" and world > 1 and not args.no_weak:
+        wB = args.per_gpu
+        wpl = make_rows(rank * wB, wB)
+        wv = torch.empty(wB, dtype=torch.float64, device=dev)
+        ws = torch.empty(wB, dtype=torch.int32, device=dev)
+        wstep = lambda: step_on(wpl, wB, rank * wB, wv, ws)  # noqa: E731
+        for _ in range(2):
+            wstep()
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        wt = torch.tensor([time_steps(wstep, flush, stream, args.steps, dev)], dtype=torch.float64, device=dev)
+        dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        wms = float(wt.item()) / args.steps
+        weak = {"value": wB * world / (wms / 1e3), "unit": "evals/s", "candidates_per_gpu": wB,
+                "global_batch": wB * world, "ms_per_step": wms}
+        del wpl, wv, ws
+
     # the winner's plan reaches every rank: its owner
     # computes the PARITY per-edge flows and broadcasts row + flows over NCCL
     winner_plan = None
     if world > 1 and win[1] >= 0:
-        from paper_2406_01566_b200.dist import share_winner
+        from paper_2406_01566_b200.dist import owner_of, share_winner
+        owner = owner_of(win[1], [shard(args, world, r)[0] for r in range(world)])
         row_w = flows_w = None
-        if win[1] // B == rank:
+        if owner == rank:
             row_w = pl[win[1] - first].cpu().numpy()
             _, _, _, ne_w, _, dbl_w = eng.flows(row_w[None], True)
             flows_w = dbl_w[0, :int(ne_w[0]), 1]
         t_share = time.perf_counter()
-        row_s, flows_s = share_winner(win[1], B, row_w, flows_w)
-        winner_plan = {"owner_rank": win[1] // B, "edges": int(flows_s.size),
+        row_s, flows_s = share_winner(owner, row_w, flows_w, N)
+        winner_plan = {"owner_rank": owner, "edges": int(flows_s.size),
                        "bytes": int(row_s.nbytes + flows_s.nbytes),
                        "ms": (time.perf_counter() - t_share) * 1e3}
-    st_host = st.cpu().numpy()
-    nonzero = float((vals.cpu().numpy() > 0).mean())
 
-    # roofline of the dominant kernel (fused build+solve): algorithmic bytes per
-    # eval = 4N (int16 start/end in) + 8 (value) + 4 (status) — SURVEY §8(d).
-    bytes_per_eval = 4 * N + 8 + 4
-    kms = [k for k in kernel_ms if k and k > 0]
-    avg_kernel_ms = sum(kms) / len(kms) if kms else ms_per_step
-    achieved = bytes_per_eval * B / (avg_kernel_ms / 1e3) / 1e9
-    peak, peak_src = load_peaks()
-    tpe, tsrc, tgraphs = ncu_traffic_per_eval(args.config, args.mode)
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak,
-                "traffic": (tpe * B) if tpe is not None else None,
-                "traffic_unit": "bytes per launch (DRAM read + write)",
-                "traffic_source": (f"{tsrc}: ncu --set full of one {tgraphs}-candidate launch, per candidate x {B}"
-                                   if tsrc else "no committed capture for this config/mode"),
-                "algorithmic_bytes_per_launch": bytes_per_eval * B,
-                "kernel": f"score_kernel<{args.mode}> (fused K1 build + K2 solve, one warp per graph)",
-                "kernel_ms": avg_kernel_ms, "kernel_share_of_step": avg_kernel_ms / ms_per_step,
-                "bytes_per_eval": bytes_per_eval, "peak_source": peak_src,
-                "note": "latency/issue-bound SIMT graph kernel: HBM fraction is structurally tiny; "
-                        "see DESIGN.md and profiles/ for issue/smem evidence"}
-
-    # e2e through the C ABI with host buffers (pinned), timed on the host
-    e2e = None
+    # e2e through the C ABI with host buffers, timed on the host: the same rows
+    # copied to pinned host memory (and to pageable memory for the second leg)
+    e2e = e2e_pageable = None
     if not args.no_e2e:
-        host = torch.from_numpy(host_rows(h, args.config, list(eng.kmax), L, first, B, args.ppm, eng)).pin_memory()
-        hv = torch.empty(B, dtype=torch.float64).pin_memory()
-        hs = torch.empty(B, dtype=torch.int32).pin_memory()
-        for _ in range(2):
-            eng.score_best_host_ptr(host.data_ptr(), B, hv.data_ptr(), hs.data_ptr(), True)
-        times = []
-        for _ in range(args.steps):
+        host = torch.empty((B, N, 2), dtype=torch.int16, pin_memory=True)
+        host.copy_(pl)
+        hv = torch.empty(B, dtype=torch.float64, pin_memory=True)
+        hs = torch.empty(B, dtype=torch.int32, pin_memory=True)
+
+        def e2e_time(hin, hval, hst, steps):
+            for _ in range(2):
+                eng.score_best_host_ptr(hin.data_ptr(), B, hval.data_ptr(), hst.data_ptr(), True)
+            times, res = [], None
+            for _ in range(steps):
+                if world > 1:
+                    dist.barrier()
+                t0 = time.perf_counter()
+                res = eng.score_best_host_ptr(hin.data_ptr(), B, hval.data_ptr(), hst.data_ptr(), True)
+                times.append(time.perf_counter() - t0)
+            tt = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
             if world > 1:
-                dist.barrier()
-            t0 = time.perf_counter()
-            e2e_best = eng.score_best_host_ptr(host.data_ptr(), B, hv.data_ptr(), hs.data_ptr(), True)
-            times.append(time.perf_counter() - t0)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return G * steps / float(tt.item()), res
+
+        e2e_rate, e2e_best = e2e_time(host, hv, hs, args.steps)
         if world == 1:
-            assert int(e2e_best[1]) == recs[0][1], "e2e winner differs from the device path"
-        tt = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_rate = B * world * args.steps / float(tt.item())
-        assert torch.equal(hv.view(torch.int64), vals.cpu().view(torch.int64)), "e2e values differ from device path"
-        e2e = {"value": e2e_rate, "unit": "evals/s", "h2d_bytes_per_step": B * world * 4 * N,
-               "d2h_bytes_per_step": B * world * 12 + 16 * world,
+            assert int(e2e_best[1]) == win[1], "e2e winner differs from the device path"
+        assert torch.equal(hv.view(torch.int64), head_vals.cpu().view(torch.int64)), "e2e values differ"
+        e2e = {"value": e2e_rate, "unit": "evals/s", "h2d_bytes_per_step": G * 4 * N,
+               "d2h_bytes_per_step": G * 12 + 16 * world,
                "call": "helio_gpu_score_best_host (pinned host placements in; every value + status and the "
                        "first-max winner out)"}
+        # pageable buffers (what Engine.score and a plain ctypes caller pass):
+        # the entry stages chunks through its own pinned buffers
+        hp = torch.empty((B, N, 2), dtype=torch.int16)
+        hp.copy_(host)
+        del host
+        hvp = torch.empty(B, dtype=torch.float64)
+        hsp = torch.empty(B, dtype=torch.int32)
+        prate, _ = e2e_time(hp, hvp, hsp, min(args.steps, 5))
+        assert torch.equal(hvp.view(torch.int64), head_vals.cpu().view(torch.int64)), "pageable e2e values differ"
+        e2e_pageable = {"value": prate, "unit": "evals/s", "h2d_bytes_per_step": G * 4 * N,
+                        "d2h_bytes_per_step": G * 12 + 16 * world,
+                        "call": "helio_gpu_score_best_host with pageable host buffers (staged)"}
+        del hp, hvp, hsp
 
-    # extras (single-GPU views) only at N = 1: at N > 1 the other ranks must not
-    # wait on rank 0 outside the timed region
-    split = None
-    if world == 1 and not args.no_configs:
+    # extras (single-GPU views of the headline cluster) only at N = 1: at N > 1
+    # the other ranks must not wait on rank 0 outside the timed region
+    extras = world == 1 and headline and not args.no_configs
+    split = cfg_table = routing = search = None
+    if extras:
+        for name, fn in (("split", lambda: split_leg(eng, local, sp)),
+                         ("cfg", lambda: config_table(h, clusters, local, sp, with_reference=not args.no_cpu_baseline)),
+                         ("search", lambda: search_leg(h, clusters, local))):
+            try:
+                r = fn()
+            except Exception as ex:  # reported, never fatal
+                r = {"error": str(ex)}
+            if name == "split":
+                split = r
+            elif name == "cfg":
+                cfg_table = r
+            else:
+                search = r
+    if world == 1 and headline and not args.no_routing:
         try:
-            split = split_leg(eng, local, sp)
-        except Exception as ex:  # reported, never fatal
-            split = {"error": str(ex)}
-
-    cfg_table = None
-    if world == 1 and not args.no_configs:
-        try:
-            cfg_table = config_table(h, clusters, local, sp, with_reference=(world == 1 and not args.no_cpu_baseline))
-        except Exception as ex:  # reported, never fatal
-            cfg_table = [{"error": str(ex)}]
-
-    routing = None
-    if world == 1 and not args.no_routing:
-        try:
-            routing = routing_leg(h, clusters, local, sp, args.route_requests,
-                                  with_reference=(world == 1 and not args.no_cpu_baseline))
+            routing = routing_leg(h, clusters, local, sp, args.route_requests, with_reference=not args.no_cpu_baseline)
         except Exception as ex:  # reported, never fatal
             routing = {"value": None, "error": str(ex)}
-
-    search = None
-    if world == 1 and not args.no_configs:
-        try:
-            search = search_leg(h, clusters, local)
-        except Exception as ex:  # reported, never fatal
-            search = {"error": str(ex)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            threads = os.cpu_count() or 1
-            r, n, dt = reference_rate(d, list(eng.kmax), L, args.cpu_seconds, threads,
-                                      rows_fn=lambda f, n: host_rows(h, args.config, list(eng.kmax), L, f, n,
-                                                                     eng=eng))
-            cpu = {"value": r, "unit": "evals/s", "cores": threads, "kind": "reference",
-                   "sample": f"first {n} candidates of the workload, {dt:.1f}s wall, unmodified reference "
-                             f"build_flow_graph+max_flow on a {threads}-thread std::thread pool"}
+            cpu = reference_baseline(d, walk, args.cpu_seconds, args.ppm)
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "evals/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
-
     if search and cpu and cpu.get("value") and "runs" in search:
         for r in search["runs"]:  # the same scoring on the reference, at the measured host rate
             r["reference_equivalent_seconds"] = r["scored"] / cpu["value"]
@@ -720,33 +869,54 @@ def main():
         dist.all_gather_object(per_rank, {"sm_mhz": clocks.get("sm_mhz"), "reasons": clocks.get("reasons"),
                                           "kernel_ms": sum(k for k in kernel_ms if k) / max(1, len(kernel_ms))})
         clocks["per_rank"] = per_rank
-    # the roofline that binds this kernel: warp-instruction issue (4 schedulers
-    # per SM, one instruction per clock each) — see DESIGN.md §4
+
+    # roofline of the dominant kernel (fused build + solve).  The binding
+    # resource is warp-instruction issue: warp-instructions per
+    # candidate from the committed ncu capture x candidates per launch / the
+    # live kernel time, against SMs x 4 schedulers x the sampled SM clock.
+    # HBM (SURVEY §8(d) fused formula 4N + 8, + 4 B status) is kept beside it.
+    bytes_per_eval = 4 * N + 8 + 4
+    kms = [k for k in kernel_ms if k and k > 0]
+    avg_kernel_ms = sum(kms) / len(kms) if kms else ms_per_step
+    hbm_ach = bytes_per_eval * B / (avg_kernel_ms / 1e3) / 1e9
+    peak, peak_src = load_peaks()
+    tpe, tsrc, tgraphs = ncu_traffic_per_eval(args.config, args.mode)
     ipe = ncu_inst_per_eval(args.config, args.mode)
-    if ipe and clocks.get("sm_mhz"):
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        issue_peak = sms * 4 * clocks["sm_mhz"] * 1e6
-        issue_ach = ipe * B / (avg_kernel_ms / 1e3)
-        roofline["issue"] = {"bound": "warp-instruction issue", "warp_instr_per_eval": ipe,
-                             "achieved": issue_ach, "peak": issue_peak, "unit": "warp-instr/s",
-                             "frac": issue_ach / issue_peak,
-                             "source": "smsp__inst_executed.sum per candidate from the committed ncu capture; "
-                                       "peak = SMs x 4 schedulers x median SM clock under load"}
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mhz = clocks.get("sm_mhz") or 1965.0
+    issue_peak = sms * 4 * mhz * 1e6
+    issue_ach = ipe * B / (avg_kernel_ms / 1e3) if ipe else None
+    roofline = {"bound": "issue", "achieved": issue_ach, "peak": issue_peak, "unit": "warp-instr/s",
+                "frac": (issue_ach / issue_peak) if issue_ach else None,
+                "issue_frac": (issue_ach / issue_peak) if issue_ach else None,
+                "warp_instr_per_eval": ipe,
+                "issue_source": "smsp__inst_executed.sum per candidate from the committed ncu capture; peak = SMs x "
+                                "4 schedulers x median SM clock under load",
+                "traffic": (tpe * B) if tpe is not None else None,
+                "traffic_unit": "bytes per launch (DRAM read + write)",
+                "traffic_source": (f"{tsrc}: ncu --set full of one {tgraphs}-candidate launch, per candidate x {B}"
+                                   if tsrc else "no committed capture for this config/mode"),
+                "hbm_achieved": hbm_ach, "hbm_peak": peak, "hbm_unit": "GB/s", "hbm_frac": hbm_ach / peak,
+                "hbm_peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_per_eval * B,
+                "bytes_per_eval": bytes_per_eval,
+                "kernel": f"score_kernel<{args.mode}> (fused K1 build + K2 solve; small/middle/big slot tiers)",
+                "kernel_ms": avg_kernel_ms, "kernel_share_of_step": avg_kernel_ms / ms_per_step}
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_of(args.config), "candidates_per_gpu": B, "global_batch": B * world,
-                       "parallelism": f"dp{world} (candidate shards; NCCL all-gather of the 16 B argmax record)",
-                       "mode": args.mode, "p_uniform_ppm": args.ppm,
-                       "other_mode": {"mode": other, "value": other_rate, "unit": "evals/s",
-                                      "max_rel_diff_vs_headline": rel},
-                       "l2": "L2 flushed (256 MB write) between timed steps; inputs 168 MB/GPU",
-                       "nonzero_fraction": nonzero, "status_nonzero": int((st_host != 0).sum()),
-                       "best": {"value": win[0], "index": win[1]}, "winner_plan_broadcast": winner_plan},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "config": bench_config(args, world),
+            "details": {"mode": args.mode,
+                        "other_mode": {"mode": other, "value": other_rate, "unit": "evals/s", "candidates": ob,
+                                       "max_rel_diff_vs_headline": rel},
+                        "nonzero_fraction": nonzero, "status_nonzero": int((st_host != 0).sum()),
+                        "best": {"value": win[0], "index": win[1]}, "winner_plan_broadcast": winner_plan,
+                        "inputs_bytes_per_gpu": B * 4 * N},
+            "weak_scaling": weak,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_pageable": e2e_pageable,
+            "gpu_launches": launches,
             "routing": routing, "other_configs": cfg_table, "split_pipeline": split, "search": search,
             "clocks": clocks,
         }

@@ -19,6 +19,7 @@
 // an empty Interval in the reference's Placement map (flow_graph.cpp:53).
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -156,16 +157,172 @@ int refh_score(void* cp, const int16_t* pl, int64_t B, int allow_partial, int nt
   return 0;
 }
 
-// Solve-only rate on pre-built graphs (reported beside the whole-eval rate).
-double refh_solve_only(void* cp, const int16_t* pl, int64_t B, int allow_partial) {
+// Solve-only rate on pre-built graphs (SURVEY.md §8(d) "CPU reference
+// timing" item 4): build every candidate's FlowGraph first (untimed), then
+// time max_flow alone on the same std::thread pool.  Invalid rows are skipped.
+// Returns the number of graphs solved; *solve_s = wall seconds of the solves.
+int64_t refh_solve_only(void* cp, const int16_t* pl, int64_t B, int allow_partial, int nthreads,
+                        double* solve_s, double* checksum) {
   const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
   const int64_t N = static_cast<int64_t>(c.nodes.size());
+  if (nthreads < 1) nthreads = 1;
   std::vector<FlowGraph> gs;
   gs.reserve(B);
-  for (int64_t b = 0; b < B; ++b) gs.push_back(build_flow_graph(c, to_placement(c, pl + b * N * 2), allow_partial != 0));
+  for (int64_t b = 0; b < B; ++b) {
+    try {
+      gs.push_back(build_flow_graph(c, to_placement(c, pl + b * N * 2), allow_partial != 0));
+    } catch (const ValidationError&) {
+    }
+  }
+  const int64_t G = static_cast<int64_t>(gs.size());
+  std::vector<double> part(nthreads, 0.0);
+  auto work = [&](int t, int64_t lo, int64_t hi) {
+    double acc = 0;
+    for (int64_t b = lo; b < hi; ++b) acc += max_flow(gs[b]);
+    part[t] = acc;
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  const int64_t chunk = (G + nthreads - 1) / nthreads;
+  for (int t = 0; t < nthreads; ++t) {
+    int64_t lo = t * chunk, hi = std::min(G, lo + chunk);
+    if (lo >= hi) break;
+    pool.emplace_back(work, t, lo, hi);
+  }
+  for (auto& th : pool) th.join();
+  *solve_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   double acc = 0;
-  for (auto& g : gs) acc += max_flow(g);
-  return acc;
+  for (double x : part) acc += x;
+  *checksum = acc;
+  return G;
+}
+
+// The benchmark workload generator G(seed, i) of SURVEY.md §8(d), restated
+// here over the reference's own ClusterSpec so the reference arm of bench.py
+// needs nothing but this library: k_i from ClusterSpec::max_layers
+// (cluster.cpp:62-68), walk adjacency from c.links.  The specification (and
+// the product's copy, used by the GPU arm) is paper_2406_01566_b200/csrc/gen.h;
+// tests/test_oracle_golden.py checks the two produce identical rows.
+namespace gen {
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+uint64_t fmix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint64_t key_of(uint64_t seed, uint64_t i) { return fmix(fmix(seed + kGolden) + (i + 1) * kGolden); }
+uint64_t draw(uint64_t key, uint32_t k) { return fmix(key + (uint64_t)(k + 1) * kGolden); }
+uint32_t uniform(uint64_t x, uint32_t m) { return (uint32_t)(((x >> 32) * (uint64_t)m) >> 32); }
+
+// covering chains: a random node order; each node takes U[1,k_i] layers from
+// the running layer (wrapping at L); with probability ppm/1e6 a uniform interval
+void chain(const std::vector<int>& kmax, int L, uint64_t seed, uint64_t i, uint32_t ppm, int16_t* out) {
+  const int N = static_cast<int>(kmax.size());
+  const uint64_t key = key_of(seed, i);
+  std::vector<int> order(N);
+  for (int k = 0; k < N; ++k) order[k] = k;
+  for (int k = N - 1; k >= 1; --k) std::swap(order[k], order[uniform(draw(key, k), k + 1)]);
+  int layer = 0;
+  for (int pos = 0; pos < N; ++pos) {
+    const int node = order[pos], k = kmax[node];
+    const uint32_t d = (uint32_t)N + 3u * (uint32_t)pos;
+    int s = 0, e = 0;
+    if (k >= 1) {
+      if (ppm > 0 && uniform(draw(key, d), 1000000u) < ppm) {
+        const int len = (int)uniform(draw(key, d + 1), (uint32_t)k + 1u);
+        s = (int)uniform(draw(key, d + 2), (uint32_t)(L - len) + 1u);
+        e = s + len;
+      } else {
+        const int len = 1 + (int)uniform(draw(key, d + 1), (uint32_t)k);
+        s = layer;
+        e = std::min(layer + len, L);
+        layer = e == L ? 0 : e;
+      }
+    }
+    out[2 * node] = (int16_t)s;
+    out[2 * node + 1] = (int16_t)e;
+  }
+}
+
+// link walks (sparse topologies): from the coordinator, step to a uniformly
+// chosen unused node over a declared link; restart at layer 0 on reaching L
+// or a dead end.  succ[0] = coordinator's targets, succ[1+k] = node k's.
+void walk(const std::vector<int>& kmax, int L, uint64_t seed, uint64_t i,
+          const std::vector<std::vector<int>>& succ, int16_t* out) {
+  const int N = static_cast<int>(kmax.size());
+  const uint64_t key = key_of(seed, i);
+  std::vector<char> used(N, 0);
+  std::fill(out, out + 2 * N, int16_t(0));
+  int prev = -1, layer = 0;
+  uint32_t nd = 0;
+  for (int step = 0; step < 2 * N; ++step) {
+    std::vector<int> open;
+    for (int j : succ[prev + 1])
+      if (!used[j] && kmax[j] >= 1) open.push_back(j);
+    if (open.empty()) {
+      if (prev == -1) break;
+      prev = -1;
+      layer = 0;
+      continue;
+    }
+    const int j = open[uniform(draw(key, nd++), (uint32_t)open.size())];
+    used[j] = 1;
+    const int len = 1 + (int)uniform(draw(key, nd++), (uint32_t)kmax[j]);
+    const int e = std::min(layer + len, L);
+    out[2 * j] = (int16_t)layer;
+    out[2 * j + 1] = (int16_t)e;
+    if (e == L) {
+      prev = -1;
+      layer = 0;
+    } else {
+      prev = j;
+      layer = e;
+    }
+  }
+}
+}  // namespace gen
+
+// rows [first, first + n) of the workload into out[n][N][2]; walk != 0 draws
+// link walks.  Returns 0.
+int refh_generate(void* cp, uint64_t seed, int64_t first, int64_t n, uint32_t ppm, int walk, int nthreads,
+                  int16_t* out) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  const int N = static_cast<int>(c.nodes.size());
+  const int L = c.model.num_layers;
+  std::vector<int> kmax(N);
+  for (int k = 0; k < N; ++k) kmax[k] = c.max_layers(c.nodes[k]);
+  // declared links, first occurrence of each (src, dst) pair; undeclared
+  // endpoints, coordinator loops and self-links never carry flow
+  std::vector<std::vector<int>> succ(N + 1);
+  std::vector<std::vector<char>> seen(N + 1, std::vector<char>(N, 0));
+  for (const LinkSpec& l : c.links) {
+    const int a = l.src == c.coordinator_id ? -1 : c.node_index(l.src);
+    const int b = l.dst == c.coordinator_id ? -1 : c.node_index(l.dst);
+    if ((a < 0 && l.src != c.coordinator_id) || b < 0 || a == b) continue;
+    if (!seen[a + 1][b]) {
+      seen[a + 1][b] = 1;
+      succ[a + 1].push_back(b);
+    }
+  }
+  if (nthreads < 1) nthreads = 1;
+  auto work = [&](int64_t lo, int64_t hi) {
+    for (int64_t r = lo; r < hi; ++r) {
+      int16_t* o = out + r * 2 * N;
+      if (walk)
+        gen::walk(kmax, L, seed, (uint64_t)(first + r), succ, o);
+      else
+        gen::chain(kmax, L, seed, (uint64_t)(first + r), ppm, o);
+    }
+  };
+  std::vector<std::thread> pool;
+  const int64_t chunk = (n + nthreads - 1) / nthreads;
+  for (int t = 0; t < nthreads; ++t) {
+    int64_t lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo >= hi) break;
+    pool.emplace_back(work, lo, hi);
+  }
+  for (auto& th : pool) th.join();
+  return 0;
 }
 
 double refh_maxflow_raw(int n, int s, int t, int m, const int32_t* u, const int32_t* v,

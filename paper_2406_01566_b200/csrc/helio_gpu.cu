@@ -438,7 +438,6 @@ void launch_score_mode(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t
   const int grid = (int)std::min<int64_t>(ctx->small_blocks[MODE], (B + warps - 1) / warps);
   score_kernel<MODE><<<grid, 32 * warps, sl.bytes * warps, st>>>(ctx->cd, sl, d_pl, B, partial, d_val, d_st, work,
                                                                  l1, l2, oc, 0, fo);
-  if (timed) cudaEventRecord(ctx->ev1, st);
   // graphs that overflowed the small slot: the same kernel with the middle
   // slot, then whatever overflows that with the big slot (one warp per CTA)
   const Layout& bl = ctx->slot_big_ok[MODE] ? ctx->slot_big[MODE] : sl;
@@ -454,6 +453,8 @@ void launch_score_mode(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t
     score_kernel<MODE><<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
                                                                      work + 2, l1, nullptr, oc, 1, fo);
   }
+  // kernel time = all tier launches (small, middle, big)
+  if (timed) cudaEventRecord(ctx->ev1, st);
 }
 
 int launch_score(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, int partial,

@@ -1,16 +1,18 @@
 """Multi-rank plumbing for candidate sharding (one process per GPU).
 
-The path partitions: rank r owns global candidate indices [r*B, (r+1)*B)
-(weak scaling) and needs no input exchange.  The only collective is the
-argmax: each rank's 16-byte record (value bits, global index) is all-gathered
-and reduced deterministically — max value, then min index — which reproduces
-the strict first-wins `v > best` of tests/oracles/enumerate.hpp:59 over the
-global enumeration order.
+The path partitions: every candidate is independent, so a rank scores a
+contiguous range of global candidate indices and needs no input exchange.
+Strong scaling splits a global batch G as [r*G/N, (r+1)*G/N); weak scaling
+gives every rank its own `per_rank` candidates [r*B, (r+1)*B).  The only
+collective is the argmax: each rank's 16-byte record (value bits, global index)
+is all-gathered and reduced deterministically — max value, then min index —
+which reproduces the strict first-wins `v > best` of
+tests/oracles/enumerate.hpp:59 over the global enumeration order.
 """
 
 from __future__ import annotations
 
-from typing import List, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -18,6 +20,24 @@ import numpy as np
 def shard_range(per_rank: int, rank: int) -> Tuple[int, int]:
     """Global index range of `rank` under weak scaling."""
     return rank * per_rank, (rank + 1) * per_rank
+
+
+def strong_range(total: int, world: int, rank: int) -> Tuple[int, int]:
+    """Global index range of `rank` when `total` candidates are split over
+    `world` ranks (strong scaling; sizes differ by at most one)."""
+    return rank * total // world, (rank + 1) * total // world
+
+
+def owner_of(index: int, starts: Sequence[int]) -> int:
+    """The rank whose range holds global `index`, given every rank's first
+    index (ascending); -1 for a negative index (no valid candidate)."""
+    if index < 0:
+        return -1
+    owner = 0
+    for r, s in enumerate(starts):
+        if s <= index:
+            owner = r
+    return owner
 
 
 def reduce_best(records: Sequence[Tuple[float, int]]) -> Tuple[float, int]:
@@ -31,13 +51,12 @@ def reduce_best(records: Sequence[Tuple[float, int]]) -> Tuple[float, int]:
     return best_v, best_i
 
 
-def pack_record(value: float, index: int):
-    """16-byte int64 pair: float64 bits + global index."""
+def pack_record(value: float, index: int, device=None):
+    """16-byte int64 pair: float64 bits + global index, on `device` (the
+    backend's device: CUDA for NCCL, CPU for gloo)."""
     import torch
-    rec = torch.empty(2, dtype=torch.int64)
-    rec[0] = int(np.array([value], np.float64).view(np.int64)[0])
-    rec[1] = index
-    return rec
+    rec = torch.tensor([int(np.array([value], np.float64).view(np.int64)[0]), int(index)], dtype=torch.int64)
+    return rec if device is None else rec.to(device)
 
 
 def unpack_records(gathered) -> List[Tuple[float, int]]:
@@ -47,7 +66,7 @@ def unpack_records(gathered) -> List[Tuple[float, int]]:
 
 def gather_best(rec, world: int, group=None) -> Tuple[float, int]:
     """All-gather each rank's packed record (a 2-element int64 tensor on the
-    backend's device) and reduce it identically on every rank."""
+    backend's device, see pack_record) and reduce it identically on every rank."""
     import torch
     import torch.distributed as dist
     out = torch.empty(2 * world, dtype=torch.int64, device=rec.device)
@@ -55,29 +74,35 @@ def gather_best(rec, world: int, group=None) -> Tuple[float, int]:
     return reduce_best(unpack_records(out))
 
 
-def share_winner(index: int, per_rank: int, row=None, flows=None, group=None):
-    """after the argmax, the rank that owns global
-    candidate `index` broadcasts the winning placement row (int16 [N][2]) and
-    its PARITY per-edge flows (float64 [E], reference edge order) so that every
-    rank can materialise the plan and route without re-scoring.  `row` and
-    `flows` are read on the owner only.  -> (row int16 [N][2], flows float64 [E])
-    on every rank, as CPU numpy arrays."""
+def share_winner(owner: int, row=None, flows=None, n_nodes: Optional[int] = None, group=None):
+    """after the argmax, rank `owner` (a rank within
+    `group`; see owner_of) broadcasts the winning placement row (int16 [N][2])
+    and its PARITY per-edge flows (float64 [E], reference edge order) so that
+    every rank can materialise the plan and route without re-scoring.  `row`
+    and `flows` are read on the owner only.  -> (row int16 [N][2], flows
+    float64 [E]) on every rank, as CPU numpy arrays; None when owner < 0 (no
+    valid candidate anywhere)."""
     import torch
     import torch.distributed as dist
-    owner = index // per_rank
+    if owner < 0:
+        return None
     me = dist.get_rank(group)
+    src = owner if group is None else dist.get_global_rank(group, owner)
     dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
     meta = torch.zeros(2, dtype=torch.int64, device=dev)
     if me == owner:
         meta[0] = int(np.asarray(row).size)
         meta[1] = int(np.asarray(flows).size)
-    dist.broadcast(meta, src=owner, group=group)
+    dist.broadcast(meta, src=src, group=group)
     nr, ne = int(meta[0]), int(meta[1])
     r = torch.zeros(nr, dtype=torch.int32, device=dev)  # gloo has no int16 collectives
     f = torch.zeros(ne, dtype=torch.float64, device=dev)
     if me == owner:
         r.copy_(torch.from_numpy(np.ascontiguousarray(row, np.int32).reshape(-1)))
         f.copy_(torch.from_numpy(np.ascontiguousarray(flows, np.float64).reshape(-1)))
-    dist.broadcast(r, src=owner, group=group)
-    dist.broadcast(f, src=owner, group=group)
-    return r.cpu().numpy().astype(np.int16).reshape(-1, 2), f.cpu().numpy()
+    dist.broadcast(r, src=src, group=group)
+    dist.broadcast(f, src=src, group=group)
+    out_row = r.cpu().numpy().astype(np.int16).reshape(-1, 2)
+    if n_nodes is not None and out_row.shape[0] != n_nodes:
+        raise ValueError(f"broadcast row has {out_row.shape[0]} nodes, expected {n_nodes}")
+    return out_row, f.cpu().numpy()

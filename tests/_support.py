@@ -231,8 +231,12 @@ def ref():
         lib.refh_graph.restype = C.c_int
         lib.refh_score.argtypes = [C.c_void_p, _i16p, C.c_int64, C.c_int, C.c_int, _f64p, _i32p]
         lib.refh_score.restype = C.c_int
-        lib.refh_solve_only.argtypes = [C.c_void_p, _i16p, C.c_int64, C.c_int]
-        lib.refh_solve_only.restype = C.c_double
+        lib.refh_solve_only.argtypes = [C.c_void_p, _i16p, C.c_int64, C.c_int, C.c_int,
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        lib.refh_solve_only.restype = C.c_int64
+        lib.refh_generate.argtypes = [C.c_void_p, C.c_uint64, C.c_int64, C.c_int64, C.c_uint32, C.c_int,
+                                      C.c_int, _i16p]
+        lib.refh_generate.restype = C.c_int
         lib.refh_maxflow_raw.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _i32p, _i32p, _f64p, _f64p]
         lib.refh_maxflow_raw.restype = C.c_double
         lib.refh_ac1_graphs.argtypes = [C.c_uint64, C.c_int, _i32p, _i32p, _i32p, _i32p, _i32p, _f64p,
@@ -283,6 +287,13 @@ class RefCluster:
         s = np.zeros(B, np.int32)
         self.lib.refh_score(self.h, rows, B, int(partial), threads, v, s)
         return v, s
+
+    def generate(self, seed, first, n, ppm=0, walk=False, threads=1):
+        """bench.py's workload rows G(seed, i) restated over the reference's
+        ClusterSpec (refh_generate; the reference arm's input generator)."""
+        out = np.zeros((n, self.N, 2), np.int16)
+        self.lib.refh_generate(self.h, seed, first, n, ppm, int(walk), threads, out)
+        return out
 
     def graph(self, row, partial=True):
         row = np.ascontiguousarray(row, np.int16)

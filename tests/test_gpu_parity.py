@@ -327,6 +327,9 @@ def test_walk_generator_device_matches_host_and_syn256_walk_parity():
     torch.cuda.synchronize()
     rows = e.generate_walk_host(7, 100, B)
     assert np.array_equal(out.cpu().numpy(), rows)
+    from _support import RefCluster, ref_available
+    if ref_available():  # bench.py's reference arm draws the same walks over the reference's ClusterSpec
+        assert np.array_equal(RefCluster(d).generate(7, 100, B, 0, True, 4), rows)
     o = Oracle(d)
     sub = rows[:150]
     vo, so = o.score(sub)

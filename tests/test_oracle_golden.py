@@ -115,3 +115,23 @@ def test_host_generator_matches_fixture_generator():
             assert np.array_equal(a, b)
         n0 = len(z["rows"]) - 0
         assert np.array_equal(generate_host(k, L, seed, 0, 8, 0), z["rows"][:8])
+
+
+@pytest.mark.parametrize("config", ["het42-70b", "single24-30b", "geo24"])
+def test_reference_arm_generator_matches_product_generator(config):
+    """bench.py --impl reference draws its rows with refh_generate (over the
+    reference's ClusterSpec) so it loads nothing from the package: the rows must
+    be the product generator's (csrc/gen.h) exactly, chains and uniform mixes."""
+    from paper_2406_01566_b200 import clusters, generate_host
+    from _support import RefCluster, ref_available
+
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    d = clusters.CONFIGS[config]("float")
+    rc = RefCluster(d)
+    k = [int(rc.lib.refh_max_layers(rc.h, i)) for i in range(rc.N)]
+    L = int(d["model"]["num_layers"])
+    for first, ppm, threads in ((0, 0, 1), (123456, 100000, 4), (10**9, 0, 3)):
+        a = generate_host(k, L, 20240611, first, 257, ppm)
+        b = rc.generate(20240611, first, 257, ppm, False, threads)
+        assert np.array_equal(a, b)
