@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -125,6 +126,19 @@ struct helio_gpu_ctx {
   const int32_t* d_walk_list = nullptr;
   std::vector<int32_t> h_walk_beg, h_walk_list;
 
+  // Ordering of the shared device-pointer scratch (set kApiSet, the argmax
+  // row kSets, the split pipeline's counters) across caller streams: the host
+  // mutex only serialises enqueue, so every use makes its stream wait for the
+  // previous use's completion event and then records its own (api_begin/end).
+  cudaEvent_t api_ev = nullptr;
+  bool api_ev_used = false;
+
+  // grow-only device scratch of the synchronous host entries (flows_host,
+  // maxflow_raw_host): carved per call, so the per-call path makes no
+  // cudaMalloc/cudaFree (cudaFree synchronises the whole device)
+  void* d_host_arena = nullptr;
+  size_t host_arena_cap = 0;
+
   // routing arena (route.cu), grows only
   void* d_route = nullptr;
   size_t route_cap = 0;
@@ -144,5 +158,43 @@ inline int fail(helio_gpu_ctx* c, int code, const std::string& msg) {
     if (e_ != cudaSuccess)                                                         \
       return fail(ctx, HELIO_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
+
+// Carves typed, 256-byte aligned pieces out of one allocation.  With base ==
+// nullptr it only measures (pass 1), then the same sequence is replayed on the
+// real base (pass 2).
+struct Carve {
+  char* base = nullptr;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* r = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += sizeof(T) * (n ? n : 1);
+    return r;
+  }
+};
+
+// The host-entry arena (helio_gpu_ctx::d_host_arena) with at least `bytes`.
+inline int host_arena(helio_gpu_ctx* ctx, size_t bytes, char** out) {
+  if (ctx->host_arena_cap < bytes) {
+    cudaFree(ctx->d_host_arena);
+    ctx->d_host_arena = nullptr;
+    ctx->host_arena_cap = 0;
+    const size_t cap = std::max<size_t>(bytes + bytes / 4, size_t(1) << 20);
+    CK(cudaMalloc(&ctx->d_host_arena, cap));
+    ctx->host_arena_cap = cap;
+  }
+  *out = static_cast<char*>(ctx->d_host_arena);
+  return HELIO_OK;
+}
+
+// See helio_gpu_ctx::api_ev.
+inline cudaError_t api_begin(helio_gpu_ctx* c, cudaStream_t st) {
+  return c->api_ev_used ? cudaStreamWaitEvent(st, c->api_ev, 0) : cudaSuccess;
+}
+inline cudaError_t api_end(helio_gpu_ctx* c, cudaStream_t st) {
+  c->api_ev_used = true;
+  return cudaEventRecord(c->api_ev, st);
+}
 
 }  // namespace helio_engine

@@ -480,20 +480,35 @@ int launch_score(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, in
 int helio_engine_score_parity(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int partial, double* d_val,
                               int32_t* d_st, cudaStream_t st) {
   FlowOut fo{nullptr, nullptr, nullptr, 0};
-  return launch_score(ctx, helio_gpu_ctx::kApiSet, d_pl, B, partial, d_val, d_st, st, fo, false, HELIO_MODE_PARITY);
+  CK(api_begin(ctx, st));
+  const int rc =
+      launch_score(ctx, helio_gpu_ctx::kApiSet, d_pl, B, partial, d_val, d_st, st, fo, false, HELIO_MODE_PARITY);
+  CK(api_end(ctx, st));
+  return rc;
 }
 
 namespace {
 
 int ensure_stage(helio_gpu_ctx* ctx, int64_t chunk) {
   if (ctx->stage_cap >= chunk) return HELIO_OK;
+  // every set is released (and nulled, cap 0) before any reallocation, so a
+  // failed allocation leaves no dangling pointer behind
   for (int i = 0; i < helio_gpu_ctx::kPipeSets; ++i) {
-    if (ctx->d_pl[i]) cudaFree(ctx->d_pl[i]);
-    if (ctx->d_val[i]) cudaFree(ctx->d_val[i]);
-    if (ctx->d_st[i]) cudaFree(ctx->d_st[i]);
-    if (ctx->h_pl_pin[i]) cudaFreeHost(ctx->h_pl_pin[i]);
-    if (ctx->h_val_pin[i]) cudaFreeHost(ctx->h_val_pin[i]);
-    if (ctx->h_st_pin[i]) cudaFreeHost(ctx->h_st_pin[i]);
+    cudaFree(ctx->d_pl[i]);
+    cudaFree(ctx->d_val[i]);
+    cudaFree(ctx->d_st[i]);
+    cudaFreeHost(ctx->h_pl_pin[i]);
+    cudaFreeHost(ctx->h_val_pin[i]);
+    cudaFreeHost(ctx->h_st_pin[i]);
+    ctx->d_pl[i] = nullptr;
+    ctx->d_val[i] = nullptr;
+    ctx->d_st[i] = nullptr;
+    ctx->h_pl_pin[i] = nullptr;
+    ctx->h_val_pin[i] = nullptr;
+    ctx->h_st_pin[i] = nullptr;
+  }
+  ctx->stage_cap = 0;
+  for (int i = 0; i < helio_gpu_ctx::kPipeSets; ++i) {
     CK(cudaMalloc(&ctx->d_pl[i], sizeof(int16_t) * 2 * ctx->N * chunk));
     CK(cudaMalloc(&ctx->d_val[i], sizeof(double) * chunk));
     CK(cudaMalloc(&ctx->d_st[i], sizeof(int32_t) * chunk));
@@ -543,6 +558,7 @@ int helio_gpu_create(int device, helio_gpu_ctx** out) {
       cudaStreamCreateWithFlags(&ctx->pipe[2], cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->api_ev, cudaEventDisableTiming) != cudaSuccess ||
       cudaMalloc(&ctx->d_work, 32 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMalloc(&ctx->d_ovf_count, 2 * helio_gpu_ctx::kSets * sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc(&ctx->d_pv, (helio_gpu_ctx::kSets + 1) * 4096 * sizeof(double)) != cudaSuccess ||
@@ -594,8 +610,10 @@ void helio_gpu_destroy(helio_gpu_ctx* ctx) {
   cudaFree(ctx->d_best);
   cudaFree(ctx->d_bidx);
   cudaFree(ctx->d_route);
+  cudaFree(ctx->d_host_arena);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->api_ev) cudaEventDestroy(ctx->api_ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -895,8 +913,11 @@ int helio_gpu_score(helio_gpu_ctx* ctx, const int16_t* d_pl, int64_t B, int allo
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   FlowOut fo{nullptr, nullptr, nullptr, 0};
-  return launch_score(ctx, helio_gpu_ctx::kApiSet, d_pl, B, allow_partial ? 1 : 0, d_values, d_status, st, fo, true,
-                      ctx->mode);
+  CK(api_begin(ctx, st));
+  const int rc = launch_score(ctx, helio_gpu_ctx::kApiSet, d_pl, B, allow_partial ? 1 : 0, d_values, d_status, st,
+                              fo, true, ctx->mode);
+  CK(api_end(ctx, st));
+  return rc;
 }
 
 }  // extern "C"
@@ -1112,36 +1133,41 @@ int helio_gpu_flows_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t K, int
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
   const size_t row = sizeof(int16_t) * 2 * ctx->N;
-  int16_t* d_pl = nullptr;
-  double* d_val = nullptr;
-  int32_t *d_st = nullptr, *d_nv = nullptr, *d_ne = nullptr;
-  helio_edge* d_ed = nullptr;
-  int rc = HELIO_OK;
-  const size_t edge_bytes = sizeof(helio_edge) * (size_t)K * std::max(max_edges, 1);
-  if (cudaMalloc(&d_pl, row * K) != cudaSuccess || cudaMalloc(&d_val, 8 * K) != cudaSuccess ||
-      cudaMalloc(&d_st, 4 * K) != cudaSuccess || cudaMalloc(&d_nv, 4 * K) != cudaSuccess ||
-      cudaMalloc(&d_ne, 4 * K) != cudaSuccess || cudaMalloc(&d_ed, edge_bytes) != cudaSuccess) {
-    rc = fail(ctx, HELIO_ERR_CUDA, "cudaMalloc failed in flows");
-  }
-  if (!rc && cudaMemcpyAsync(d_pl, h_pl, row * K, cudaMemcpyHostToDevice, st) != cudaSuccess)
-    rc = fail(ctx, HELIO_ERR_CUDA, "H2D failed in flows");
-  if (!rc) {
-    FlowOut fo{d_ed, d_nv, d_ne, max_edges};
-    rc = launch_score(ctx, helio_gpu_ctx::kApiSet, d_pl, K, allow_partial ? 1 : 0, d_val, d_st, st, fo, false,
-                      HELIO_MODE_PARITY);
-  }
-  if (!rc) {
-    bool ok = cudaMemcpyAsync(h_values, d_val, 8 * K, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-              cudaMemcpyAsync(h_status, d_st, 4 * K, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-              cudaMemcpyAsync(h_nv, d_nv, 4 * K, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-              cudaMemcpyAsync(h_ne, d_ne, 4 * K, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-              (max_edges == 0 || cudaMemcpyAsync(h_edges, d_ed, sizeof(helio_edge) * (size_t)K * max_edges,
-                                                 cudaMemcpyDeviceToHost, st) == cudaSuccess) &&
-              cudaStreamSynchronize(st) == cudaSuccess;
-    if (!ok) rc = fail(ctx, HELIO_ERR_CUDA, std::string("flows: ") + cudaGetErrorString(cudaGetLastError()));
-  }
-  cudaFree(d_pl); cudaFree(d_val); cudaFree(d_st); cudaFree(d_nv); cudaFree(d_ne); cudaFree(d_ed);
-  return rc;
+  const size_t ne_alloc = (size_t)K * std::max(max_edges, 1);
+  auto carve = [&](Carve& c, int16_t*& pl, double*& val, int32_t*& sts, int32_t*& nv, int32_t*& ne,
+                   helio_edge*& ed) {
+    pl = c.take<int16_t>(2 * ctx->N * (size_t)K);
+    val = c.take<double>(K);
+    sts = c.take<int32_t>(K);
+    nv = c.take<int32_t>(K);
+    ne = c.take<int32_t>(K);
+    ed = c.take<helio_edge>(ne_alloc);
+  };
+  int16_t* d_pl;
+  double* d_val;
+  int32_t *d_st, *d_nv, *d_ne;
+  helio_edge* d_ed;
+  Carve measure;
+  carve(measure, d_pl, d_val, d_st, d_nv, d_ne, d_ed);
+  Carve c;
+  int rc = host_arena(ctx, measure.off, &c.base);
+  if (rc) return rc;
+  carve(c, d_pl, d_val, d_st, d_nv, d_ne, d_ed);
+  CK(api_begin(ctx, st));
+  CK(cudaMemcpyAsync(d_pl, h_pl, row * K, cudaMemcpyHostToDevice, st));
+  FlowOut fo{d_ed, d_nv, d_ne, max_edges};
+  rc = launch_score(ctx, helio_gpu_ctx::kApiSet, d_pl, K, allow_partial ? 1 : 0, d_val, d_st, st, fo, false,
+                    HELIO_MODE_PARITY);
+  CK(api_end(ctx, st));
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(h_values, d_val, 8 * K, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_status, d_st, 4 * K, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_nv, d_nv, 4 * K, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_ne, d_ne, 4 * K, cudaMemcpyDeviceToHost, st));
+  if (max_edges > 0)
+    CK(cudaMemcpyAsync(h_edges, d_ed, sizeof(helio_edge) * (size_t)K * max_edges, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return HELIO_OK;
 }
 
 int helio_gpu_maxflow_raw_host(helio_gpu_ctx* ctx, int64_t G, const int32_t* h_n, const int32_t* h_s,
@@ -1182,19 +1208,30 @@ int helio_gpu_maxflow_raw_host(helio_gpu_ctx* ctx, int64_t G, const int32_t* h_n
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raw_kernel, 32 * warps, lay.bytes * warps));
   if (per_sm < 1) per_sm = 1;
   cudaStream_t st = ctx->stream;
-  int32_t *d_n, *d_s, *d_t, *d_u = nullptr, *d_v = nullptr;
-  int64_t* d_off;
-  double *d_cap = nullptr, *d_val, *d_fl = nullptr;
   const int64_t Ea = std::max<int64_t>(Etot, 1);
-  CK(cudaMalloc(&d_n, 4 * G));
-  CK(cudaMalloc(&d_s, 4 * G));
-  CK(cudaMalloc(&d_t, 4 * G));
-  CK(cudaMalloc(&d_off, 8 * (G + 1)));
-  CK(cudaMalloc(&d_u, 4 * Ea));
-  CK(cudaMalloc(&d_v, 4 * Ea));
-  CK(cudaMalloc(&d_cap, 8 * Ea));
-  CK(cudaMalloc(&d_val, 8 * G));
-  if (h_flows) CK(cudaMalloc(&d_fl, 8 * Ea));
+  auto carve = [&](Carve& c, int32_t*& n, int32_t*& s, int32_t*& t, int64_t*& off, int32_t*& u, int32_t*& v,
+                   double*& cap, double*& val, double*& fl) {
+    n = c.take<int32_t>(G);
+    s = c.take<int32_t>(G);
+    t = c.take<int32_t>(G);
+    off = c.take<int64_t>(G + 1);
+    u = c.take<int32_t>(Ea);
+    v = c.take<int32_t>(Ea);
+    cap = c.take<double>(Ea);
+    val = c.take<double>(G);
+    fl = c.take<double>(h_flows ? Ea : 1);
+  };
+  int32_t *d_n, *d_s, *d_t, *d_u, *d_v;
+  int64_t* d_off;
+  double *d_cap, *d_val, *d_fl;
+  Carve measure;
+  carve(measure, d_n, d_s, d_t, d_off, d_u, d_v, d_cap, d_val, d_fl);
+  Carve c;
+  int rc = host_arena(ctx, measure.off, &c.base);
+  if (rc) return rc;
+  carve(c, d_n, d_s, d_t, d_off, d_u, d_v, d_cap, d_val, d_fl);
+  if (!h_flows) d_fl = nullptr;
+  CK(api_begin(ctx, st));
   CK(cudaMemcpyAsync(d_n, h_n, 4 * G, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_s, h_s, 4 * G, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_t, h_t, 4 * G, cudaMemcpyHostToDevice, st));
@@ -1209,12 +1246,11 @@ int helio_gpu_maxflow_raw_host(helio_gpu_ctx* ctx, int64_t G, const int32_t* h_n
   raw_kernel<<<grid, 32 * warps, lay.bytes * warps, st>>>(lay, G, d_n, d_s, d_t, d_off, d_u, d_v, d_cap,
                                                            d_val, d_fl, ctx->d_work);
   CK(cudaGetLastError());
+  CK(api_end(ctx, st));
   ctx->launches++;
   CK(cudaMemcpyAsync(h_values, d_val, 8 * G, cudaMemcpyDeviceToHost, st));
   if (h_flows && Etot > 0) CK(cudaMemcpyAsync(h_flows, d_fl, 8 * Etot, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  cudaFree(d_n); cudaFree(d_s); cudaFree(d_t); cudaFree(d_off); cudaFree(d_u); cudaFree(d_v);
-  cudaFree(d_cap); cudaFree(d_val); cudaFree(d_fl);
   return HELIO_OK;
 }
 
@@ -1243,7 +1279,10 @@ int helio_gpu_argmax(helio_gpu_ctx* ctx, const double* d_values, const int32_t* 
   if (!d_best || !d_index || (B > 0 && (!d_values || !d_status))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-  return argmax_on(ctx, helio_gpu_ctx::kSets, d_values, d_status, B, index_base, d_best, d_index, st);
+  CK(api_begin(ctx, st));
+  const int rc = argmax_on(ctx, helio_gpu_ctx::kSets, d_values, d_status, B, index_base, d_best, d_index, st);
+  CK(api_end(ctx, st));
+  return rc;
 }
 
 int helio_gpu_generate(helio_gpu_ctx* ctx, uint64_t seed, int64_t first, int64_t B, uint32_t ppm,

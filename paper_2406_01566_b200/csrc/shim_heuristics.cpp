@@ -188,6 +188,12 @@ LocalSearchResult sampled_search_placement(const ClusterSpec& c, const Placement
   LocalSearchResult r = local_search_placement(c, mid, allow_partial);
   r.moves += a.moves + improvements;
   r.scored += a.scored + scored;
+  // the middle phase accepts SCORE-mode moves, which on float capacities can
+  // be rounding noise: never return less than the first PARITY local optimum
+  if (r.value < a.value) {
+    r.placement = a.placement;
+    r.value = a.value;
+  }
   return r;
 }
 

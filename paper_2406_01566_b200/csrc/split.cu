@@ -189,10 +189,12 @@ extern "C" int helio_gpu_build_csr(helio_gpu_ctx* ctx, const int16_t* d_pl, int6
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_build_kernel, 32 * warps, smem));
   const int grid = (int)std::min<int64_t>((int64_t)std::max(per_sm, 1) * ctx->sm_count, (B + warps - 1) / warps);
+  CK(api_begin(ctx, st));
   CK(cudaMemsetAsync(ctx->d_work + 8, 0, sizeof(unsigned long long), st));
   csr_build_kernel<<<grid, 32 * warps, smem, st>>>(ctx->cd, ctx->small, sl, d_pl, B, allow_partial ? 1 : 0,
                                                    static_cast<char*>(d_slabs), d_status, ctx->d_work + 8);
   CK(cudaGetLastError());
+  CK(api_end(ctx, st));
   ctx->launches++;
   return HELIO_OK;
 }
@@ -214,10 +216,12 @@ extern "C" int helio_gpu_solve_csr(helio_gpu_ctx* ctx, const void* d_slabs, int6
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_solve_kernel, 32 * warps, smem));
   const int grid = (int)std::min<int64_t>((int64_t)std::max(per_sm, 1) * ctx->sm_count, (B + warps - 1) / warps);
+  CK(api_begin(ctx, st));
   CK(cudaMemsetAsync(ctx->d_work + 9, 0, sizeof(unsigned long long), st));
   csr_solve_kernel<<<grid, 32 * warps, smem, st>>>(ctx->small, sl, static_cast<const char*>(d_slabs), B, d_values,
                                                    d_status, ctx->d_work + 9);
   CK(cudaGetLastError());
+  CK(api_end(ctx, st));
   ctx->launches++;
   return HELIO_OK;
 }

@@ -388,6 +388,37 @@ def test_concurrent_callers_on_one_engine():
     assert len({obj for _, obj in got}) == 1
 
 
+def test_device_scoring_on_two_streams_shares_no_scratch():
+    # score_device calls on different caller streams must not
+    # overlap on the context's shared scratch (work counters, overflow lists)
+    import torch
+    c, e = engine("het42-70b_float")
+    B = 200_000
+    pl = [torch.empty((B, e.num_nodes, 2), dtype=torch.int16, device="cuda") for _ in range(2)]
+    for i in range(2):
+        e.generate_device(77 + i, 0, B, 0, pl[i].data_ptr(), 0)
+    torch.cuda.synchronize()
+    want = []
+    for i in range(2):
+        v = torch.empty(B, dtype=torch.float64, device="cuda")
+        s = torch.empty(B, dtype=torch.int32, device="cuda")
+        e.score_device(pl[i].data_ptr(), B, v.data_ptr(), s.data_ptr(), True, 0)
+        torch.cuda.synchronize()
+        want.append((v.clone(), s.clone()))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for rep in range(3):
+        outs = []
+        for i in range(2):
+            v = torch.full((B,), -1.0, dtype=torch.float64, device="cuda")
+            s = torch.full((B,), -1, dtype=torch.int32, device="cuda")
+            torch.cuda.synchronize()
+            e.score_device(pl[i].data_ptr(), B, v.data_ptr(), s.data_ptr(), True, streams[i].cuda_stream)
+            outs.append((v, s))
+        torch.cuda.synchronize()
+        for (v, s), (wv, ws) in zip(outs, want):
+            assert torch.equal(v.view(torch.int64), wv.view(torch.int64)) and torch.equal(s, ws)
+
+
 # --- solver-boundary sweep: V = 2N + 2 crosses the bitset solver's word counts
 # (32 / 64 / 96 / 128 vertices), the N <= 64 cover-mask builders and the
 # general per-node-list builder --------------------------------------------------

@@ -174,6 +174,21 @@ def test_plan_sampled_at_least_local():
 
 
 @pytest.mark.gpu
+def test_plan_search_on_syn256_scores_moves_in_score_mode_and_returns_parity_values():
+    """Clusters above 64 nodes score search moves in SCORE mode and re-solve
+    the result in PARITY (shim_heuristics.cpp): the objective is the
+    reference-exact max-flow of the returned placement and never below a seed."""
+    c = _cluster(clusters.CONFIGS["syn256-120l"]())
+    seeds = {m: h.plan(c, m).objective for m in ("swarm", "petals")}
+    p = h.plan(c, "local")
+    assert p.objective == h.max_flow_value(c, p.placement)
+    assert all(p.objective >= v for v in seeds.values())
+    q = h.plan(c, "sampled")
+    assert q.objective == h.max_flow_value(c, q.placement)
+    assert q.objective >= p.objective
+
+
+@pytest.mark.gpu
 def test_local_search_rejects_invalid_seed():
     d = clusters.CONFIGS["geo24"]()
     c = _cluster(d)
