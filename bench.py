@@ -324,7 +324,7 @@ def routing_leg(h, clusters, dev, sp, requests, with_reference):
     torch.cuda.synchronize(pl.device)
     row = pl[int(bi.item())].cpu().numpy()
     pe, pf, obj = e.plan_edges(row)
-    _, inl, outl = h.generate_trace(requests, 0.0, "offline", 7)
+    _, inl, outl = h.generate_trace_arrays(requests, 0.0, "offline", 7)
     e.route(row, pe, pf, inl[:1000], outl[:1000], 0, False)  # warm-up
     times = []
     for _ in range(3):
@@ -339,6 +339,17 @@ def routing_leg(h, clusters, dev, sp, requests, with_reference):
            "requests": requests, "value": rate, "unit": "routes/s",
            "timing": "host wall clock around helio_gpu_route_host (H2D lengths, kernels, D2H hop nodes)",
            "hops_mean": float(nh[nh > 0].mean()), "deferred": int(den), "plan_edges": int(len(pf))}
+    # the stateful drop-in (Scheduler::admit / complete, one call per request,
+    # picks from device-built IWRR cycles): per-admit latency in the same order
+    try:
+        placement = {c.node_ids[k]: (int(row[k, 0]), int(row[k, 1])) for k in range(len(row)) if row[k, 1] > row[k, 0]}
+        sched = h.Scheduler(c, h.plan_for_placement(c, placement), "iwrr", 7)
+        snh, secs = sched.run_ac8(inl, outl)
+        out["stateful"] = {"value": requests / secs, "unit": "routes/s", "per_admit_us": secs / requests * 1e6,
+                           "call": "Scheduler.admit + complete per request (AC8 order), host-timed without Python",
+                           "identical_to_batch": bool(np.array_equal(snh, nh))}
+    except Exception as ex:  # reported, never fatal
+        out["stateful"] = {"error": str(ex)}
     if with_reference:
         try:
             sys.path.insert(0, os.path.join(ROOT, "tests"))

@@ -264,6 +264,21 @@ int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_placement,
 /* iwrr_weights (scheduler.cpp:46-56) of one candidate list, on the device. */
 int helio_gpu_iwrr_weights(helio_gpu_ctx* ctx, const double* h_flows, int32_t n, int64_t* h_weights);
 
+/* IWRR cycles of `nlists` candidate lists (list l = entries [h_off[l],
+ * h_off[l+1]) of the flattened arrays): with h_flows != NULL the weights are
+ * iwrr_weights(flows) (scheduler.cpp:46-56) and written to h_weights; with
+ * h_flows == NULL h_weights is read as the caller's weights (the IwrrPicker
+ * constructor, scheduler.cpp:24-26).  List l's cycle — the (round, index)
+ * slots with w_i >= round in the order IwrrPicker::next visits them
+ * (scheduler.cpp:28-44) — is written to h_cycles[h_cyc_off[l] ...] as
+ * candidate indices, its length (sum of the weights) to h_cyc_len[l].  Slot
+ * ranges must hold the cycle (32 * list size always does for flow weights).
+ * The k-th unmasked IwrrPicker::next call of a fresh picker returns
+ * cycle[k mod length]. */
+int helio_gpu_iwrr_cycles(helio_gpu_ctx* ctx, int32_t nlists, const int32_t* h_off, const double* h_flows,
+                          int64_t* h_weights, const int64_t* h_cyc_off, int32_t* h_cycles,
+                          int64_t* h_cyc_len);
+
 /* IwrrPicker::next (scheduler.cpp:28-44) `calls` times on the device.  The
  * picker state (round, idx) is read from and written back to *h_round/*h_idx
  * (a fresh picker is round 1, idx 0).  h_masks holds, per call, ceil(n/64)

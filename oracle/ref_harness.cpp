@@ -33,7 +33,9 @@
 #include "helio/placement.hpp"
 #include "helio/rng.hpp"
 #include "helio/scheduler.hpp"
+#include "helio/sim.hpp"
 #include "helio/workload.hpp"
+#include "json.hpp"
 #include "oracles/enumerate.hpp"
 #include "oracles/random_cluster.hpp"
 
@@ -542,6 +544,168 @@ int refh_heuristic(void* cp, int method, int16_t* row, char* warn, int warnlen) 
   } catch (const std::exception& e) {
     set_err(warn, warnlen, e.what());
     return -1;
+  }
+}
+
+// --- plan / report formats, stateful scheduler, simulator, pruning ------------
+
+namespace {
+int put_text(const std::string& s, char* buf, int buflen) {
+  if (static_cast<int>(s.size()) + 1 > buflen) return -static_cast<int>(s.size() + 1);
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
+}
+}  // namespace
+
+// serialize_plan(plan_from_placement(c, row)) (placement.cpp:459-469, :603-625).
+int refh_plan_json(void* cp, const int16_t* pl, int allow_partial, const char* method, char* buf, int buflen) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  try {
+    return put_text(serialize_plan(plan_from_placement(c, to_placement(c, pl), allow_partial != 0, method)), buf,
+                    buflen);
+  } catch (const std::exception& e) {
+    set_err(buf, buflen, e.what());
+    return -1000000000;
+  }
+}
+
+// serialize_plan(parse_plan(text)) (placement.cpp:603-658): the reference
+// reading a plan written elsewhere and writing it back.
+int refh_plan_roundtrip(const char* text, char* buf, int buflen) {
+  try {
+    return put_text(serialize_plan(parse_plan(text, "<refh>")), buf, buflen);
+  } catch (const std::exception& e) {
+    set_err(buf, buflen, e.what());
+    return -1000000000;
+  }
+}
+
+// to_dot after max_flow (flow_graph.cpp:257-271), and the min-cut source side
+// (:231-255) as vertex ids.
+int refh_to_dot(void* cp, const int16_t* pl, int allow_partial, char* buf, int buflen, int32_t* cut, int* ncut) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  try {
+    FlowGraph g = build_flow_graph(c, to_placement(c, pl), allow_partial != 0);
+    max_flow(g);
+    std::vector<int> side = min_cut_source_side(g);
+    *ncut = static_cast<int>(side.size());
+    for (size_t i = 0; i < side.size(); ++i) cut[i] = side[i];
+    return put_text(to_dot(g), buf, buflen);
+  } catch (const std::exception& e) {
+    set_err(buf, buflen, e.what());
+    return -1000000000;
+  }
+}
+
+// A stateful Scheduler driven by an op list: op k = (kind[k], id[k], len[k]),
+// kind 0 = admit(id, len), 1 = complete(id, len) — skipped (nh[k] = -2) when
+// that id's admit was deferred, as the simulator only completes admitted
+// requests.  For every admit the hop
+// count (-1 = deferred) goes to nh[k] and the hops to hop_node/s/e at stride
+// max_hops; kv[k] = kv_estimate of node `probe` after the op, avg[k] =
+// avg_output().  Returns 0, or -1 with the exception text in err.
+int refh_sched_ops(void* cp, const int16_t* pl, int allow_partial, uint64_t seed, int64_t K, const int32_t* kind,
+                   const int64_t* id, const int32_t* len, int max_hops, int32_t* nh, int32_t* hop_node,
+                   int32_t* hop_s, int32_t* hop_e, const char* probe, double* kv, double* avg, char* err,
+                   int errlen) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  try {
+    PlacementPlan plan = plan_from_placement(c, to_placement(c, pl), allow_partial != 0, "custom");
+    Scheduler sched(c, plan, SchedPolicy::kIwrr, seed);
+    std::vector<char> admitted;
+    for (int64_t k = 0; k < K; ++k) {
+      nh[k] = 0;
+      if (id[k] >= static_cast<int64_t>(admitted.size())) admitted.resize(id[k] + 1, 0);
+      if (kind[k] == 0) {
+        auto r = sched.admit(static_cast<long>(id[k]), len[k]);
+        if (!r) {
+          nh[k] = -1;
+        } else {
+          admitted[id[k]] = 1;
+          nh[k] = static_cast<int32_t>(r->size());
+          for (int h = 0; h < nh[k] && h < max_hops; ++h) {
+            hop_node[k * max_hops + h] = c.node_index((*r)[h].node);
+            hop_s[k * max_hops + h] = (*r)[h].exec_start;
+            hop_e[k * max_hops + h] = (*r)[h].exec_end;
+          }
+        }
+      } else if (admitted[id[k]]) {
+        sched.complete(static_cast<long>(id[k]), len[k]);
+      } else {
+        nh[k] = -2;
+      }
+      kv[k] = sched.kv_estimate(probe);
+      avg[k] = sched.avg_output();
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return -1;
+  }
+}
+
+// simulate(c, plan_from_placement(c, row), trace, cfg) (sim.cpp:382-388); the
+// metrics go out as the reference binding's dict keys (pymodule.cpp:34-74),
+// JSON, doubles at full precision.
+int refh_simulate(void* cp, const int16_t* pl, int allow_partial, int64_t n, const double* arrival,
+                  const int32_t* in_len, const int32_t* out_len, int online, int policy, uint64_t seed,
+                  double horizon_s, double warmup_s, char* buf, int buflen) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  try {
+    PlacementPlan plan = plan_from_placement(c, to_placement(c, pl), allow_partial != 0, "custom");
+    std::vector<Request> reqs(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) reqs[i] = {arrival[i], in_len[i], out_len[i]};
+    SimConfig cfg;
+    cfg.mode = online ? TraceMode::kOnline : TraceMode::kOffline;
+    cfg.policy = policy == 0 ? SchedPolicy::kIwrr : policy == 1 ? SchedPolicy::kRandom
+                 : policy == 2 ? SchedPolicy::kSqf : SchedPolicy::kSwarm;
+    cfg.seed = seed;
+    cfg.horizon_s = horizon_s;
+    cfg.warmup_s = online ? warmup_s : 0;
+    SimMetrics m = simulate(c, plan, reqs, cfg);
+    nlohmann::ordered_json d;
+    d["window_s"] = m.window_s;
+    d["requests_arrived"] = m.requests_arrived;
+    d["requests_completed"] = m.requests_completed;
+    d["requests_completed_total"] = m.requests_completed_total;
+    d["throughput_tps"] = m.throughput_tps;
+    d["output_tps"] = m.output_tps;
+    d["latency_mean_s"] = m.latency_mean_s;
+    d["latency_p50_s"] = m.latency_p50_s;
+    d["latency_p95_s"] = m.latency_p95_s;
+    d["latency_max_s"] = m.latency_max_s;
+    d["ttft_mean_s"] = m.ttft_mean_s;
+    d["ttft_p95_s"] = m.ttft_p95_s;
+    d["deferrals"] = m.deferrals;
+    d["nodes"] = nlohmann::ordered_json::array();
+    for (const NodeStats& x : m.nodes)
+      d["nodes"].push_back({{"id", x.id}, {"utilization", x.utilization}, {"batches", x.batches},
+                            {"layer_tokens", x.layer_tokens}, {"kv_pages", x.kv_pages}});
+    d["links"] = nlohmann::ordered_json::array();
+    for (const LinkStats& l : m.links)
+      d["links"].push_back({{"src", l.src}, {"dst", l.dst}, {"bytes", l.bytes}, {"transfers", l.transfers},
+                            {"queue_delay_mean_s", l.queue_delay_mean_s},
+                            {"queue_delay_max_s", l.queue_delay_max_s}});
+    d["warnings"] = m.warnings;
+    return put_text(d.dump(), buf, buflen);
+  } catch (const std::exception& e) {
+    set_err(buf, buflen, e.what());
+    return -1000000000;
+  }
+}
+
+// serialize_cluster(prune_links(c, degree)) (placement.cpp:230-332,
+// cluster.cpp:191-228).
+int refh_prune_json(void* cp, double degree, char* buf, int buflen, int* removed) {
+  const ClusterSpec& c = *static_cast<ClusterSpec*>(cp);
+  try {
+    PruneReport rep;
+    ClusterSpec p = prune_links(c, degree, &rep);
+    *removed = rep.links_removed;
+    return put_text(serialize_cluster(p), buf, buflen);
+  } catch (const std::exception& e) {
+    set_err(buf, buflen, e.what());
+    return -1000000000;
   }
 }
 

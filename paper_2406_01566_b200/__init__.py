@@ -39,10 +39,12 @@ from ._helio import (  # noqa: E402
     IwrrPicker,
     ParseError,
     Plan,
+    Scheduler,
     ValidationError,
     build_flow_graph,
     generate_host,
     generate_trace,
+    generate_trace_arrays,
     heuristic_placement,
     iwrr_weights,
     local_search,
@@ -51,7 +53,10 @@ from ._helio import (  # noqa: E402
     max_flow_value,
     plan,
     plan_for_placement,
+    prune_links,
     route_requests,
+    simulate,
+    throughput_upper_bound,
 )
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
@@ -97,5 +102,5 @@ __all__ = [
     "ValidationError", "best_placement", "build_flow_graph", "generate_host", "generate_trace",
     "iwrr_weights", "max_flow", "max_flow_raw", "max_flow_value", "max_flow_values",
     "placement_rows", "plan_for_placement", "route_requests", "heuristic_placement", "local_search",
-    "plan",
+    "plan", "Scheduler", "simulate", "prune_links", "throughput_upper_bound", "generate_trace_arrays",
 ]

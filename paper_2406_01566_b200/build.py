@@ -27,8 +27,9 @@ CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-s
 
 CU_SOURCES = ["helio_gpu.cu", "route.cu", "search.cu", "split.cu"]
 SHIM_SOURCES = ["shim_cluster.cpp", "shim_flow.cpp", "shim_plan.cpp", "shim_sched.cpp", "shim_heuristics.cpp"]
-HEADERS = ["engine.h", "gen.h", "device_common.cuh", "build.cuh", "solve_parity.cuh", "solve_score.cuh", "shim.hpp", "shim_engine.hpp", "helio/cluster.hpp", "helio/errors.hpp",
-           "helio/flow_graph.hpp", "helio/placement.hpp", "helio/scheduler.hpp", "helio/heuristics.hpp"]
+HEADERS = ["engine.h", "gen.h", "device_common.cuh", "build.cuh", "solve_parity.cuh", "solve_score.cuh", "shim.hpp",
+           "shim_engine.hpp", "helio/cluster.hpp", "helio/errors.hpp", "helio/flow_graph.hpp", "helio/placement.hpp",
+           "helio/scheduler.hpp", "helio/heuristics.hpp", "helio/rng.hpp"]
 
 
 def _run(cmd, quiet=False):
@@ -87,6 +88,63 @@ def build(force: bool = False, verbose: bool = False) -> None:
               "-L" + LIB, "-lhelio", "-lhelio_gpu", "-Wl,-rpath,$ORIGIN/lib"], quiet=not verbose)
 
 
+# The reference's host planner + simulator, compiled from its own sources where
+# they lie, linked over this drop-in's flow-graph and scheduler translation
+# units (include/helio_planner.h).  Skipped, keeping a prebuilt library, when
+# the reference tree is absent (the GPU box).
+REF = os.environ.get("HELIO_REFERENCE", "/root/reference/proj")
+PLANNER_REF_SOURCES = ["log", "cluster", "lp", "lp_format", "bnb", "heuristics", "placement", "workload", "sim"]
+PLANNER_SHIM_SOURCES = ["shim_flow.cpp", "shim_sched.cpp"]
+
+
+def _json_include() -> str:
+    """nlohmann/json v3.11.3 single header (the reference vendors it but does not
+    ship it, proj/.gitignore:2); the cudnn_frontend wheel carries the same file."""
+    site = sysconfig.get_paths()["purelib"]
+    return os.path.join(site, "include", "cudnn_frontend", "thirdparty", "nlohmann")
+
+
+def build_planner(force: bool = False, verbose: bool = False) -> None:
+    out = os.path.join(LIB, "libhelio_planner.so")
+    if not os.path.exists(os.path.join(REF, "src", "sim.cpp")):
+        if not verbose:
+            return
+        print(f"planner: {REF} absent; keeping prebuilt {out}" if os.path.exists(out) else
+              f"planner: {REF} absent; plan(method='milp') and simulate() are unavailable")
+        return
+    pobj = os.path.join(OBJ, "planner")
+    os.makedirs(pobj, exist_ok=True)
+    ref_flags = ["-O3", "-DNDEBUG", "-std=c++20", "-fPIC", "-fvisibility=hidden", "-I" + os.path.join(REF, "include"),
+                 "-I" + _json_include()]
+    objs = []
+    for name in PLANNER_REF_SOURCES:
+        src = os.path.join(REF, "src", name + ".cpp")
+        o = os.path.join(pobj, name + ".o")
+        if force or _newer(o, [src]):
+            _run(["g++", *ref_flags, "-c", src, "-o", o], quiet=not verbose)
+        objs.append(o)
+    api = os.path.join(CSRC, "planner", "planner_api.cpp")
+    o = os.path.join(pobj, "planner_api.o")
+    if force or _newer(o, [api, os.path.join(ROOT, "include", "helio_planner.h")]):
+        _run(["g++", *ref_flags, "-c", api, "-o", o], quiet=not verbose)
+    objs.append(o)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "helio_gpu.h")]
+    for name in PLANNER_SHIM_SOURCES:
+        src = os.path.join(CSRC, name)
+        o = os.path.join(pobj, name.replace(".cpp", ".o"))
+        if force or _newer(o, [src] + hdrs):
+            _run(["g++", *CXX_FLAGS, "-fvisibility=hidden", "-I" + CSRC, "-I" + os.path.join(ROOT, "include"),
+                  "-c", src, "-o", o], quiet=not verbose)
+        objs.append(o)
+    vs = os.path.join(OBJ, "planner", "exports.map")
+    with open(vs, "w") as f:
+        f.write("{ global: helio_planner_*; local: *; };\n")
+    libgpu = os.path.join(LIB, "libhelio_gpu.so")
+    if force or _newer(out, objs + [libgpu]):
+        _run(["g++", "-shared", *objs, "-o", out, "-L" + LIB, "-lhelio_gpu", "-Wl,-rpath,$ORIGIN",
+              "-Wl,--version-script=" + vs, "-lpthread"], quiet=not verbose)
+
+
 def build_oracle() -> None:
     """Test infrastructure: oracle/_ref (reference, when /root/reference exists) + C oracle."""
     _run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "-j8"], quiet=True)
@@ -94,4 +152,5 @@ def build_oracle() -> None:
 
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
+    build_planner(force="--force" in sys.argv, verbose=True)
     build_oracle()

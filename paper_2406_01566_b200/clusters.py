@@ -285,6 +285,19 @@ def fan3() -> dict:
             "coordinator": {"id": "coord"}, "nodes": nodes, "links": links}
 
 
+def het42_prune12(capacity: str = "float") -> dict:
+    """het42 after the reference's prune_links(c, 12) (placement.cpp:230-332;
+    SURVEY.md §8(d) item 3): 1,806 -> 588 links, average degree 12.  The JSON
+    is the reference's own output (tests/golden/make_workloads.py), shipped
+    as data; prune_links(cluster, 12) reproduces it on the engine side."""
+    import gzip
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", f"het42-70b-prune12_{capacity}.json.gz")
+    with gzip.open(path, "rt") as f:
+        return json.load(f)
+
+
 CONFIGS: Dict[str, callable] = {
     "single24-70b": lambda cap="float": single24("llama2-70b", cap),
     "single24-30b": lambda cap="float": single24("llama-30b", cap),
@@ -292,6 +305,7 @@ CONFIGS: Dict[str, callable] = {
     "geo24": lambda cap="float": geo24("m24", cap),
     "geo24-70b": lambda cap="float": geo24("70b", cap),
     "syn256-120l": lambda cap="float": syn256(cap),
+    "het42-70b-prune12": het42_prune12,
 }
 
 

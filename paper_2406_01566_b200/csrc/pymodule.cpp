@@ -11,11 +11,15 @@
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include <dlfcn.h>
+
+#include <chrono>
 #include <cmath>
 #include <random>
 
 #include "shim.hpp"
 #include "helio/heuristics.hpp"
+#include "../../include/helio_planner.h"
 
 namespace py = pybind11;
 using namespace helio;
@@ -178,7 +182,7 @@ std::string serialize_cluster(const ClusterSpec& c) {
     links.append(jl);
   }
   root["links"] = links;
-  return py::module_::import("json").attr("dumps")(root, py::arg("indent") = 2).cast<std::string>() + "\n";
+  return py::module_::import("json").attr("dumps")(root, py::arg("indent") = 2, py::arg("ensure_ascii") = false).cast<std::string>() + "\n";
 }
 
 Placement placement_from_dict(const py::dict& d) {
@@ -235,7 +239,7 @@ std::string serialize_plan(const PlacementPlan& plan) {
   }
   root["nodes"] = nodes;
   root["edges"] = edges;
-  return py::module_::import("json").attr("dumps")(root, py::arg("indent") = 2).cast<std::string>() + "\n";
+  return py::module_::import("json").attr("dumps")(root, py::arg("indent") = 2, py::arg("ensure_ascii") = false).cast<std::string>() + "\n";
 }
 
 PlacementPlan parse_plan(const std::string& text, const std::string& origin) {
@@ -363,6 +367,78 @@ py::tuple generate_trace(int count, double rate, const std::string& mode, uint64
   }
   return py::make_tuple(arr, in, out);
 }
+
+// --- the reference planner / simulator linked over this engine ---------------
+// lib/libhelio_planner.so (include/helio_planner.h), next to libhelio.so;
+// loaded on first use so the scoring surface works without it.
+struct Planner {
+  decltype(&helio_planner_plan_milp) plan_milp = nullptr;
+  decltype(&helio_planner_simulate) simulate = nullptr;
+  decltype(&helio_planner_prune_links) prune_links = nullptr;
+  decltype(&helio_planner_upper_bound) upper_bound = nullptr;
+  decltype(&helio_planner_free) free = nullptr;
+};
+
+const Planner& planner() {
+  static Planner p;
+  static std::string error;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    Dl_info info{};
+    std::string path = "libhelio_planner.so";
+    if (dladdr(reinterpret_cast<void*>(&planner), &info) && info.dli_fname) {
+      std::string self = info.dli_fname;
+      path = self.substr(0, self.rfind('/') + 1) + "lib/libhelio_planner.so";
+    }
+    void* h = dlopen(path.c_str(), RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      error = dlerror();
+    } else {
+      p.plan_milp = reinterpret_cast<decltype(p.plan_milp)>(dlsym(h, "helio_planner_plan_milp"));
+      p.simulate = reinterpret_cast<decltype(p.simulate)>(dlsym(h, "helio_planner_simulate"));
+      p.prune_links = reinterpret_cast<decltype(p.prune_links)>(dlsym(h, "helio_planner_prune_links"));
+      p.upper_bound = reinterpret_cast<decltype(p.upper_bound)>(dlsym(h, "helio_planner_upper_bound"));
+      p.free = reinterpret_cast<decltype(p.free)>(dlsym(h, "helio_planner_free"));
+      if (!p.plan_milp || !p.simulate || !p.prune_links || !p.upper_bound || !p.free) error = "missing symbols";
+    }
+  }
+  if (!error.empty())
+    throw InternalError("the reference planner/simulator library (lib/libhelio_planner.so, built by build.py from "
+                        "/root/reference) is unavailable: " + error);
+  return p;
+}
+
+void planner_check(int rc, const char* err) {
+  switch (rc) {
+    case 0: return;
+    case 1: throw ParseError(err);
+    case 2: throw ValidationError(err);
+    default: throw InternalError(err);
+  }
+}
+
+py::object json_loads(const char* text) { return py::module_::import("json").attr("loads")(py::str(text)); }
+
+// generate_trace as the reference binding returns it: a list of
+// (arrival_s, input_len, output_len) tuples (proj/bindings/pymodule.cpp:179-195)
+py::list generate_trace_list(int count, double rate, const std::string& mode, uint64_t seed, double mean_input,
+                             double mean_output) {
+  py::tuple t = generate_trace(count, rate, mode, seed, mean_input, mean_output, 2048, 1024, 0.496);
+  auto a = t[0].cast<py::array_t<double>>().unchecked<1>();
+  auto i = t[1].cast<py::array_t<int32_t>>().unchecked<1>();
+  auto o = t[2].cast<py::array_t<int32_t>>().unchecked<1>();
+  py::list out;
+  for (py::ssize_t k = 0; k < a.shape(0); ++k) out.append(py::make_tuple(a(k), i(k), o(k)));
+  return out;
+}
+
+// Python Scheduler: owns a copy of the cluster and the plan, since the
+// reference Scheduler keeps `const ClusterSpec&` (scheduler.hpp:83).
+struct PyScheduler {
+  std::unique_ptr<ClusterSpec> cluster;
+  std::unique_ptr<Scheduler> sched;
+};
 
 // --- batched engine handle ---------------------------------------------------
 
@@ -556,9 +632,26 @@ PYBIND11_MODULE(_helio, m) {
 
   m.def(
       "plan",
-      [](const ClusterSpec& c, const std::string& method, bool allow_partial, int max_moves) {
-        // pymodule.cpp:130-157 for the heuristics; "local" is this engine's
-        // search and "milp" stays with the reference
+      [](const ClusterSpec& c, const std::string& method, bool allow_partial, double prune_degree, double gap,
+         double time_budget_s, long node_budget, bool warm_starts, bool lex_tiebreak, int max_moves) {
+        // pymodule.cpp:130-157: "milp" is the reference's planner linked over
+        // this engine (every max-flow it takes runs on the B200); the
+        // heuristics wrap their placement into a plan; "local" / "sampled"
+        // are this engine's device searches
+        if (method == "milp") {
+          const Planner& pl = planner();
+          helio_plan_options o{allow_partial ? 1 : 0, prune_degree, gap, time_budget_s, (int64_t)node_budget,
+                               warm_starts ? 1 : 0, lex_tiebreak ? 1 : 0};
+          PlacementPlan plan;
+          char err[1024] = {0};
+          int rc;
+          {
+            py::gil_scoped_release rel;
+            rc = pl.plan_milp(&c, &o, &plan, err, sizeof(err));
+          }
+          planner_check(rc, err);
+          return plan;
+        }
         if (method == "swarm" || method == "petals" || method == "sp") {
           HeuristicResult h = method == "swarm"    ? swarm_placement(c)
                               : method == "petals" ? petals_placement(c)
@@ -596,13 +689,140 @@ PYBIND11_MODULE(_helio, m) {
           for (const std::string& w : warnings) plan.warnings.push_back(w);
           return plan;
         }
-        if (method == "milp")
-          throw ValidationError("method 'milp' is the reference's planner; link it over this engine (INTEGRATION.md)");
         throw ValidationError("unknown method '" + method + "'");
       },
-      py::arg("cluster"), py::arg("method") = "local", py::arg("allow_partial") = true, py::arg("max_moves") = -1,
-      "Compute a placement plan (method: swarm, petals, sp; local = device local search from those seeds; "
-      "sampled = local search, sampled multi-node search, local search again from each seed).");
+      py::arg("cluster"), py::arg("method") = "milp", py::arg("allow_partial") = true,
+      py::arg("prune_degree") = 0.0, py::arg("gap") = 0.02, py::arg("time_budget_s") = 600.0,
+      py::arg("node_budget") = -1, py::arg("warm_starts") = true, py::arg("lex_tiebreak") = true,
+      py::arg("max_moves") = -1,
+      "Compute a placement plan (method: milp, swarm, petals, or sp, as the reference; plus local = device "
+      "local search from the heuristic seeds, sampled = local search, sampled multi-node search, local search "
+      "again from each seed).");
+
+  m.def(
+      "simulate",
+      [](const ClusterSpec& c, const PlacementPlan& plan, const py::list& trace, const std::string& mode,
+         const std::string& scheduler, uint64_t seed, double horizon_s, double warmup_s) {
+        // pymodule.cpp:197-218: the reference's discrete-event simulator
+        // (sim.cpp) over this engine's Scheduler
+        std::vector<double> arr;
+        std::vector<int32_t> in, out;
+        for (const auto& row : trace) {
+          auto t = row.cast<std::tuple<double, int, int>>();
+          arr.push_back(std::get<0>(t));
+          in.push_back(std::get<1>(t));
+          out.push_back(std::get<2>(t));
+        }
+        if (mode != "online" && mode != "offline")
+          throw ValidationError("unknown trace mode '" + mode + "' (expected online or offline)");
+        const SchedPolicy pol = sched_policy_from_str(scheduler);
+        helio_sim_config cfg{mode == "online" ? 1 : 0, horizon_s, mode == "online" ? warmup_s : 0.0,
+                             static_cast<int32_t>(pol), seed, 32, 2048, 0.01, 0.002};
+        const Planner& pl = planner();
+        char* js = nullptr;
+        char err[1024] = {0};
+        int rc;
+        {
+          py::gil_scoped_release rel;
+          rc = pl.simulate(&c, &plan, (int64_t)arr.size(), arr.data(), in.data(), out.data(), &cfg, &js, err,
+                           sizeof(err));
+        }
+        planner_check(rc, err);
+        py::object d = json_loads(js);
+        pl.free(js);
+        return d;
+      },
+      py::arg("cluster"), py::arg("plan"), py::arg("trace"), py::arg("mode") = "online",
+      py::arg("scheduler") = "iwrr", py::arg("seed") = 1, py::arg("horizon_s") = 120.0,
+      py::arg("warmup_s") = 20.0,
+      "Run a trace through the reference's discrete-event simulator over this engine; returns a metrics dict.");
+
+  m.def(
+      "prune_links",
+      [](const ClusterSpec& c, double target_avg_degree) {
+        const Planner& pl = planner();
+        ClusterSpec out;
+        int32_t removed = 0;
+        double before = 0, after = 0;
+        char* warn = nullptr;
+        char err[1024] = {0};
+        planner_check(pl.prune_links(&c, target_avg_degree, &out, &removed, &before, &after, &warn, err,
+                                     sizeof(err)),
+                      err);
+        py::dict rep;
+        rep["links_removed"] = removed;
+        rep["avg_degree_before"] = before;
+        rep["avg_degree_after"] = after;
+        rep["warnings"] = json_loads(warn);
+        pl.free(warn);
+        return py::make_tuple(out, rep);
+      },
+      py::arg("cluster"), py::arg("target_avg_degree"),
+      "The reference's prune_links (placement.cpp:230-332): (pruned cluster, report dict).");
+
+  m.def(
+      "throughput_upper_bound",
+      [](const ClusterSpec& c) {
+        double v = 0;
+        char err[1024] = {0};
+        planner_check(planner().upper_bound(&c, &v, err, sizeof(err)), err);
+        return v;
+      },
+      py::arg("cluster"), "Compute-only throughput ceiling for a cluster.");
+
+  py::class_<PyScheduler>(m, "Scheduler")
+      .def(py::init([](const ClusterSpec& c, const PlacementPlan& plan, const std::string& policy, uint64_t seed) {
+             auto ps = std::make_unique<PyScheduler>();
+             ps->cluster = std::make_unique<ClusterSpec>(c);
+             ps->sched = std::make_unique<Scheduler>(*ps->cluster, plan, sched_policy_from_str(policy), seed);
+             return ps;
+           }),
+           py::arg("cluster"), py::arg("plan"), py::arg("policy") = "iwrr", py::arg("seed") = 1)
+      .def(
+          "admit",
+          [](PyScheduler& s, long request_id, int input_len) -> py::object {
+            auto r = s.sched->admit(request_id, input_len);
+            if (!r) return py::none();
+            py::list hops;
+            for (const RouteHop& h : *r) hops.append(py::make_tuple(h.node, h.exec_start, h.exec_end));
+            return std::move(hops);
+          },
+          py::arg("request_id"), py::arg("input_len"),
+          "Scheduler::admit (scheduler.cpp:158-181): [(node, exec_start, exec_end)] or None when deferred.")
+      .def("complete", [](PyScheduler& s, long id, int out) { s.sched->complete(id, out); }, py::arg("request_id"),
+           py::arg("output_len"))
+      .def("kv_estimate", [](const PyScheduler& s, const std::string& n) { return s.sched->kv_estimate(n); })
+      .def("kv_capacity", [](const PyScheduler& s, const std::string& n) { return s.sched->kv_capacity(n); })
+      .def_property_readonly("avg_output", [](const PyScheduler& s) { return s.sched->avg_output(); })
+      .def(
+          "run_ac8",
+          [](PyScheduler& s, py::array_t<int32_t, py::array::c_style | py::array::forcecast> in,
+             py::array_t<int32_t, py::array::c_style | py::array::forcecast> out) {
+            // admit(r, in[r]); if admitted complete(r, out[r]) (acceptance_main.cpp:529-537),
+            // timed without Python in the loop: (hops per request or -1, seconds)
+            const int64_t R = in.size();
+            py::array_t<int32_t> nh(R);
+            auto n = nh.mutable_unchecked<1>();
+            const int32_t* pi = in.data();
+            const int32_t* po = out.data();
+            double secs = 0;
+            {
+              py::gil_scoped_release rel;
+              const auto t0 = std::chrono::steady_clock::now();
+              for (int64_t r = 0; r < R; ++r) {
+                auto route = s.sched->admit((long)r, pi[r]);
+                if (!route) {
+                  n(r) = -1;
+                  continue;
+                }
+                n(r) = (int32_t)route->size();
+                s.sched->complete((long)r, po[r]);
+              }
+              secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            }
+            return py::make_tuple(nh, secs);
+          },
+          py::arg("input_lens"), py::arg("output_lens"));
 
   m.def(
       "heuristic_placement",
@@ -706,8 +926,11 @@ PYBIND11_MODULE(_helio, m) {
   m.def(
       "route_requests",
       [](const ClusterSpec& c, const PlacementPlan& plan, const std::vector<int>& in, const std::vector<int>& out) {
-        Scheduler s(c, plan);
-        auto routes = s.route(in, out);
+        std::vector<std::optional<std::vector<RouteHop>>> routes;
+        {
+          py::gil_scoped_release rel;
+          routes = route_requests(c, plan, in, out);
+        }
         py::list res;
         for (auto& r : routes) {
           if (!r) {
@@ -723,10 +946,14 @@ PYBIND11_MODULE(_helio, m) {
       py::arg("cluster"), py::arg("plan"), py::arg("input_lens"), py::arg("output_lens"),
       "IWRR routes in AC8 order (admit then complete); None = deferred.");
 
-  m.def("generate_trace", &generate_trace, py::arg("count"), py::arg("rate") = 0.0, py::arg("mode") = "offline",
-        py::arg("seed") = 1, py::arg("mean_input") = 763.0, py::arg("mean_output") = 232.0,
-        py::arg("max_input") = 2048, py::arg("max_output") = 1024, py::arg("sigma") = 0.496,
-        "Sample (arrival_s[], input_len[], output_len[]) exactly as the reference's generate_trace.");
+  m.def("generate_trace", &generate_trace_list, py::arg("count"), py::arg("rate") = 0.0,
+        py::arg("mode") = "offline", py::arg("seed") = 1, py::arg("mean_input") = 763.0,
+        py::arg("mean_output") = 232.0, "Sample (arrival_s, input_len, output_len) request tuples.");
+  m.def("generate_trace_arrays", &generate_trace, py::arg("count"), py::arg("rate") = 0.0,
+        py::arg("mode") = "offline", py::arg("seed") = 1, py::arg("mean_input") = 763.0,
+        py::arg("mean_output") = 232.0, py::arg("max_input") = 2048, py::arg("max_output") = 1024,
+        py::arg("sigma") = 0.496,
+        "generate_trace as three arrays (arrival_s[], input_len[], output_len[]) for large traces.");
 
   m.def(
       "generate_host",

@@ -449,22 +449,62 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
 }
 
 // ---------------------------------------------------------------------------
-// Stand-alone iwrr_weights / IwrrPicker::next on the device.
+// Stand-alone iwrr_weights / IwrrPicker cycles / IwrrPicker::next on the
+// device.  Buffers come from the context's host-entry arena (no per-call
+// cudaMalloc/cudaFree).
 namespace {
 
-__global__ void iwrr_weights_kernel(int n, const double* __restrict__ flow, long long* __restrict__ w) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// iwrr_weights (scheduler.cpp:46-56) of list `l` = [off[l], off[l+1]).
+__device__ void list_weights(const double* __restrict__ flow, long long* __restrict__ w, int b, int e) {
   long long wmax = 0;
-  for (int i = 0; i < n; ++i) {
+  for (int i = b; i < e; ++i) {
     long long v = llround(1000.0 * flow[i]);
     w[i] = v > 1 ? v : 1;
     wmax = w[i] > wmax ? w[i] : wmax;
   }
   if (wmax > 32)
-    for (int i = 0; i < n; ++i) {
+    for (int i = b; i < e; ++i) {
       long long v = llround(w[i] * 32.0 / wmax);
       w[i] = v > 1 ? v : 1;
     }
+}
+
+__global__ void iwrr_weights_kernel(int nlists, const int32_t* __restrict__ off, const double* __restrict__ flow,
+                                    long long* __restrict__ w) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < nlists) list_weights(flow, w, off[l], off[l + 1]);
+}
+
+// One warp per candidate list: (flows -> weights, when flow != nullptr), then
+// the IWRR cycle — the slots (round r, index i) with w_i >= r in (r, i) order,
+// i.e. the order IwrrPicker::next (scheduler.cpp:28-44) visits them when
+// every candidate is eligible.  cyc[cyc_off[l] + k] = candidate index of the
+// k-th slot; cyc_len[l] = sum of the weights.
+__global__ void iwrr_cycles_kernel(int nlists, const int32_t* __restrict__ off, const double* __restrict__ flow,
+                                   long long* __restrict__ w, const int64_t* __restrict__ cyc_off,
+                                   int32_t* __restrict__ cyc, int64_t* __restrict__ cyc_len) {
+  const int lane = threadIdx.x & 31;
+  const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (l >= nlists) return;
+  const int b = off[l], e = off[l + 1];
+  if (flow != nullptr && lane == 0) list_weights(flow, w, b, e);
+  __syncwarp();
+  long long wm = 1;  // IwrrPicker ctor: wmax_ starts at 1
+  for (int i = b + lane; i < e; i += 32) wm = w[i] > wm ? w[i] : wm;
+  for (int d = 16; d; d >>= 1) {
+    const long long o = __shfl_xor_sync(0xffffffffu, wm, d);
+    wm = o > wm ? o : wm;
+  }
+  int64_t p = cyc_off[l];
+  for (long long r = 1; r <= wm; ++r)
+    for (int base = b; base < e; base += 32) {
+      const int i = base + lane;
+      const bool take = i < e && w[i] >= r;
+      const unsigned m = __ballot_sync(0xffffffffu, take);
+      if (take) cyc[p + __popc(m & ((1u << lane) - 1u))] = i - b;
+      p += __popc(m);
+    }
+  if (lane == 0) cyc_len[l] = p - cyc_off[l];
 }
 
 __global__ void iwrr_picks_kernel(int n, const long long* __restrict__ w, long long* state, int calls,
@@ -504,18 +544,87 @@ extern "C" int helio_gpu_iwrr_weights(helio_gpu_ctx* ctx, const double* h_flows,
   if (n < 0 || (n > 0 && (!h_flows || !h_w))) return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   if (n == 0) return HELIO_OK;
   CK(cudaSetDevice(ctx->device));
-  double* d_f = nullptr;
-  long long* d_w = nullptr;
-  CK(cudaMalloc(&d_f, 8 * n));
-  CK(cudaMalloc(&d_w, 8 * n));
-  CK(cudaMemcpyAsync(d_f, h_flows, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
-  iwrr_weights_kernel<<<1, 32, 0, ctx->stream>>>(n, d_f, d_w);
+  cudaStream_t st = ctx->stream;
+  auto carve = [&](Carve& c, int32_t*& off, double*& f, long long*& w) {
+    off = c.take<int32_t>(2);
+    f = c.take<double>(n);
+    w = c.take<long long>(n);
+  };
+  int32_t* d_off;
+  double* d_f;
+  long long* d_w;
+  Carve measure, c;
+  carve(measure, d_off, d_f, d_w);
+  int rc = host_arena(ctx, measure.off, &c.base);
+  if (rc) return rc;
+  carve(c, d_off, d_f, d_w);
+  const int32_t off[2] = {0, n};
+  CK(cudaMemcpyAsync(d_off, off, sizeof(off), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_f, h_flows, 8 * n, cudaMemcpyHostToDevice, st));
+  iwrr_weights_kernel<<<1, 32, 0, st>>>(1, d_off, d_f, d_w);
   ctx->launches++;
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(h_w, d_w, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  cudaFree(d_f);
-  cudaFree(d_w);
+  CK(cudaMemcpyAsync(h_w, d_w, 8 * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return HELIO_OK;
+}
+
+extern "C" int helio_gpu_iwrr_cycles(helio_gpu_ctx* ctx, int32_t nlists, const int32_t* h_off,
+                                     const double* h_flows, int64_t* h_weights, const int64_t* h_cyc_off,
+                                     int32_t* h_cycles, int64_t* h_cyc_len) {
+  if (!ctx) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);  // contexts serialise their callers
+  if (nlists < 0 || (nlists > 0 && (!h_off || !h_weights || !h_cyc_off || !h_cyc_len)))
+    return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
+  if (nlists == 0) return HELIO_OK;
+  const int32_t n = h_off[nlists];
+  if (h_off[0] != 0 || n < 0) return fail(ctx, HELIO_ERR_INVALID, "list offsets must start at 0");
+  for (int l = 0; l < nlists; ++l)
+    if (h_off[l + 1] < h_off[l]) return fail(ctx, HELIO_ERR_INVALID, "list offsets must be non-decreasing");
+  const int64_t total = h_cyc_off[nlists];
+  if (h_cyc_off[0] != 0 || total < 0 || (total > 0 && !h_cycles))
+    return fail(ctx, HELIO_ERR_INVALID, "bad cycle offsets");
+  if (!h_flows)  // caller weights: every list's cycle (sum of its weights) must fit its slot range
+    for (int l = 0; l < nlists; ++l) {
+      long long sum = 0;
+      for (int i = h_off[l]; i < h_off[l + 1]; ++i) sum += h_weights[i] > 0 ? h_weights[i] : 0;
+      if (sum > h_cyc_off[l + 1] - h_cyc_off[l]) return fail(ctx, HELIO_ERR_INVALID, "cycle range too small");
+    }
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  auto carve = [&](Carve& c, int32_t*& off, double*& f, long long*& w, int64_t*& coff, int32_t*& cyc,
+                   int64_t*& clen) {
+    off = c.take<int32_t>(nlists + 1);
+    f = c.take<double>(h_flows ? n : 1);
+    w = c.take<long long>(n);
+    coff = c.take<int64_t>(nlists + 1);
+    cyc = c.take<int32_t>(total);
+    clen = c.take<int64_t>(nlists);
+  };
+  int32_t *d_off, *d_cyc;
+  double* d_f;
+  long long* d_w;
+  int64_t *d_coff, *d_clen;
+  Carve measure, c;
+  carve(measure, d_off, d_f, d_w, d_coff, d_cyc, d_clen);
+  int rc = host_arena(ctx, measure.off, &c.base);
+  if (rc) return rc;
+  carve(c, d_off, d_f, d_w, d_coff, d_cyc, d_clen);
+  CK(cudaMemcpyAsync(d_off, h_off, 4 * (nlists + 1), cudaMemcpyHostToDevice, st));
+  if (h_flows)
+    CK(cudaMemcpyAsync(d_f, h_flows, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+  else if (n > 0)
+    CK(cudaMemcpyAsync(d_w, h_weights, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_coff, h_cyc_off, 8 * (nlists + 1), cudaMemcpyHostToDevice, st));
+  const int warps = 4;
+  iwrr_cycles_kernel<<<(nlists + warps - 1) / warps, 32 * warps, 0, st>>>(nlists, d_off, h_flows ? d_f : nullptr,
+                                                                          d_w, d_coff, d_cyc, d_clen);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  if (h_flows && n > 0) CK(cudaMemcpyAsync(h_weights, d_w, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  if (total > 0) CK(cudaMemcpyAsync(h_cycles, d_cyc, 4 * (size_t)total, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h_cyc_len, d_clen, 8 * (size_t)nlists, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   return HELIO_OK;
 }
 
@@ -527,29 +636,33 @@ extern "C" int helio_gpu_iwrr_picks(helio_gpu_ctx* ctx, const int64_t* h_w, int3
     return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   if (calls == 0) return HELIO_OK;
   CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
   const int words = (n + 63) / 64;
-  long long *d_w = nullptr, *d_state = nullptr;
-  unsigned long long* d_m = nullptr;
-  int* d_out = nullptr;
-  long long st[2] = {(long long)*h_round, (long long)*h_idx};
-  CK(cudaMalloc(&d_w, 8 * std::max(n, 1)));
-  CK(cudaMalloc(&d_state, 16));
-  CK(cudaMalloc(&d_m, 8 * std::max<size_t>((size_t)calls * words, 1)));
-  CK(cudaMalloc(&d_out, 4 * calls));
-  if (n > 0) CK(cudaMemcpyAsync(d_w, h_w, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d_state, st, 16, cudaMemcpyHostToDevice, ctx->stream));
-  if (n > 0) CK(cudaMemcpyAsync(d_m, h_masks, 8 * (size_t)calls * words, cudaMemcpyHostToDevice, ctx->stream));
-  iwrr_picks_kernel<<<1, 32, 0, ctx->stream>>>(n, d_w, d_state, calls, d_m, d_out);
+  auto carve = [&](Carve& c, long long*& w, long long*& state, unsigned long long*& m, int*& out) {
+    w = c.take<long long>(n);
+    state = c.take<long long>(2);
+    m = c.take<unsigned long long>((size_t)calls * words);
+    out = c.take<int>(calls);
+  };
+  long long *d_w, *d_state;
+  unsigned long long* d_m;
+  int* d_out;
+  Carve measure, c;
+  carve(measure, d_w, d_state, d_m, d_out);
+  int rc = host_arena(ctx, measure.off, &c.base);
+  if (rc) return rc;
+  carve(c, d_w, d_state, d_m, d_out);
+  long long stt[2] = {(long long)*h_round, (long long)*h_idx};
+  if (n > 0) CK(cudaMemcpyAsync(d_w, h_w, 8 * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_state, stt, 16, cudaMemcpyHostToDevice, st));
+  if (n > 0) CK(cudaMemcpyAsync(d_m, h_masks, 8 * (size_t)calls * words, cudaMemcpyHostToDevice, st));
+  iwrr_picks_kernel<<<1, 32, 0, st>>>(n, d_w, d_state, calls, d_m, d_out);
   ctx->launches++;
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(h_out, d_out, 4 * calls, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(st, d_state, 16, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  *h_round = st[0];
-  *h_idx = st[1];
-  cudaFree(d_w);
-  cudaFree(d_state);
-  cudaFree(d_m);
-  cudaFree(d_out);
+  CK(cudaMemcpyAsync(h_out, d_out, 4 * calls, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(stt, d_state, 16, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *h_round = stt[0];
+  *h_idx = stt[1];
   return HELIO_OK;
 }

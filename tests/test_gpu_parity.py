@@ -181,7 +181,7 @@ def test_routes_bit_exact(tag):
 def test_routes_one_million_match_oracle():
     z = golden("route_geo24.npz")
     c, e = engine("geo24_float")
-    _, inl, outl = h.generate_trace(1_000_000, 0.0, "offline", 7)
+    _, inl, outl = h.generate_trace_arrays(1_000_000, 0.0, "offline", 7)
     pe = np.stack([z["plan_src"], z["plan_dst"], z["plan_es"], z["plan_ee"]], 1).astype(np.int32)
     nh, hn, hs, he, den = e.route(z["row"], pe, z["plan_flow"], inl, outl, c.num_layers)
     o = Oracle(golden_cluster("geo24_float"))
@@ -194,7 +194,7 @@ def test_routes_one_million_match_oracle():
 
 def test_generate_trace_matches_reference_fixture():
     z = golden("route_geo24.npz")
-    _, inl, outl = h.generate_trace(len(z["in_len"]), 0.0, "offline", 7)
+    _, inl, outl = h.generate_trace_arrays(len(z["in_len"]), 0.0, "offline", 7)
     assert np.array_equal(inl, z["in_len"]) and np.array_equal(outl, z["out_len"])
 
 
