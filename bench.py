@@ -350,10 +350,39 @@ def routing_leg(h, clusters, dev, sp, requests, with_reference):
                            "identical_to_batch": bool(np.array_equal(snh, nh))}
     except Exception as ex:  # reported, never fatal
         out["stateful"] = {"error": str(ex)}
+    # KV masking binds: the same plan with kv_bytes_per_token_layer = 1 MB
+    # (~40% of admissions deferred) takes the exact replay kernel
+    try:
+        dm = json.loads(json.dumps(d))
+        dm["model"]["kv_bytes_per_token_layer"] = 1e6
+        cm = h.Cluster.from_json(json.dumps(dm))
+        em = h.Engine(cm, device=dev)
+        em.route(row, pe, pf, inl[:1000], outl[:1000], 0, False)  # warm-up
+        mt = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            mnh, mhn, _, _, mden = em.route(row, pe, pf, inl, outl, 0, False)
+            mt.append(time.perf_counter() - t0)
+        out["masked"] = {"value": requests / min(mt), "unit": "routes/s", "deferred": int(mden),
+                         "kernel": "route_masked_warp (exact AC8 replay, one warp, state in shared memory)",
+                         "workload": "same plan and requests, kv_bytes_per_token_layer = 1e6"}
+    except Exception as ex:  # reported, never fatal
+        out["masked"] = {"error": str(ex)}
     if with_reference:
         try:
             sys.path.insert(0, os.path.join(ROOT, "tests"))
             from _support import RefCluster  # test infrastructure: reference timing only
+            if "value" in out.get("masked", {}):
+                t0 = time.perf_counter()
+                rden_m, rnh_m, rhn_m, _, _ = RefCluster(dm).route(row, inl, outl, True, seed=7)
+                rtm = time.perf_counter() - t0
+                Hm = mhn.shape[1]
+                mm = np.arange(Hm)[None, :] < np.maximum(mnh, 0)[:, None]
+                out["masked"]["reference"] = {"value": requests / rtm, "unit": "routes/s", "cores": 1,
+                                              "kind": "reference",
+                                              "sample": f"{requests} Scheduler::admit+complete, one thread"}
+                out["masked"]["identical_to_reference"] = bool(
+                    rden_m == mden and np.array_equal(rnh_m, mnh) and np.array_equal(rhn_m[:, :Hm][mm], mhn[mm]))
             rc = RefCluster(d)
             t0 = time.perf_counter()
             rden, rnh, rhn, _, _ = rc.route(row, inl, outl, True, seed=7)

@@ -16,8 +16,9 @@
 // (scheduler.cpp:100-108) may exceed 0.9 * kv_cap; in the AC8 order every
 // charge is released before the next admit, so the host checks that bound with
 // the largest possible running mean of output lengths.  If it may bind (or the
-// plan's exec intervals are not node-consistent) the exact sequential replay
-// kernel runs instead — still on the device.
+// plan's exec intervals are not node-consistent) the exact replay runs instead:
+// one warp walking the device-built cycles with the state in shared memory
+// (route_masked_warp).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -116,91 +117,143 @@ __global__ void route_apply(int64_t R, int x, int L, int max_hops, const int32_t
   }
 }
 
-// Exact sequential replay of Scheduler::admit/complete (masking may bind).
-__global__ void route_sequential(int64_t R, int nv, int L, int max_hops, double kvb,
-                                 const int32_t* __restrict__ obeg, const int32_t* __restrict__ odst,
-                                 const int32_t* __restrict__ oes, const int32_t* __restrict__ oee,
-                                 const long long* __restrict__ w, const long long* __restrict__ wmaxv,
-                                 const int32_t* __restrict__ node_of, const double* __restrict__ kv_cap,
-                                 double* kv_est, long long* p_round, int32_t* p_idx,
-                                 const int32_t* __restrict__ in_len, const int32_t* __restrict__ out_len,
-                                 int32_t* nh, int32_t* hop_node, int32_t* hop_s, int32_t* hop_e,
-                                 int32_t* ch_v, double* ch_b, long long* deferred, int* err) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+// Exact replay of Scheduler::admit/complete in the AC8 order when KV masking
+// may bind.  One warp, state in shared memory.  In the AC8 order every charge
+// is released (complete, or the rollback of a deferral) before the next
+// admit, and a route visits a vertex at most once (exec ranges strictly
+// increase), so at every eligibility test kv_est[d] is exactly 0.0 (b - b ==
+// 0 in IEEE arithmetic) and the reference's test (scheduler.cpp:105-108)
+// reduces to  (in_len + avg) * kvb * (exec_end - exec_start) <= 0.9 *
+// kv_cap[d]  — the same double operations in the same order.  The serial
+// state is each vertex's picker position plus the running output mean; the
+// warp scans 32 cycle slots per step (ballot, first eligible lane), and the
+// division of the next mean update is issued before the route is walked
+// (it does not depend on it).  A deferred request leaves the positions it
+// advanced, as IwrrPicker::next does (scheduler.cpp:165-168 rolls back only
+// the KV charges).
+__global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double kvb,
+                                  const int32_t* __restrict__ obeg, const int32_t* __restrict__ odst,
+                                  const int32_t* __restrict__ oes, const int32_t* __restrict__ oee,
+                                  const int32_t* __restrict__ node_of, const double* __restrict__ kv_cap,
+                                  const int32_t* __restrict__ cyc_len, const int16_t* __restrict__ cyc,
+                                  const int32_t* __restrict__ in_len, const int32_t* __restrict__ out_len,
+                                  int32_t* nh, int32_t* hop_node, int32_t* hop_s, int32_t* hop_e,
+                                  long long* deferred, int* err) {
+  extern __shared__ __align__(16) char sm[];
+  const int lane = threadIdx.x;
+  // Slot-ordered records: vertex x's cycle occupies slots [base_x, base_x +
+  // W_x); slot k carries its edge's (threshold, exec length) as doubles and
+  // (dst, exec_start, exec_end, node of dst) as int16, so a pick costs one
+  // vertex load and one slot load.  Threshold = 0.9 * kv_cap[dst]; the
+  // coordinator never masks (+inf).
+  int32_t* vbase = reinterpret_cast<int32_t*>(sm);
+  int32_t* vW = vbase + nv;
+  int32_t* vpos = vW + nv;
+  double2* srec = reinterpret_cast<double2*>(sm + (((size_t)12 * nv + 15) & ~size_t(15)));
+  int W_tot = 0;  // every lane computes the same prefix
   for (int x = 0; x < nv; ++x) {
-    p_round[x] = 1;
-    p_idx[x] = 0;
-    kv_est[x] = 0.0;
+    const int W = obeg[x + 1] > obeg[x] ? cyc_len[x] : 0;
+    if (lane == 0) {
+      vbase[x] = W_tot;
+      vW[x] = W;
+      vpos[x] = 0;
+    }
+    W_tot += W;
   }
-  double avg = 232.0;
-  long long samples = 1, den = 0;
-  for (int64_t r = 0; r < R; ++r) {
-    int v = 0, covered = 0, n = 0;
-    bool ok = true;
-    while (covered < L) {
-      const int b = obeg[v], deg = obeg[v + 1] - b;
-      int pick = -1;
-      if (deg > 0) {
-        const long long wm = wmaxv[v];
-        const long long positions = wm * (long long)deg;
-        for (long long it = 0; it < positions; ++it) {
-          if (p_idx[v] == deg) {
-            p_idx[v] = 0;
-            p_round[v] = p_round[v] == wm ? 1 : p_round[v] + 1;
-          }
-          const int i = p_idx[v]++;
-          if (w[b + i] >= p_round[v]) {
-            const int d = odst[b + i];
-            bool elig = true;
-            if (d != 0) {
-              const double tokens = in_len[r] + avg;
-              const double charge = tokens * kvb * (double)(oee[b + i] - oes[b + i]);
-              elig = kv_est[d] + charge <= 0.9 * kv_cap[d];
+  short4* smeta = reinterpret_cast<short4*>(srec + W_tot);
+  for (int x = 0; x < nv; ++x) {
+    const int W = obeg[x + 1] > obeg[x] ? cyc_len[x] : 0;
+    int base = 0;
+    for (int y = 0; y < x; ++y) base += obeg[y + 1] > obeg[y] ? cyc_len[y] : 0;
+    for (int k = lane; k < W; k += 32) {
+      const int e = obeg[x] + cyc[32 * obeg[x] + k];
+      const int d = odst[e];
+      srec[base + k] = make_double2(d == 0 ? 1.0e308 : 0.9 * kv_cap[d], (double)(oee[e] - oes[e]));
+      smeta[base + k] = make_short4((short)d, (short)oes[e], (short)oee[e], (short)node_of[d]);
+    }
+  }
+  __syncwarp();
+  double avg = 232.0, samples = 1.0;
+  long long den = 0;
+  for (int64_t r0 = 0; r0 < R; r0 += 32) {
+    const int nb = R - r0 < 32 ? (int)(R - r0) : 32;
+    const int my_in = lane < nb ? in_len[r0 + lane] : 0;
+    const int my_out = lane < nb ? out_len[r0 + lane] : 0;
+    for (int j = 0; j < nb; ++j) {
+      const int64_t r = r0 + j;
+      const int in = __shfl_sync(0xffffffffu, my_in, j);
+      const int out = __shfl_sync(0xffffffffu, my_out, j);
+      const double tk = ((double)in + avg) * kvb;  // hop_charge = tk * (exec_end - exec_start)
+      int v = 0, covered = 0, h = 0;
+      bool ok = true;
+      while (covered < L) {
+        const int base = vbase[v], W = vW[v], p = vpos[v];
+        if (W == 0) {  // no out-edges: IwrrPicker::next returns -1
+          ok = false;
+          break;
+        }
+        // the slot at the current position first (the common case), then
+        // the rest of one full cycle 32 slots at a time
+        int slot = base + p, np = p + 1 == W ? 0 : p + 1;
+        double2 rc = srec[slot];
+        if (!(tk * rc.y <= rc.x)) {
+          slot = -1;
+          for (int k0 = 1; k0 < W; k0 += 32) {
+            const int k = k0 + lane;
+            bool el = false;
+            int sl = 0;
+            if (k < W) {
+              const int q = p + k;
+              sl = base + (q >= W ? q - W : q);
+              const double2 x = srec[sl];
+              el = tk * x.y <= x.x;
             }
-            if (elig) {
-              pick = i;
+            const unsigned m = __ballot_sync(0xffffffffu, el);
+            if (m) {
+              const int jl = __ffs(m) - 1;
+              slot = __shfl_sync(0xffffffffu, sl, jl);
+              int q = p + k0 + jl + 1;
+              while (q >= W) q -= W;
+              np = q;
               break;
             }
           }
+          if (slot < 0) {  // one full cycle with nothing eligible: position unchanged
+            ok = false;
+            break;
+          }
         }
-      }
-      if (pick < 0) {
-        for (int q = 0; q < n; ++q) kv_est[ch_v[q]] -= ch_b[q];
-        ok = false;
-        break;
-      }
-      const int e = b + pick, d = odst[e];
-      if (d == 0 || oes[e] != covered) {
-        *err = 1;
-        return;
-      }
-      const double tokens = in_len[r] + avg;
-      const double bytes = tokens * kvb * (double)(oee[e] - oes[e]);
-      kv_est[d] += bytes;
-      ch_v[n] = d;
-      ch_b[n] = bytes;
-      if (n < max_hops) {
-        hop_node[r * max_hops + n] = node_of[d];
-        if (hop_s) {
-          hop_s[r * max_hops + n] = oes[e];
-          hop_e[r * max_hops + n] = oee[e];
+        const short4 mt = smeta[slot];
+        const int d = mt.x;
+        if (d == 0 || mt.y != covered) {  // scheduler.cpp:170-171
+          if (lane == 0) atomicExch(err, 1);
+          return;
         }
+        if (lane == 0) {
+          vpos[v] = np;
+          if (h < max_hops) {
+            hop_node[r * max_hops + h] = mt.w;
+            if (hop_s) {
+              hop_s[r * max_hops + h] = mt.y;
+              hop_e[r * max_hops + h] = mt.z;
+            }
+          }
+        }
+        __syncwarp();
+        ++h;
+        covered = mt.z;
+        v = d;
       }
-      ++n;
-      covered = oee[e];
-      v = d;
+      if (ok) {  // complete(): the running mean (scheduler.cpp:183-190)
+        samples += 1.0;
+        avg += ((double)out - avg) / samples;
+      } else {
+        ++den;
+      }
+      if (lane == 0) nh[r] = ok ? h : -1;
     }
-    if (!ok) {
-      nh[r] = -1;
-      ++den;
-      continue;
-    }
-    nh[r] = n;
-    for (int q = 0; q < n; ++q) kv_est[ch_v[q]] -= ch_b[q];
-    ++samples;
-    avg += (out_len[r] - avg) / (double)samples;
   }
-  *deferred = den;
+  if (lane == 0) *deferred = den;
 }
 
 // Route buffers are carved from one context-owned device arena that only
@@ -306,9 +359,9 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   int32_t *d_obeg = nullptr, *d_odst = nullptr, *d_oes = nullptr, *d_oee = nullptr, *d_node = nullptr,
           *d_cycoff = nullptr, *d_in = nullptr, *d_out = nullptr, *d_cur = nullptr, *d_nh = nullptr,
           *d_flag = nullptr, *d_rank = nullptr, *d_hn = nullptr, *d_hs = nullptr, *d_he = nullptr,
-          *d_pidx = nullptr, *d_chv = nullptr, *d_cyclen = nullptr;
-  double *d_flow = nullptr, *d_kvcap = nullptr, *d_kvest = nullptr, *d_chb = nullptr;
-  long long *d_w = nullptr, *d_wmax = nullptr, *d_pround = nullptr, *d_den = nullptr;
+          *d_cyclen = nullptr;
+  double *d_flow = nullptr, *d_kvcap = nullptr;
+  long long *d_w = nullptr, *d_wmax = nullptr, *d_den = nullptr;
   int16_t *d_cyc = nullptr, *d_cov = nullptr;
   int* d_err = nullptr;
   void* d_tmp = nullptr;
@@ -353,12 +406,6 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
       TRY(ar.take(&d_flag, R));
       TRY(ar.take(&d_rank, R));
       TRY(ar.take(reinterpret_cast<char**>(&d_tmp), tmp_bytes));
-    } else {
-      TRY(ar.take(&d_kvest, nv));
-      TRY(ar.take(&d_pround, nv));
-      TRY(ar.take(&d_pidx, nv));
-      TRY(ar.take(&d_chv, L + 1));
-      TRY(ar.take(&d_chb, L + 1));
     }
     if (pass == 0 && ar.off > ctx->route_cap) {
       cudaFree(ctx->d_route);
@@ -417,12 +464,18 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
     }
   } else if (!rc && R > 0) {
     {
-      route_sequential<<<1, 1, 0, st>>>(R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst, d_oes,
-                                        d_oee, d_w, d_wmax, d_node, d_kvcap, d_kvest, d_pround, d_pidx,
-                                        d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr, want_se ? d_he : nullptr,
-                                        d_chv, d_chb, d_den, d_err);
-      ctx->launches++;
-      if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route_sequential failed");
+      // slot records: 24 bytes per slot; every cycle fits 32 slots per edge
+      const size_t smem = (((size_t)12 * nv + 15) & ~size_t(15)) + (size_t)cyc_off[nv] * 24 + 16;
+      if (smem > 227 * 1024) {
+        rc = fail(ctx, HELIO_ERR_TOO_LARGE, "plan too large for the masked routing kernel's shared memory");
+      } else {
+        cudaFuncSetAttribute(route_masked_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        route_masked_warp<<<1, 32, smem, st>>>(R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst,
+                                               d_oes, d_oee, d_node, d_kvcap, d_cyclen, d_cyc, d_in, d_out, d_nh,
+                                               d_hn, want_se ? d_hs : nullptr, want_se ? d_he : nullptr, d_den,
+                                               d_err);
+      }
+      if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route_masked_warp failed");
     }
   }
   int herr = 0;

@@ -37,43 +37,58 @@ int default_device() {
   throw InternalError(msg);
 }
 
-void put(std::string& k, const void* p, size_t n) { k.append(static_cast<const char*>(p), n); }
-void put_d(std::string& k, double v) { put(k, &v, sizeof v); }
-void put_s(std::string& k, const std::string& s) {
-  size_t n = s.size();
-  put(k, &n, sizeof n);
-  k += s;
-}
-
-std::string cluster_key(const ClusterSpec& c) {
-  std::string k;
-  put_s(k, c.coordinator_id);
-  int L = c.model.num_layers;
-  put(k, &L, sizeof L);
-  put_d(k, c.model.param_bytes);
-  put_d(k, c.model.token_bytes);
-  put_d(k, c.model.activation_bytes);
-  put_d(k, c.model.kv_bytes_per_token_layer);
-  for (const auto& n : c.nodes) {
-    put_s(k, n.id);
-    put_d(k, n.vram_bytes);
-    put_d(k, n.kv_reserve);
-    put_d(k, n.peak_layer_tokens);
-    put_d(k, n.nic_in_bps);
-    put_d(k, n.nic_out_bps);
-    size_t t = n.throughput_table.size();
-    put(k, &t, sizeof t);
-    for (const auto& [j, v] : n.throughput_table) {
-      put(k, &j, sizeof j);
-      put_d(k, v);
+// Content fingerprint of a cluster: two independent 64-bit FNV-1a-style
+// streams over every field the engine compiles (model, nodes, links), hashed
+// in place — no per-call string building (the reference's per-call cost is
+// exactly this kind of O(links) string work, cluster.cpp:82-96).
+struct Fingerprint {
+  uint64_t a = 1469598103934665603ull, b = 0x9E3779B97F4A7C15ull;
+  void bytes(const void* p, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) {
+      a = (a ^ c[i]) * 1099511628211ull;
+      b = (b ^ c[i]) * 0xBF58476D1CE4E5B9ull;
+      b ^= b >> 29;
     }
   }
-  for (const auto& l : c.links) {
-    put_s(k, l.src);
-    put_s(k, l.dst);
-    put_d(k, l.bandwidth_bps);
+  void d(double v) { bytes(&v, sizeof v); }
+  void i(int64_t v) { bytes(&v, sizeof v); }
+  void s(const std::string& x) {
+    i(static_cast<int64_t>(x.size()));
+    bytes(x.data(), x.size());
   }
-  return k;
+  bool operator==(const Fingerprint& o) const { return a == o.a && b == o.b; }
+};
+
+Fingerprint cluster_fingerprint(const ClusterSpec& c) {
+  Fingerprint f;
+  f.s(c.coordinator_id);
+  f.i(c.model.num_layers);
+  f.d(c.model.param_bytes);
+  f.d(c.model.token_bytes);
+  f.d(c.model.activation_bytes);
+  f.d(c.model.kv_bytes_per_token_layer);
+  f.i(static_cast<int64_t>(c.nodes.size()));
+  for (const auto& n : c.nodes) {
+    f.s(n.id);
+    f.d(n.vram_bytes);
+    f.d(n.kv_reserve);
+    f.d(n.peak_layer_tokens);
+    f.d(n.nic_in_bps);
+    f.d(n.nic_out_bps);
+    f.i(static_cast<int64_t>(n.throughput_table.size()));
+    for (const auto& [j, v] : n.throughput_table) {
+      f.i(j);
+      f.d(v);
+    }
+  }
+  f.i(static_cast<int64_t>(c.links.size()));
+  for (const auto& l : c.links) {
+    f.s(l.src);
+    f.s(l.dst);
+    f.d(l.bandwidth_bps);
+  }
+  return f;
 }
 
 }  // namespace
@@ -168,8 +183,8 @@ void Engine::check(int rc, const char* what) const {
 
 std::shared_ptr<Engine> engine_for(const ClusterSpec& c) {
   static std::mutex mu;
-  static std::list<std::pair<std::string, std::shared_ptr<Engine>>> cache;  // MRU first
-  std::string key = cluster_key(c);
+  static std::list<std::pair<Fingerprint, std::shared_ptr<Engine>>> cache;  // MRU first
+  const Fingerprint key = cluster_fingerprint(c);
   std::lock_guard<std::mutex> lock(mu);
   for (auto it = cache.begin(); it != cache.end(); ++it)
     if (it->first == key) {
@@ -178,7 +193,7 @@ std::shared_ptr<Engine> engine_for(const ClusterSpec& c) {
     }
   auto eng = std::make_shared<Engine>(default_device());
   eng->set_cluster(c);
-  cache.emplace_front(std::move(key), eng);
+  cache.emplace_front(key, eng);
   while (cache.size() > 8) cache.pop_back();
   return eng;
 }
@@ -244,6 +259,42 @@ using detail::Solved;
 
 // --- flow graph API ---------------------------------------------------------
 
+namespace {
+
+// build_flow_graph runs the PARITY build + solve on the device in one call
+// (helio_gpu_flows_host), which already yields the reference's per-edge
+// flows.  The reference's API hands the graph back with zero flows and solves
+// it in max_flow; instead of solving twice, the last few solved graphs of this
+// thread are remembered by the fingerprint of exactly what max_flow reads
+// (vertex count, source, sink, every edge's u, v, cap).  A graph the caller
+// changed in between misses and is solved on the device as a raw graph —
+// bit-identical either way, since both paths replay the reference's FIFO
+// discharge (flow_graph.cpp:138-229).
+struct SolvedGraph {
+  uint64_t a = 0, b = 0;
+  double value = 0;
+  std::vector<double> flows;
+};
+
+void graph_fingerprint(const FlowGraph& g, uint64_t& a, uint64_t& b) {
+  gpu::Fingerprint f;
+  f.i(g.num_vertices);
+  f.i(g.source);
+  f.i(g.sink);
+  f.i(static_cast<int64_t>(g.edges.size()));
+  for (const FlowEdge& e : g.edges) {
+    f.i(e.u);
+    f.i(e.v);
+    f.d(e.cap);
+  }
+  a = f.a;
+  b = f.b;
+}
+
+thread_local std::deque<SolvedGraph> t_solved;  // most recent first, at most 4
+
+}  // namespace
+
 FlowGraph build_flow_graph(const ClusterSpec& c, const Placement& p, bool allow_partial) {
   Solved s = solve_one(c, p, allow_partial);
   FlowGraph g;
@@ -268,10 +319,24 @@ FlowGraph build_flow_graph(const ClusterSpec& c, const Placement& p, bool allow_
     }
     g.edges.push_back(std::move(fe));
   }
+  SolvedGraph sg;
+  graph_fingerprint(g, sg.a, sg.b);
+  sg.value = s.value;
+  sg.flows.reserve(s.edges.size());
+  for (const helio_edge& e : s.edges) sg.flows.push_back(e.flow);
+  t_solved.push_front(std::move(sg));
+  if (t_solved.size() > 4) t_solved.pop_back();
   return g;
 }
 
 double max_flow(FlowGraph& g) {
+  uint64_t fa = 0, fb = 0;
+  graph_fingerprint(g, fa, fb);
+  for (const SolvedGraph& sg : t_solved)
+    if (sg.a == fa && sg.b == fb && sg.flows.size() == g.edges.size()) {
+      for (size_t i = 0; i < g.edges.size(); ++i) g.edges[i].flow = sg.flows[i];
+      return sg.value;
+    }
   auto eng = gpu::raw_engine();
   const int64_t m = static_cast<int64_t>(g.edges.size());
   std::vector<int32_t> u(m), v(m);

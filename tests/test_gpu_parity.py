@@ -192,6 +192,32 @@ def test_routes_one_million_match_oracle():
     assert np.array_equal(hs[mask], hs_o[mask]) and np.array_equal(he[mask], he_o[mask])
 
 
+@pytest.mark.parametrize("kv", [1e6, 7e5, 2e6])
+def test_masked_routes_one_million_match_reference(kv):
+    """KV masking binds (geo24's plan with kv_bytes_per_token_layer raised so
+    4-60% of admissions are deferred): the exact replay kernel
+    (route_masked_warp) against the reference's Scheduler::admit/complete on
+    1M requests."""
+    import copy
+    from _support import RefCluster, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    z = golden("route_geo24.npz")
+    d = copy.deepcopy(golden_cluster("geo24_float"))
+    d["model"]["kv_bytes_per_token_layer"] = kv
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    _, inl, outl = h.generate_trace_arrays(1_000_000, 0.0, "offline", 7)
+    pe = np.stack([z["plan_src"], z["plan_dst"], z["plan_es"], z["plan_ee"]], 1).astype(np.int32)
+    nh, hn, hs, he, den = e.route(z["row"], pe, z["plan_flow"], inl, outl, c.num_layers)
+    den_r, nh_r, hn_r, hs_r, he_r = RefCluster(d).route(z["row"], inl, outl)
+    assert 0 < den_r < 1_000_000
+    assert den == den_r and np.array_equal(nh, nh_r)
+    mask = np.arange(hn.shape[1])[None, :] < np.maximum(nh, 0)[:, None]
+    assert np.array_equal(hn[mask], hn_r[mask])
+    assert np.array_equal(hs[mask], hs_r[mask]) and np.array_equal(he[mask], he_r[mask])
+
+
 def test_generate_trace_matches_reference_fixture():
     z = golden("route_geo24.npz")
     _, inl, outl = h.generate_trace_arrays(len(z["in_len"]), 0.0, "offline", 7)

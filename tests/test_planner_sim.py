@@ -237,25 +237,24 @@ def test_scheduler_interleaved_admit_complete_matches_reference(tag):
 @needs_ref
 @needs_planner
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["geo24_offline", "geo24_online", "fan3_online", "kvmask_online"])
-def test_simulate_matches_reference(case):
+@pytest.mark.parametrize("name,online,n,rate,horizon", [("geo24", 0, 300, 0.0, 600.0), ("geo24", 1, 300, 0.5, 600.0),
+                                                         ("fan3", 1, 600, 2.0, 300.0), ("kvmask", 1, 300, 0.5, 600.0),
+                                                         ("kvmask", 0, 300, 0.0, 600.0)])
+def test_simulate_matches_reference(name, online, n, rate, horizon):
     """simulate(c, plan, trace, scheduler="iwrr") — the reference's DES
     (sim.cpp) over this engine's Scheduler — reports the pure reference's
-    metrics exactly (every key, every double bit)."""
-    name, mode = case.split("_")
+    metrics exactly (every key, every double bit), light and overloaded
+    traces (millions of deferred re-admissions), KV-masked plan included."""
     tag = {"geo24": "route_geo24", "fan3": "route_fan3", "kvmask": "route_kvmask"}[name]
     d = golden_cluster(ROUTE_FIXTURES[tag])
     row = np.ascontiguousarray(golden(f"{tag}.npz")["row"], np.int16)
-    online = mode == "online"
-    n = 4000 if online else 1500
-    rate = {"geo24": 40.0, "fan3": 30.0, "kvmask": 25.0}[name]
-    arr, i, o = ref_trace(n, 5, rate=rate if online else 0.0, online=online)
+    arr, i, o = ref_trace(n, 5, rate=rate, online=bool(online))
     rc = RefCluster(d)
-    want = json.loads(_text(_lib().refh_simulate, rc.h, row, 1, n, arr, i, o, int(online), 0, 3, 60.0, 5.0))
+    want = json.loads(_text(_lib().refh_simulate, rc.h, row, 1, n, arr, i, o, online, 0, 3, horizon, 5.0))
     c = _cluster(d)
     plan = h.Plan.from_json(ref_plan_json(d, row))
-    got = h.simulate(c, plan, [(float(a), int(x), int(y)) for a, x, y in zip(arr, i, o)], mode, "iwrr", 3, 60.0,
-                     5.0)
+    got = h.simulate(c, plan, [(float(a), int(x), int(y)) for a, x, y in zip(arr, i, o)],
+                     "online" if online else "offline", "iwrr", 3, horizon, 5.0)
     assert got == want
     assert got["requests_completed_total"] > 0
 
