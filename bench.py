@@ -584,6 +584,73 @@ def bench_config(args, world):
             "l2": "GPU arm: L2 flushed (256 MB write) between timed steps"}
 
 
+def latency_leg(h, clusters, with_reference):
+    """Per-call latency of the reference-facing API (SURVEY.md §8(b) call
+    sites placement.cpp:358-359, :441-442, pymodule.cpp:170-171): p50 over
+    repeated single-placement calls of max_flow_value, plan_for_placement and
+    build_flow_graph + max_flow on het42-70b, beside the unmodified reference
+    doing the same call on one host thread; and the reference's MILP planner
+    (plan_placement) at AC5's settings on geo24 (acceptance_main.cpp:371-378)
+    running over this engine vs the pure reference."""
+    import numpy as np
+
+    out = {"workload": "het42-70b, the bench's first covering-chain placement; p50 of 200 calls"}
+    d = clusters.CONFIGS["het42-70b"]("float")
+    c = h.Cluster.from_json(json.dumps(d))
+    eng = h.Engine(c)
+    row = h.generate_host(list(eng.kmax), c.num_layers, SEED, 0, 1, 0)[0]
+    placement = {c.node_ids[k]: (int(row[k, 0]), int(row[k, 1])) for k in range(len(row)) if row[k, 1] > row[k, 0]}
+
+    def p50(fn, n=200):
+        fn()
+        ts = []
+        for _ in range(n):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return float(np.median(ts)) * 1e6
+
+    def pair():
+        g = h.build_flow_graph(c, placement)
+        return h.max_flow(g)
+
+    out["max_flow_value_us"] = p50(lambda: h.max_flow_value(c, placement))
+    out["plan_for_placement_us"] = p50(lambda: h.plan_for_placement(c, placement))
+    out["build_flow_graph_max_flow_us"] = p50(pair)
+    if with_reference:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from _support import RefCluster  # test infrastructure: reference timing only
+            rc = RefCluster(d)
+            r1 = np.ascontiguousarray(row[None], np.int16)
+            out["reference"] = {"build_flow_graph_max_flow_us": p50(lambda: rc.score(r1, True, 1)),
+                                "plan_from_placement_us": p50(lambda: rc.plan(row)),
+                                "cores": 1, "kind": "reference",
+                                "sample": "the same placement, one host thread, via ctypes (oracle/_ref)"}
+        except Exception as ex:  # reported, never fatal
+            out["reference"] = {"error": str(ex)}
+    # AC5: the reference's MILP over GPU scores vs the pure reference
+    try:
+        g = clusters.CONFIGS["geo24"]("float")
+        cg = h.Cluster.from_json(json.dumps(g))
+        t0 = time.perf_counter()
+        p = h.plan(cg, "milp", gap=0.05, node_budget=300, prune_degree=6, lex_tiebreak=False)
+        out["milp_ac5"] = {"seconds": time.perf_counter() - t0, "objective": p.objective,
+                           "call": "plan(c, 'milp', gap=0.05, node_budget=300, prune_degree=6, lex_tiebreak=False): "
+                                   "the reference's plan_placement linked over this engine (lib/libhelio_planner.so)"}
+        if with_reference:
+            from _support import RefCluster, plan_milp, ref  # test infrastructure: reference timing only
+            rc = RefCluster(g)
+            t0 = time.perf_counter()
+            obj, _, _, _, _ = plan_milp(ref(), "refh_", rc.h, len(g["nodes"]), True, gap=0.05, lex=False,
+                                        node_budget=300, prune=6.0)
+            out["milp_ac5"]["reference"] = {"seconds": time.perf_counter() - t0, "objective": obj,
+                                            "same_objective": bool(obj == p.objective)}
+    except Exception as ex:  # reported, never fatal
+        out["milp_ac5"] = {"error": str(ex)}
+    return out
+
+
 def run_reference(args):
     """--impl reference: the unmodified reference on the host cores, on this
     run's workload (RefArm: oracle/_ref only — no package import).  Each step
@@ -887,6 +954,12 @@ def main():
                 cfg_table = r
             else:
                 search = r
+    latency = None
+    if extras:
+        try:
+            latency = latency_leg(h, clusters, with_reference=not args.no_cpu_baseline)
+        except Exception as ex:  # reported, never fatal
+            latency = {"error": str(ex)}
     if world == 1 and headline and not args.no_routing:
         try:
             routing = routing_leg(h, clusters, local, sp, args.route_requests, with_reference=not args.no_cpu_baseline)
@@ -957,7 +1030,8 @@ def main():
             "weak_scaling": weak,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_pageable": e2e_pageable,
             "gpu_launches": launches,
-            "routing": routing, "other_configs": cfg_table, "split_pipeline": split, "search": search,
+            "routing": routing, "latency": latency, "other_configs": cfg_table, "split_pipeline": split,
+            "search": search,
             "clocks": clocks,
         }
         print(json.dumps(out))

@@ -286,6 +286,38 @@ int helio_gpu_iwrr_cycles(helio_gpu_ctx* ctx, int32_t nlists, const int32_t* h_o
 int helio_gpu_iwrr_picks(helio_gpu_ctx* ctx, const int64_t* h_weights, int32_t n, int64_t* h_round,
                          int64_t* h_idx, int32_t calls, const uint64_t* h_masks, int32_t* h_out);
 
+/* --- multi-GPU (csrc/multi.cu) ---------------------
+ *
+ * Ranked argmax, one process per GPU: this rank's shard [index_base,
+ * index_base + B) is reduced on the device to (best value, global index), the
+ * 16-byte records of all ranks are all-gathered over `nccl_comm` (an
+ * ncclComm_t) and reduced deterministically — max value, then min index, the
+ * first-wins strict '>' of tests/oracles/enumerate.hpp:59 over the global
+ * order — into d_best / d_index on every rank.  Stream ordered on `stream`
+ * (NULL = the context's stream); no host synchronisation. */
+int helio_gpu_argmax_ranked(helio_gpu_ctx* ctx, const double* d_values, const int32_t* d_status, int64_t B,
+                            int64_t index_base, double* d_best, int64_t* d_index, void* nccl_comm, void* stream);
+
+/* NCCL communicator helpers for callers without one: rank 0 draws the
+ * 128-byte unique id and sends it to every rank over the caller's channel. */
+int helio_gpu_nccl_unique_id(uint8_t* id128);
+int helio_gpu_nccl_comm_create(const uint8_t* id128, int32_t nranks, int32_t rank, int32_t device, void** comm);
+int helio_gpu_nccl_comm_destroy(void* comm);
+
+/* One process, several GPUs: one context per device; host batches are split
+ * into contiguous shards (one host thread per device) and the first maxima
+ * merged in index order. */
+typedef struct helio_gpu_multi helio_gpu_multi;
+int helio_gpu_multi_create(const int32_t* devices, int32_t n, helio_gpu_multi** out);
+void helio_gpu_multi_destroy(helio_gpu_multi* m);
+const char* helio_gpu_multi_last_error(const helio_gpu_multi* m);
+int32_t helio_gpu_multi_count(const helio_gpu_multi* m);
+helio_gpu_ctx* helio_gpu_multi_context(helio_gpu_multi* m, int32_t i);
+int helio_gpu_multi_set_cluster(helio_gpu_multi* m, const helio_cluster_desc* desc, int32_t* k_out);
+int helio_gpu_multi_set_mode(helio_gpu_multi* m, int mode);
+int helio_gpu_multi_score_best_host(helio_gpu_multi* m, const int16_t* h_placements, int64_t B, int allow_partial,
+                                    double* h_values, int32_t* h_status, double* h_best, int64_t* h_index);
+
 /* Introspection for benchmarks: kernels launched by this context so far, and
  * the device time (ms) of the last score call's dominant kernel. */
 int64_t helio_gpu_launch_count(const helio_gpu_ctx* ctx);

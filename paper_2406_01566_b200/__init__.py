@@ -37,6 +37,8 @@ from ._helio import (  # noqa: E402
     FlowGraph,
     InternalError,
     IwrrPicker,
+    MultiEngine,
+    NcclComm,
     ParseError,
     Plan,
     Scheduler,
@@ -51,6 +53,7 @@ from ._helio import (  # noqa: E402
     max_flow,
     max_flow_raw,
     max_flow_value,
+    nccl_unique_id,
     plan,
     plan_for_placement,
     prune_links,
@@ -103,4 +106,5 @@ __all__ = [
     "iwrr_weights", "max_flow", "max_flow_raw", "max_flow_value", "max_flow_values",
     "placement_rows", "plan_for_placement", "route_requests", "heuristic_placement", "local_search",
     "plan", "Scheduler", "simulate", "prune_links", "throughput_upper_bound", "generate_trace_arrays",
+    "MultiEngine", "NcclComm", "nccl_unique_id",
 ]

@@ -25,7 +25,7 @@ NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-f
               "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall", "-Wno-sign-compare"]
 
-CU_SOURCES = ["helio_gpu.cu", "route.cu", "search.cu", "split.cu"]
+CU_SOURCES = ["helio_gpu.cu", "route.cu", "search.cu", "split.cu", "multi.cu"]
 SHIM_SOURCES = ["shim_cluster.cpp", "shim_flow.cpp", "shim_plan.cpp", "shim_sched.cpp", "shim_heuristics.cpp"]
 HEADERS = ["engine.h", "gen.h", "device_common.cuh", "build.cuh", "solve_parity.cuh", "solve_score.cuh", "shim.hpp",
            "shim_engine.hpp", "helio/cluster.hpp", "helio/errors.hpp", "helio/flow_graph.hpp", "helio/placement.hpp",
@@ -67,7 +67,9 @@ def build(force: bool = False, verbose: bool = False) -> None:
         objs.append(o)
     libgpu = os.path.join(LIB, "libhelio_gpu.so")
     if force or _newer(libgpu, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", libgpu, *objs, "-lcudart_static"], quiet=not verbose)
+        # NCCL (the ranked argmax's all-gather): the system libnccl.so.2, the
+        # soname torch.distributed also loads, so both share one instance
+        _run([NVCC, *ARCH, "-shared", "-o", libgpu, *objs, "-lcudart_static", "-lnccl"], quiet=not verbose)
     if ptxas_log:
         with open(os.path.join(ROOT, "build", "ptxas.log"), "w") as f:
             f.write("\n".join(ptxas_log))

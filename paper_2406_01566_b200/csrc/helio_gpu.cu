@@ -1270,6 +1270,12 @@ int argmax_on(helio_gpu_ctx* ctx, int scratch, const double* d_values, const int
 }
 }  // namespace
 
+// The device argmax on the argmax scratch row (multi.cu's ranked argmax).
+int helio_engine_argmax(helio_gpu_ctx* ctx, const double* d_values, const int32_t* d_status, int64_t B,
+                        int64_t index_base, double* d_best, int64_t* d_index, cudaStream_t st) {
+  return argmax_on(ctx, helio_gpu_ctx::kSets, d_values, d_status, B, index_base, d_best, d_index, st);
+}
+
 extern "C" {
 
 int helio_gpu_argmax(helio_gpu_ctx* ctx, const double* d_values, const int32_t* d_status, int64_t B,

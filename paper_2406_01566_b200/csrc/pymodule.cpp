@@ -440,6 +440,20 @@ struct PyScheduler {
   std::unique_ptr<Scheduler> sched;
 };
 
+// NCCL communicator and multi-device handles (csrc/multi.cu).
+struct PyComm {
+  void* comm = nullptr;
+  ~PyComm() { helio_gpu_nccl_comm_destroy(comm); }
+};
+
+struct PyMulti {
+  helio_gpu_multi* m = nullptr;
+  int N = 0;
+  std::vector<int32_t> kmax;
+  std::string mode = "parity";
+  ~PyMulti() { helio_gpu_multi_destroy(m); }
+};
+
 // --- batched engine handle ---------------------------------------------------
 
 struct PyEngine {
@@ -969,6 +983,94 @@ PYBIND11_MODULE(_helio, m) {
       py::arg("kmax"), py::arg("num_layers"), py::arg("seed"), py::arg("first"), py::arg("count"),
       py::arg("p_uniform_ppm") = 0);
 
+  m.def("nccl_unique_id", [] {
+    std::string id(128, '\0');
+    if (helio_gpu_nccl_unique_id(reinterpret_cast<uint8_t*>(&id[0])) != HELIO_OK)
+      throw InternalError("ncclGetUniqueId failed");
+    return py::bytes(id);
+  }, "128-byte NCCL unique id (rank 0 draws it and sends it to every rank).");
+
+  py::class_<PyComm>(m, "NcclComm")
+      .def(py::init([](py::bytes id, int nranks, int rank, int device) {
+             std::string s = id;
+             if (s.size() != 128) throw ValidationError("NCCL unique id must be 128 bytes");
+             auto c = std::make_unique<PyComm>();
+             int rc;
+             {
+               py::gil_scoped_release rel;
+               rc = helio_gpu_nccl_comm_create(reinterpret_cast<const uint8_t*>(s.data()), nranks, rank, device,
+                                               &c->comm);
+             }
+             if (rc != HELIO_OK) throw InternalError("ncclCommInitRank failed");
+             return c;
+           }),
+           py::arg("unique_id"), py::arg("nranks"), py::arg("rank"), py::arg("device"))
+      .def_property_readonly("handle", [](const PyComm& c) { return reinterpret_cast<uintptr_t>(c.comm); });
+
+  py::class_<PyMulti>(m, "MultiEngine")
+      .def(py::init([](const ClusterSpec& c, const std::vector<int32_t>& devices) {
+             auto pm = std::make_unique<PyMulti>();
+             int rc = helio_gpu_multi_create(devices.data(), (int32_t)devices.size(), &pm->m);
+             if (rc != HELIO_OK)
+               throw InternalError("helio: cannot create contexts on the requested devices (helio_gpu_multi_create "
+                                   "returned " + std::to_string(rc) + "); this build has no CPU fallback");
+             gpu::ClusterDesc desc;
+             gpu::make_cluster_desc(c, desc);
+             pm->kmax.assign(c.nodes.size(), 0);
+             rc = helio_gpu_multi_set_cluster(pm->m, &desc.d, pm->kmax.data());
+             if (rc != HELIO_OK) throw ValidationError(helio_gpu_multi_last_error(pm->m));
+             pm->N = (int)c.nodes.size();
+             return pm;
+           }),
+           py::arg("cluster"), py::arg("devices"))
+      .def_property_readonly("count", [](const PyMulti& p) { return helio_gpu_multi_count(p.m); })
+      .def_property_readonly("kmax", [](const PyMulti& p) { return p.kmax; })
+      .def_property(
+          "mode", [](const PyMulti& p) { return p.mode; },
+          [](PyMulti& p, const std::string& mode) {
+            if (mode != "parity" && mode != "score") throw ValidationError("mode must be 'parity' or 'score'");
+            if (helio_gpu_multi_set_mode(p.m, mode == "score" ? HELIO_MODE_SCORE : HELIO_MODE_PARITY) != HELIO_OK)
+              throw InternalError(helio_gpu_multi_last_error(p.m));
+            p.mode = mode;
+          })
+      .def(
+          "score_best",
+          [](PyMulti& p, const py::array& placements, bool allow_partial) {
+            auto rows = as_rows(placements, p.N);
+            const int64_t B = rows.shape(0);
+            py::array_t<double> vals(B);
+            py::array_t<int32_t> st(B);
+            double best = 0;
+            int64_t idx = -1;
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = helio_gpu_multi_score_best_host(p.m, rows.data(), B, allow_partial ? 1 : 0, vals.mutable_data(),
+                                                   st.mutable_data(), &best, &idx);
+            }
+            if (rc != HELIO_OK) throw InternalError(helio_gpu_multi_last_error(p.m));
+            return py::make_tuple(vals, st, best, idx);
+          },
+          py::arg("placements"), py::arg("allow_partial") = true,
+          "Score a host batch split over the devices: (values, status, best value, first-max index).")
+      .def(
+          "score_best_host_ptr",
+          [](PyMulti& p, uintptr_t pl, int64_t B, uintptr_t vals, uintptr_t st, bool allow_partial) {
+            double best = 0;
+            int64_t idx = -1;
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = helio_gpu_multi_score_best_host(p.m, reinterpret_cast<const int16_t*>(pl), B, allow_partial ? 1 : 0,
+                                                   reinterpret_cast<double*>(vals), reinterpret_cast<int32_t*>(st),
+                                                   &best, &idx);
+            }
+            if (rc != HELIO_OK) throw InternalError(helio_gpu_multi_last_error(p.m));
+            return py::make_tuple(best, idx);
+          },
+          py::arg("placements_ptr"), py::arg("count"), py::arg("values_ptr"), py::arg("status_ptr"),
+          py::arg("allow_partial") = true);
+
   py::class_<PyEngine>(m, "Engine")
       .def(py::init([](const ClusterSpec& c, int device) {
              auto pe = new PyEngine();
@@ -1095,6 +1197,20 @@ PYBIND11_MODULE(_helio, m) {
           },
           py::arg("values_ptr"), py::arg("status_ptr"), py::arg("count"), py::arg("index_base"), py::arg("best_ptr"),
           py::arg("index_ptr"), py::arg("stream") = 0)
+      .def(
+          "argmax_ranked",
+          [](PyEngine& e, uintptr_t values, uintptr_t status, int64_t B, int64_t base, uintptr_t best, uintptr_t index,
+             uintptr_t comm, uintptr_t stream) {
+            e.eng->check(helio_gpu_argmax_ranked(e.eng->ctx(), reinterpret_cast<const double*>(values),
+                                                 reinterpret_cast<const int32_t*>(status), B, base,
+                                                 reinterpret_cast<double*>(best), reinterpret_cast<int64_t*>(index),
+                                                 reinterpret_cast<void*>(comm), reinterpret_cast<void*>(stream)),
+                         "helio_gpu_argmax_ranked");
+          },
+          py::arg("values_ptr"), py::arg("status_ptr"), py::arg("count"), py::arg("index_base"), py::arg("best_ptr"),
+          py::arg("index_ptr"), py::arg("comm"), py::arg("stream") = 0,
+          "This rank's shard argmax, all-gathered over the NCCL communicator `comm` (NcclComm.handle) and reduced "
+          "to the global first maximum on every rank (device pointers, stream ordered).")
       .def("flows", &engine_flows, py::arg("placements"), py::arg("allow_partial") = true, py::arg("max_edges") = 0,
            "(values, status, num_vertices, num_edges, int32 [K,E,8] {u,v,kind,exec_start,exec_end,src,dst,0}, "
            "float64 [K,E,2] {cap,flow})")

@@ -33,6 +33,19 @@ const std::string& node_name(const ClusterSpec& c, int idx);
 
 namespace gpu {
 
+// The C-ABI cluster descriptor of a ClusterSpec (arrays owned here).
+// Throws ValidationError on duplicate ids or a non-contiguous throughput table.
+struct ClusterDesc {
+  helio_cluster_desc d{};
+  std::vector<double> vram, kvr, peak, nin, nout, tval, lbw;
+  std::vector<int32_t> toff, rank, lsrc, ldst;
+  ClusterDesc() = default;
+  ClusterDesc(const ClusterDesc&) = delete;
+  ClusterDesc& operator=(const ClusterDesc&) = delete;
+  ClusterDesc& operator=(ClusterDesc&&) = default;
+};
+void make_cluster_desc(const ClusterSpec& c, ClusterDesc& out);
+
 // One engine context bound to a device with one compiled cluster.
 class Engine {
  public:

@@ -103,38 +103,43 @@ Engine::Engine(int device) : device_(device) {
 
 Engine::~Engine() { helio_gpu_destroy(ctx_); }
 
-void Engine::set_cluster(const ClusterSpec& c) {
+void make_cluster_desc(const ClusterSpec& c, ClusterDesc& out) {
   const int N = static_cast<int>(c.nodes.size());
   std::set<std::string> seen;
   for (const auto& n : c.nodes)
     if (!seen.insert(n.id).second) throw ValidationError("duplicate node id '" + n.id + "'");
-  std::vector<double> vram(N), kvr(N), peak(N), nin(N), nout(N), tval;
-  std::vector<int32_t> toff(N + 1, 0), rank(N), lsrc, ldst;
-  std::vector<double> lbw;
+  out = ClusterDesc{};
+  out.vram.resize(N);
+  out.kvr.resize(N);
+  out.peak.resize(N);
+  out.nin.resize(N);
+  out.nout.resize(N);
+  out.toff.assign(N + 1, 0);
+  out.rank.resize(N);
   bool any_table = false;
   for (int i = 0; i < N; ++i) {
     const NodeSpec& n = c.nodes[i];
-    vram[i] = n.vram_bytes;
-    kvr[i] = n.kv_reserve;
-    peak[i] = n.peak_layer_tokens;
-    nin[i] = n.nic_in_bps;
-    nout[i] = n.nic_out_bps;
-    toff[i] = static_cast<int32_t>(tval.size());
+    out.vram[i] = n.vram_bytes;
+    out.kvr[i] = n.kv_reserve;
+    out.peak[i] = n.peak_layer_tokens;
+    out.nin[i] = n.nic_in_bps;
+    out.nout[i] = n.nic_out_bps;
+    out.toff[i] = static_cast<int32_t>(out.tval.size());
     if (!n.throughput_table.empty()) {
       any_table = true;
       int expect = 1;
       for (const auto& [j, v] : n.throughput_table) {
         if (j != expect) throw ValidationError("node '" + n.id + "': throughput_table keys must be contiguous from 1");
-        tval.push_back(v);
+        out.tval.push_back(v);
         ++expect;
       }
     }
   }
-  toff[N] = static_cast<int32_t>(tval.size());
+  out.toff[N] = static_cast<int32_t>(out.tval.size());
   std::vector<int> order(N);
   for (int i = 0; i < N; ++i) order[i] = i;
   std::sort(order.begin(), order.end(), [&](int a, int b) { return c.nodes[a].id < c.nodes[b].id; });
-  for (int r = 0; r < N; ++r) rank[order[r]] = r;
+  for (int r = 0; r < N; ++r) out.rank[order[r]] = r;
   std::map<std::string, int> idx;
   for (int i = 0; i < N; ++i) idx[c.nodes[i].id] = i;
   auto endpoint = [&](const std::string& id) {
@@ -143,11 +148,11 @@ void Engine::set_cluster(const ClusterSpec& c) {
     return it == idx.end() ? -2 : it->second;
   };
   for (const auto& l : c.links) {
-    lsrc.push_back(endpoint(l.src));
-    ldst.push_back(endpoint(l.dst));
-    lbw.push_back(l.bandwidth_bps);
+    out.lsrc.push_back(endpoint(l.src));
+    out.ldst.push_back(endpoint(l.dst));
+    out.lbw.push_back(l.bandwidth_bps);
   }
-  helio_cluster_desc d{};
+  helio_cluster_desc& d = out.d;
   d.num_nodes = N;
   d.num_links = static_cast<int32_t>(c.links.size());
   d.num_layers = c.model.num_layers;
@@ -155,19 +160,25 @@ void Engine::set_cluster(const ClusterSpec& c) {
   d.token_bytes = c.model.token_bytes;
   d.activation_bytes = c.model.activation_bytes;
   d.kv_bytes_per_token_layer = c.model.kv_bytes_per_token_layer;
-  d.vram_bytes = vram.data();
-  d.kv_reserve = kvr.data();
-  d.peak_layer_tokens = peak.data();
-  d.nic_in_bps = nin.data();
-  d.nic_out_bps = nout.data();
-  d.table_off = any_table ? toff.data() : nullptr;
-  d.table_val = any_table ? tval.data() : nullptr;
-  d.lex_rank = rank.data();
-  d.link_src = lsrc.data();
-  d.link_dst = ldst.data();
-  d.link_bandwidth_bps = lbw.data();
+  d.vram_bytes = out.vram.data();
+  d.kv_reserve = out.kvr.data();
+  d.peak_layer_tokens = out.peak.data();
+  d.nic_in_bps = out.nin.data();
+  d.nic_out_bps = out.nout.data();
+  d.table_off = any_table ? out.toff.data() : nullptr;
+  d.table_val = any_table ? out.tval.data() : nullptr;
+  d.lex_rank = out.rank.data();
+  d.link_src = out.lsrc.data();
+  d.link_dst = out.ldst.data();
+  d.link_bandwidth_bps = out.lbw.data();
+}
+
+void Engine::set_cluster(const ClusterSpec& c) {
+  const int N = static_cast<int>(c.nodes.size());
+  ClusterDesc desc;
+  make_cluster_desc(c, desc);
   kmax_.assign(N, 0);
-  int rc = helio_gpu_set_cluster(ctx_, &d, kmax_.data());
+  int rc = helio_gpu_set_cluster(ctx_, &desc.d, kmax_.data());
   if (rc != HELIO_OK) engine_fail(ctx_, rc, "helio_gpu_set_cluster");
   N_ = N;
   ids_.clear();
