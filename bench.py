@@ -37,7 +37,7 @@ WORKLOAD = ("het42-70b: covering-chain placements (SURVEY.md §8(d) G(seed,i)) o
 SEED = 20240611
 # --config other than the headline: the BASELINE configs as extra bench lines
 # (sparse topologies draw link-walking placements)
-WALK_CONFIGS = {"syn256-120l", "geo24-70b"}
+WALK_CONFIGS = {"syn256-120l", "geo24-70b", "het42-70b-prune12"}
 
 
 def workload_of(name):
@@ -404,6 +404,7 @@ OTHER_CONFIGS = [
     ("single24-30b", "float", "chain", 100_000),
     ("geo24", "float", "chain", 100_000),
     ("het42-70b", "int", "chain", 100_000),
+    ("het42-70b-prune12", "float", "walk", 100_000),
     ("syn256-120l", "float", "walk", 20_000),
 ]
 

@@ -67,9 +67,9 @@ def build(force: bool = False, verbose: bool = False) -> None:
         objs.append(o)
     libgpu = os.path.join(LIB, "libhelio_gpu.so")
     if force or _newer(libgpu, objs):
-        # NCCL (the ranked argmax's all-gather): the system libnccl.so.2, the
-        # soname torch.distributed also loads, so both share one instance
-        _run([NVCC, *ARCH, "-shared", "-o", libgpu, *objs, "-lcudart_static", "-lnccl"], quiet=not verbose)
+        # NCCL (the ranked argmax's all-gather) is bound at run time
+        # (multi.cu nccl_api), never linked: torch needs its own newer copy
+        _run([NVCC, *ARCH, "-shared", "-o", libgpu, *objs, "-lcudart_static", "-ldl"], quiet=not verbose)
     if ptxas_log:
         with open(os.path.join(ROOT, "build", "ptxas.log"), "w") as f:
             f.write("\n".join(ptxas_log))

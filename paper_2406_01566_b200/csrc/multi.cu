@@ -14,9 +14,11 @@
 // * multi-device (one process, several GPUs): helio_gpu_multi_* own one
 //   context per device; host batches are split across them with one host
 //   thread per device and the per-device first maxima merged on the host.
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: NCCL is resolved at run time (nccl_api below)
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -31,6 +33,41 @@ int helio_engine_argmax(helio_gpu_ctx* ctx, const double* d_values, const int32_
                         int64_t index_base, double* d_best, int64_t* d_index, cudaStream_t st);
 
 namespace {
+
+// NCCL is bound lazily, never as a load-time dependency: a process that also
+// uses torch.distributed must share torch's libnccl.so.2 (whose newer symbols
+// torch needs), so the library already loaded under that soname is used when
+// there is one (RTLD_NOLOAD), else $HELIO_NCCL_LIB, else the system
+// libnccl.so.2.  The Python bindings import torch first when it is installed.
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclCommCount) comm_count = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  bool ok = false;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+    if (!h) {
+      const char* env = std::getenv("HELIO_NCCL_LIB");
+      if (env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.comm_count = reinterpret_cast<decltype(api.comm_count)>(dlsym(h, "ncclCommCount"));
+    api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
+    api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.comm_count && api.all_gather;
+  });
+  return api;
+}
 
 __global__ void pack_record(const double* __restrict__ best, const int64_t* __restrict__ index,
                             long long* __restrict__ rec) {
@@ -69,8 +106,10 @@ extern "C" {
 
 int helio_gpu_nccl_unique_id(uint8_t* id128) {
   if (!id128) return HELIO_ERR_INVALID;
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) return HELIO_ERR_CUDA;
   ncclUniqueId id;
-  if (ncclGetUniqueId(&id) != ncclSuccess) return HELIO_ERR_CUDA;
+  if (nc.get_unique_id(&id) != ncclSuccess) return HELIO_ERR_CUDA;
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
   std::memcpy(id128, &id, 128);
   return HELIO_OK;
@@ -78,18 +117,22 @@ int helio_gpu_nccl_unique_id(uint8_t* id128) {
 
 int helio_gpu_nccl_comm_create(const uint8_t* id128, int32_t nranks, int32_t rank, int32_t device, void** comm) {
   if (!id128 || !comm || nranks < 1 || rank < 0 || rank >= nranks) return HELIO_ERR_INVALID;
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) return HELIO_ERR_CUDA;
   if (cudaSetDevice(device) != cudaSuccess) return HELIO_ERR_CUDA;
   ncclUniqueId id;
   std::memcpy(&id, id128, 128);
   ncclComm_t c = nullptr;
-  if (ncclCommInitRank(&c, nranks, id, rank) != ncclSuccess) return HELIO_ERR_CUDA;
+  if (nc.comm_init_rank(&c, nranks, id, rank) != ncclSuccess) return HELIO_ERR_CUDA;
   *comm = c;
   return HELIO_OK;
 }
 
 int helio_gpu_nccl_comm_destroy(void* comm) {
   if (!comm) return HELIO_OK;
-  return ncclCommDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? HELIO_OK : HELIO_ERR_CUDA;
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) return HELIO_ERR_CUDA;
+  return nc.comm_destroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? HELIO_OK : HELIO_ERR_CUDA;
 }
 
 int helio_gpu_argmax_ranked(helio_gpu_ctx* ctx, const double* d_values, const int32_t* d_status, int64_t B,
@@ -100,9 +143,11 @@ int helio_gpu_argmax_ranked(helio_gpu_ctx* ctx, const double* d_values, const in
     return fail(ctx, HELIO_ERR_INVALID, "bad buffers");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) return fail(ctx, HELIO_ERR_CUDA, "NCCL (libnccl.so.2) could not be loaded");
   ncclComm_t c = static_cast<ncclComm_t>(comm);
   int n = 0;
-  if (ncclCommCount(c, &n) != ncclSuccess || n < 1) return fail(ctx, HELIO_ERR_CUDA, "ncclCommCount failed");
+  if (nc.comm_count(c, &n) != ncclSuccess || n < 1) return fail(ctx, HELIO_ERR_CUDA, "ncclCommCount failed");
   // records: [0, 2) this rank's, [2, 2 + 2n) everyone's — in the context's
   // host-entry arena (grow-only; this call is stream ordered on `st`, so the
   // arena's synchronous host users are ordered behind it by api_begin/end)
@@ -115,7 +160,7 @@ int helio_gpu_argmax_ranked(helio_gpu_ctx* ctx, const double* d_values, const in
   rc = helio_engine_argmax(ctx, d_values, d_status, B, index_base, d_best, d_index, st);
   if (rc) return rc;
   pack_record<<<1, 1, 0, st>>>(d_best, d_index, rec);
-  if (ncclAllGather(rec, all, 2, ncclInt64, c, st) != ncclSuccess)
+  if (nc.all_gather(rec, all, 2, ncclInt64, c, st) != ncclSuccess)
     return fail(ctx, HELIO_ERR_CUDA, "ncclAllGather failed");
   reduce_records<<<1, 1, 0, st>>>(all, n, d_best, d_index);
   CK(cudaGetLastError());

@@ -983,7 +983,16 @@ PYBIND11_MODULE(_helio, m) {
       py::arg("kmax"), py::arg("num_layers"), py::arg("seed"), py::arg("first"), py::arg("count"),
       py::arg("p_uniform_ppm") = 0);
 
-  m.def("nccl_unique_id", [] {
+  // torch.distributed, when installed, must own the process's libnccl.so.2
+  // (multi.cu binds whichever copy is loaded): import it before NCCL is used
+  auto nccl_prepare = [] {
+    try {
+      py::module_::import("torch");
+    } catch (py::error_already_set&) {
+    }
+  };
+  m.def("nccl_unique_id", [nccl_prepare] {
+    nccl_prepare();
     std::string id(128, '\0');
     if (helio_gpu_nccl_unique_id(reinterpret_cast<uint8_t*>(&id[0])) != HELIO_OK)
       throw InternalError("ncclGetUniqueId failed");
@@ -991,7 +1000,8 @@ PYBIND11_MODULE(_helio, m) {
   }, "128-byte NCCL unique id (rank 0 draws it and sends it to every rank).");
 
   py::class_<PyComm>(m, "NcclComm")
-      .def(py::init([](py::bytes id, int nranks, int rank, int device) {
+      .def(py::init([nccl_prepare](py::bytes id, int nranks, int rank, int device) {
+             nccl_prepare();
              std::string s = id;
              if (s.size() != 128) throw ValidationError("NCCL unique id must be 128 bytes");
              auto c = std::make_unique<PyComm>();

@@ -131,6 +131,10 @@ __global__ void route_apply(int64_t R, int x, int L, int max_hops, const int32_t
 // (it does not depend on it).  A deferred request leaves the positions it
 // advanced, as IwrrPicker::next does (scheduler.cpp:165-168 rolls back only
 // the KV charges).
+// REG: every vertex's (cycle base, cycle length, position) lives in the
+// registers of lane x (plans with at most 32 vertices — one coordinator plus
+// up to 31 placed nodes); otherwise in shared memory.
+template <bool REG>
 __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double kvb,
                                   const int32_t* __restrict__ obeg, const int32_t* __restrict__ odst,
                                   const int32_t* __restrict__ oes, const int32_t* __restrict__ oee,
@@ -144,50 +148,61 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
   // Slot-ordered records: vertex x's cycle occupies slots [base_x, base_x +
   // W_x); slot k carries its edge's (threshold, exec length) as doubles and
   // (dst, exec_start, exec_end, node of dst) as int16, so a pick costs one
-  // vertex load and one slot load.  Threshold = 0.9 * kv_cap[dst]; the
-  // coordinator never masks (+inf).
-  int32_t* vbase = reinterpret_cast<int32_t*>(sm);
-  int32_t* vW = vbase + nv;
-  int32_t* vpos = vW + nv;
-  double2* srec = reinterpret_cast<double2*>(sm + (((size_t)12 * nv + 15) & ~size_t(15)));
-  int W_tot = 0;  // every lane computes the same prefix
+  // slot load.  Threshold = 0.9 * kv_cap[dst]; the coordinator never masks.
+  int32_t* vstate = reinterpret_cast<int32_t*>(sm);  // [nv][4]: base, W, pos, -
+  double2* srec = reinterpret_cast<double2*>(sm + (((size_t)16 * nv + 15) & ~size_t(15)));
+  int W_tot = 0;
+  int my_base = 0, my_W = 0, my_pos = 0;
   for (int x = 0; x < nv; ++x) {
     const int W = obeg[x + 1] > obeg[x] ? cyc_len[x] : 0;
-    if (lane == 0) {
-      vbase[x] = W_tot;
-      vW[x] = W;
-      vpos[x] = 0;
+    if (REG && lane == x) {
+      my_base = W_tot;
+      my_W = W;
+    }
+    if (!REG && lane == 0) {
+      vstate[4 * x] = W_tot;
+      vstate[4 * x + 1] = W;
+      vstate[4 * x + 2] = 0;
     }
     W_tot += W;
   }
   short4* smeta = reinterpret_cast<short4*>(srec + W_tot);
-  for (int x = 0; x < nv; ++x) {
+  for (int x = 0, base = 0; x < nv; ++x) {
     const int W = obeg[x + 1] > obeg[x] ? cyc_len[x] : 0;
-    int base = 0;
-    for (int y = 0; y < x; ++y) base += obeg[y + 1] > obeg[y] ? cyc_len[y] : 0;
     for (int k = lane; k < W; k += 32) {
       const int e = obeg[x] + cyc[32 * obeg[x] + k];
       const int d = odst[e];
       srec[base + k] = make_double2(d == 0 ? 1.0e308 : 0.9 * kv_cap[d], (double)(oee[e] - oes[e]));
       smeta[base + k] = make_short4((short)d, (short)oes[e], (short)oee[e], (short)node_of[d]);
     }
+    base += W;
   }
   __syncwarp();
   double avg = 232.0, samples = 1.0;
   long long den = 0;
+  const bool store_hops = max_hops > 0;
   for (int64_t r0 = 0; r0 < R; r0 += 32) {
     const int nb = R - r0 < 32 ? (int)(R - r0) : 32;
     const int my_in = lane < nb ? in_len[r0 + lane] : 0;
     const int my_out = lane < nb ? out_len[r0 + lane] : 0;
+    int my_nh = 0;
     for (int j = 0; j < nb; ++j) {
-      const int64_t r = r0 + j;
       const int in = __shfl_sync(0xffffffffu, my_in, j);
-      const int out = __shfl_sync(0xffffffffu, my_out, j);
       const double tk = ((double)in + avg) * kvb;  // hop_charge = tk * (exec_end - exec_start)
       int v = 0, covered = 0, h = 0;
       bool ok = true;
-      while (covered < L) {
-        const int base = vbase[v], W = vW[v], p = vpos[v];
+      do {
+        int base, W, p;
+        if (REG) {
+          base = __shfl_sync(0xffffffffu, my_base, v);
+          W = __shfl_sync(0xffffffffu, my_W, v);
+          p = __shfl_sync(0xffffffffu, my_pos, v);
+        } else {
+          const int4 vs = reinterpret_cast<const int4*>(vstate)[v];
+          base = vs.x;
+          W = vs.y;
+          p = vs.z;
+        }
         if (W == 0) {  // no out-edges: IwrrPicker::next returns -1
           ok = false;
           break;
@@ -195,7 +210,7 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
         // the slot at the current position first (the common case), then
         // the rest of one full cycle 32 slots at a time
         int slot = base + p, np = p + 1 == W ? 0 : p + 1;
-        double2 rc = srec[slot];
+        const double2 rc = srec[slot];
         if (!(tk * rc.y <= rc.x)) {
           slot = -1;
           for (int k0 = 1; k0 < W; k0 += 32) {
@@ -224,34 +239,38 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
           }
         }
         const short4 mt = smeta[slot];
-        const int d = mt.x;
-        if (d == 0 || mt.y != covered) {  // scheduler.cpp:170-171
+        if (mt.x == 0 || mt.y != covered) {  // scheduler.cpp:170-171
           if (lane == 0) atomicExch(err, 1);
           return;
         }
-        if (lane == 0) {
-          vpos[v] = np;
-          if (h < max_hops) {
-            hop_node[r * max_hops + h] = mt.w;
-            if (hop_s) {
-              hop_s[r * max_hops + h] = mt.y;
-              hop_e[r * max_hops + h] = mt.z;
-            }
+        if (REG) {
+          if (lane == v) my_pos = np;
+        } else {
+          if (lane == 0) vstate[4 * v + 2] = np;
+          __syncwarp();
+        }
+        if (store_hops && lane == 0 && h < max_hops) {
+          const int64_t at = (r0 + j) * max_hops + h;
+          hop_node[at] = mt.w;
+          if (hop_s) {
+            hop_s[at] = mt.y;
+            hop_e[at] = mt.z;
           }
         }
-        __syncwarp();
         ++h;
         covered = mt.z;
-        v = d;
-      }
+        v = mt.x;
+      } while (covered < L);
       if (ok) {  // complete(): the running mean (scheduler.cpp:183-190)
+        const int out = __shfl_sync(0xffffffffu, my_out, j);
         samples += 1.0;
         avg += ((double)out - avg) / samples;
       } else {
         ++den;
       }
-      if (lane == 0) nh[r] = ok ? h : -1;
+      if (lane == j) my_nh = ok ? h : -1;
     }
+    if (lane < nb) nh[r0 + lane] = my_nh;
   }
   if (lane == 0) *deferred = den;
 }
@@ -465,15 +484,15 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   } else if (!rc && R > 0) {
     {
       // slot records: 24 bytes per slot; every cycle fits 32 slots per edge
-      const size_t smem = (((size_t)12 * nv + 15) & ~size_t(15)) + (size_t)cyc_off[nv] * 24 + 16;
+      const size_t smem = (((size_t)16 * nv + 15) & ~size_t(15)) + (size_t)cyc_off[nv] * 24 + 16;
       if (smem > 227 * 1024) {
         rc = fail(ctx, HELIO_ERR_TOO_LARGE, "plan too large for the masked routing kernel's shared memory");
       } else {
-        cudaFuncSetAttribute(route_masked_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        route_masked_warp<<<1, 32, smem, st>>>(R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst,
-                                               d_oes, d_oee, d_node, d_kvcap, d_cyclen, d_cyc, d_in, d_out, d_nh,
-                                               d_hn, want_se ? d_hs : nullptr, want_se ? d_he : nullptr, d_den,
-                                               d_err);
+        auto kern = nv <= 32 ? route_masked_warp<true> : route_masked_warp<false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<1, 32, smem, st>>>(R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst, d_oes, d_oee, d_node,
+                                  d_kvcap, d_cyclen, d_cyc, d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr,
+                                  want_se ? d_he : nullptr, d_den, d_err);
       }
       if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route_masked_warp failed");
     }

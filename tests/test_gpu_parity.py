@@ -218,6 +218,38 @@ def test_masked_routes_one_million_match_reference(kv):
     assert np.array_equal(hs[mask], hs_r[mask]) and np.array_equal(he[mask], he_r[mask])
 
 
+@pytest.mark.parametrize("cap", ["float", "int"])
+def test_het42_prune12_variant_bit_exact_against_reference(cap):
+    """het42 after the reference's prune_links(c, 12)
+    (1,806 -> 588 links): seeded covering chains and uniform mixes scored in
+    PARITY are the reference's doubles bit for bit; SCORE within 1e-6 (exact on
+    integer capacities)."""
+    from _support import RefCluster, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    d = clusters.CONFIGS["het42-70b-prune12"](cap)
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    assert c.num_links == 588
+    rc = RefCluster(d)
+    # link walks (the pruned mesh is sparse: plain chains rarely connect) and
+    # a uniform-interval mix
+    rows = np.concatenate([rc.generate(31, 0, 3000, 0, True, 8),
+                           h.generate_host(list(e.kmax), c.num_layers, 32, 0, 1000, 150_000)])
+    assert np.array_equal(e.generate_walk_host(31, 0, 3000), rows[:3000])
+    vr, sr = rc.score(rows, True, 8)
+    v, s = e.score(rows)
+    assert np.array_equal(s, sr) and np.array_equal(bits(v), bits(vr))
+    assert (vr > 0).mean() > 0.2
+    e.mode = "score"
+    v2, s2 = e.score(rows)
+    assert np.array_equal(s2, sr)
+    if cap == "int":
+        assert np.array_equal(bits(v2), bits(vr))
+    else:
+        assert np.all(np.abs(v2 - vr) <= 1e-6 * np.maximum(1.0, np.abs(vr)))
+
+
 def test_generate_trace_matches_reference_fixture():
     z = golden("route_geo24.npz")
     _, inl, outl = h.generate_trace_arrays(len(z["in_len"]), 0.0, "offline", 7)

@@ -55,9 +55,10 @@ def test_multi_engine_equals_one_engine(mode):
     assert np.array_equal(bits(v1), bits(v2)) and np.array_equal(s1, s2)
     assert (best, idx) == _first_max(v1, s1)
     # ties across the shard boundary: the lower global index wins
-    tie = np.repeat(rows[:1], 6, axis=0)
+    tie = np.repeat(rows[1:2], 6, axis=0)
+    assert s1[1] == 0 and v1[1] > 0
     _, _, bt, it = m.score_best(tie)
-    assert it == 0 and bt == e.score(tie[:1])[0][0]
+    assert it == 0 and bt == v1[1]
 
 
 def _free_port():
