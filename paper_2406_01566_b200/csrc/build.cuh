@@ -201,17 +201,44 @@ __device__ __forceinline__ bool edge_ok(int aend, int bs, int be, int partial) {
   return partial ? (bs <= aend && aend < be) : (aend == bs);
 }
 
+// Valid out-links of node k (end e): calls f(j, link) for every declared
+// link k -> j whose head's interval chains from e (flow_graph.cpp:121), in
+// out-list order.  Four links per step: their global and shared loads are
+// independent, so a step costs one round trip of each instead of one per link.
+template <class F>
+__device__ __forceinline__ void for_valid_out_links(const ClusterDev& cd, const int32_t* pse, int k, int e,
+                                                    int partial, F&& f) {
+  const int pb = __ldg(cd.out_beg + k), pend = __ldg(cd.out_beg + k + 1);
+  for (int p = pb; p < pend; p += 4) {
+    const int n4 = min(4, pend - p);
+    int2 jl[4];
+    int32_t iv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) jl[q] = q < n4 ? __ldg(&cd.out_list[p + q]) : make_int2(0, -1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) iv[q] = q < n4 ? pse[jl[q].x] : 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int sj = (int16_t)(iv[q] & 0xffff), ej = (int16_t)(iv[q] >> 16);
+      if (q < n4 && ej > sj && edge_ok(e, sj, ej, partial)) f(jl[q].x, jl[q].y);
+    }
+  }
+}
+
+// SCORE builder for N > 64 (sparse interconnects): per used node, one pass
+// over its compiled out-link list.  Intervals are kept packed (start | end <<
+// 16, the row's own int32 words) over the ps/pe scratch.
 __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
                                  int partial, int lane, int& V, int& E) {
   const int N = cd.N, L = cd.L;
+  int32_t* pse = reinterpret_cast<int32_t*>(g.ps);  // ps/pe: 4N contiguous bytes, 4-aligned
   int bad = INT_MAX;
   const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
   for (int k = lane; k < N; k += 32) {
     const int32_t w = __ldg(row32 + k);
     const int s = (int16_t)(w & 0xffff);
     const int e = (int16_t)(w >> 16);
-    g.ps[k] = (int16_t)s;
-    g.pe[k] = (int16_t)e;
+    pse[k] = w;
     if (e > s) {
       int code = 0;
       if (s < 0 || e > L) code = 2;
@@ -232,18 +259,15 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
   for (int x = lane; x < V; x += 32) fill[x] = 0;
   __syncwarp();
   for (int k = lane; k < N; k += 32) {
-    const int s = g.ps[k], e = g.pe[k];
+    const int32_t w = pse[k];
+    const int s = (int16_t)(w & 0xffff), e = (int16_t)(w >> 16);
     if (e <= s) continue;
     int din = 1, dout = 1;
     ++nedges;
-    for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
-      const int j = __ldg(&cd.out_list[p].x);
-      const int sj = g.ps[j], ej = g.pe[j];
-      if (ej > sj && edge_ok(e, sj, ej, partial)) {
-        ++dout;
-        atomicAdd(&fill[2 + 2 * j], 1);
-      }
-    }
+    for_valid_out_links(cd, pse, k, e, partial, [&](int j, int) {
+      ++dout;
+      atomicAdd(&fill[2 + 2 * j], 1);
+    });
     nedges += dout - 1;  // each link edge counted once, at its source
     if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
       ++din;
@@ -291,7 +315,8 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
   // arcs: each lane places its node's compute pair and every edge it
   // sources; the paired reverse arc takes the next free slot at its head.
   for (int k = lane; k < N; k += 32) {
-    const int s = g.ps[k], e = g.pe[k];
+    const int32_t w = pse[k];
+    const int s = (int16_t)(w & 0xffff), e = (int16_t)(w >> 16);
     if (e <= s) continue;
     const int vi = 2 + 2 * k, vo = vi + 1;
     const int ai = g.abeg[vi];
@@ -302,20 +327,17 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
     g.to[ao] = (int16_t)vi;
     g.rv[ao] = (int16_t)ai;
     g.cap[ao] = 0.0;
-    for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
-      const int2 jl = __ldg(&cd.out_list[p]);
-      const int sj = g.ps[jl.x], ej = g.pe[jl.x];
-      if (!(ej > sj && edge_ok(e, sj, ej, partial))) continue;
-      const int vj = 2 + 2 * jl.x;
-      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+    for_valid_out_links(cd, pse, k, e, partial, [&](int j, int link) {
+      const int vj = 2 + 2 * j;
+      const int fa = ao + atomicAdd(&fill[vo], 1);
       const int ra = g.abeg[vj] + atomicAdd(&fill[vj], 1);
       g.to[fa] = (int16_t)vj;
       g.rv[fa] = (int16_t)ra;
-      g.cap[fa] = __ldg(cd.link_cap + jl.y);
+      g.cap[fa] = __ldg(cd.link_cap + link);
       g.to[ra] = (int16_t)vo;
       g.rv[ra] = (int16_t)fa;
       g.cap[ra] = 0.0;
-    }
+    });
     const int lc = __ldg(cd.cout_link + k);
     if (s == 0 && lc >= 0) {
       const int fa = g.abeg[0] + atomicAdd(&fill[0], 1);

@@ -85,6 +85,9 @@ struct helio_gpu_ctx {
   int slot_warps[2] = {4, 4};
   bool slot_big_ok[2] = {false, false};
   int mode = 0;  // HELIO_MODE_PARITY
+  // SCORE path: general builder + push-relabel when split graphs exceed 128
+  // vertices (N >= 64), else the cover-mask builder + bitset Edmonds-Karp
+  bool score_gen = false;
   bool big_ok = false;
 
   // scratch sets: kPipeSets for the host-buffer pipeline (one per stream;

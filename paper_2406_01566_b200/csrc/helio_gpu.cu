@@ -5,11 +5,13 @@
 //   device_common.cuh  shared-memory slot layout, per-warp views, warp helpers
 //   build.cuh          K1: placement row -> flow network in shared memory
 //   solve_parity.cuh   K2 PARITY: bit-exact FIFO preflow-push replay + read-out
-//   solve_score.cuh    K2 SCORE: value-only Edmonds-Karp (bitset / queue BFS)
+//   solve_score.cuh    K2 SCORE: value-only bitset Edmonds-Karp (V <= 128) and
+//                      push-relabel with global relabels (larger graphs)
 //
 // Kernels here (SIMT; the path is FP64 min/add/compare graph work — no tensor
 // cores):
-//   score_kernel<MODE>  placement rows -> graph -> max-flow value, one warp per
+//   score_kernel_{parity,small,gen} (score_body<MODE, GEN>)
+//                       placement rows -> graph -> max-flow value, one warp per
 //                       graph, persistent CTAs pulling work from an atomic
 //                       counter; graphs whose arcs exceed the small slot are
 //                       queued for the same kernel with a middle slot (twice
@@ -65,8 +67,12 @@ struct FlowOut {
 // candidates, graphs whose arcs exceed the slot appended to ovf; tier 1: the
 // ovf list, overflows appended to ovf2 when it is given (middle slot) or
 // reported HELIO_CAND_TOO_LARGE (big slot); tier 2: the ovf2 list (big slot).
-template <int MODE>
-__global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restrict__ pl, int64_t B,
+// GEN (SCORE only): an instantiation with only the general builder and the
+// push-relabel solver, for clusters whose split graphs exceed 128 vertices
+// (N >= 64), so that path's register allocation is its own; the default one
+// keeps both paths (het42 runs it at 64 registers, 8 CTAs per SM).
+template <int MODE, bool GEN>
+__device__ __forceinline__ void score_body(ClusterDev cd, Layout lay, const int16_t* __restrict__ pl, int64_t B,
                              int partial, double* __restrict__ values, int32_t* __restrict__ status,
                              unsigned long long* work, int64_t* ovf, int64_t* ovf2, unsigned int* ovf_count,
                              int tier, FlowOut fo) {
@@ -84,8 +90,8 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     int V = 0, E = 0;
     double cut = 1.0e300;  // SCORE, N <= 64: the builder's layer cut (an upper bound to stop at)
     int st = MODE == HELIO_MODE_SCORE
-                 ? (cd.out_mask ? build_graph_score_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E, cut)
-                                : build_graph_score(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E))
+                 ? (!GEN && cd.out_mask ? build_graph_score_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E, cut)
+                                        : build_graph_score(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E))
                  : (cd.less_cout && !fo.edges
                         ? build_graph_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
                         : build_graph(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E));
@@ -98,7 +104,7 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     }
     double value = 0.0;
     if (st == 0 && MODE == HELIO_MODE_SCORE) {
-      value = V <= 128          ? solve_ek_bits(g, V, 0, 1, lane, cut)
+      value = !GEN && V <= 128  ? solve_ek_bits(g, V, 0, 1, lane, cut)
               : cd.large_solver ? solve_ek_batched(g, V, 0, 1, lane)
                                 : solve_pr(g, V, 0, 1, lane, cd.pr_gr);
     } else if (st == 0) {
@@ -120,6 +126,42 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     __syncwarp();
   }
 }
+
+// The three instantiations as separate kernels, so each gets its own
+// register budget: PARITY and the N <= 64 SCORE path capped at 64 registers
+// (8 four-warp CTAs per SM; uncapped, ptxas picks 72-80 for them on their
+// own); the general SCORE path (one-warp CTAs, 8 per SM by shared memory)
+// at the compiler's choice.
+#ifndef HELIO_SMALL_MAXNREG
+#define HELIO_SMALL_MAXNREG 64
+#endif
+#define SCORE_KERNEL_ARGS                                                                              \
+  ClusterDev cd, Layout lay, const int16_t *__restrict__ pl, int64_t B, int partial,                  \
+      double *__restrict__ values, int32_t *__restrict__ status, unsigned long long *work, int64_t *ovf, \
+      int64_t *ovf2, unsigned int *ovf_count, int tier, FlowOut fo
+#define SCORE_KERNEL_PASS cd, lay, pl, B, partial, values, status, work, ovf, ovf2, ovf_count, tier, fo
+__global__ void __maxnreg__(64) score_kernel_parity(SCORE_KERNEL_ARGS) {
+  score_body<HELIO_MODE_PARITY, false>(SCORE_KERNEL_PASS);
+}
+__global__ void __maxnreg__(HELIO_SMALL_MAXNREG) score_kernel_small(SCORE_KERNEL_ARGS) {
+  score_body<HELIO_MODE_SCORE, false>(SCORE_KERNEL_PASS);
+}
+__global__ void score_kernel_gen(SCORE_KERNEL_ARGS) { score_body<HELIO_MODE_SCORE, true>(SCORE_KERNEL_PASS); }
+
+template <int MODE, bool GEN>
+struct ScoreKernel;
+template <>
+struct ScoreKernel<HELIO_MODE_PARITY, false> {
+  static constexpr auto fn = score_kernel_parity;
+};
+template <>
+struct ScoreKernel<HELIO_MODE_SCORE, false> {
+  static constexpr auto fn = score_kernel_small;
+};
+template <>
+struct ScoreKernel<HELIO_MODE_SCORE, true> {
+  static constexpr auto fn = score_kernel_gen;
+};
 
 // ---------------------------------------------------------------------------
 // max_flow on raw graphs.  Arc construction follows :140-145 literally (lane
@@ -383,8 +425,9 @@ int configure_layouts(helio_gpu_ctx* ctx) {
     }
   }
   // occupancy of both instantiations (PARITY / SCORE)
-  void* fns[2] = {reinterpret_cast<void*>(score_kernel<HELIO_MODE_PARITY>),
-                  reinterpret_cast<void*>(score_kernel<HELIO_MODE_SCORE>)};
+  void* fns[2] = {reinterpret_cast<void*>(score_kernel_parity),
+                  ctx->score_gen ? reinterpret_cast<void*>(score_kernel_gen)
+                                 : reinterpret_cast<void*>(score_kernel_small)};
   for (int m = 0; m < 2; ++m) {
     CK(cudaFuncSetAttribute(fns[m], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem));
     // the whole unified L1/shared array as shared memory: the driver's default
@@ -425,7 +468,7 @@ int ensure_ovf(helio_gpu_ctx* ctx, int set, int64_t B) {
   return HELIO_OK;
 }
 
-template <int MODE>
+template <int MODE, bool GEN = false>
 void launch_score_mode(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, int partial, double* d_val,
                        int32_t* d_st, cudaStream_t st, FlowOut fo, bool timed) {
   unsigned long long* work = ctx->d_work + 16 + 3 * set;
@@ -436,22 +479,22 @@ void launch_score_mode(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t
   const Layout& sl = ctx->slot_small[MODE];
   const int warps = ctx->slot_warps[MODE];
   const int grid = (int)std::min<int64_t>(ctx->small_blocks[MODE], (B + warps - 1) / warps);
-  score_kernel<MODE><<<grid, 32 * warps, sl.bytes * warps, st>>>(ctx->cd, sl, d_pl, B, partial, d_val, d_st, work,
-                                                                 l1, l2, oc, 0, fo);
+  ScoreKernel<MODE, GEN>::fn<<<grid, 32 * warps, sl.bytes * warps, st>>>(ctx->cd, sl, d_pl, B, partial, d_val, d_st,
+                                                                      work, l1, l2, oc, 0, fo);
   // graphs that overflowed the small slot: the same kernel with the middle
   // slot, then whatever overflows that with the big slot (one warp per CTA)
   const Layout& bl = ctx->slot_big_ok[MODE] ? ctx->slot_big[MODE] : sl;
   if (ctx->slot_mid_ok[MODE]) {
     const Layout& ml = ctx->slot_mid[MODE];
     const int wm = ctx->mid_warps[MODE];
-    score_kernel<MODE><<<ctx->mid_blocks[MODE], 32 * wm, ml.bytes * wm, st>>>(
+    ScoreKernel<MODE, GEN>::fn<<<ctx->mid_blocks[MODE], 32 * wm, ml.bytes * wm, st>>>(
         ctx->cd, ml, d_pl, B, partial, d_val, d_st, work + 1, l1, l2, oc, 1, fo);
-    score_kernel<MODE><<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
-                                                                     work + 2, l1, l2, oc, 2, fo);
+    ScoreKernel<MODE, GEN>::fn<<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
+                                                                          work + 2, l1, l2, oc, 2, fo);
     ctx->launches += 1;
   } else {
-    score_kernel<MODE><<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
-                                                                     work + 2, l1, nullptr, oc, 1, fo);
+    ScoreKernel<MODE, GEN>::fn<<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
+                                                                          work + 2, l1, nullptr, oc, 1, fo);
   }
   // kernel time = all tier launches (small, middle, big)
   if (timed) cudaEventRecord(ctx->ev1, st);
@@ -464,8 +507,10 @@ int launch_score(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, in
   if (rc) return rc;
   CK(cudaMemsetAsync(ctx->d_work + 16 + 3 * set, 0, 3 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(ctx->d_ovf_count + 2 * set, 0, 2 * sizeof(unsigned int), st));
-  if (mode == HELIO_MODE_SCORE && fo.edges == nullptr && fo.nv == nullptr)
-    launch_score_mode<HELIO_MODE_SCORE>(ctx, set, d_pl, B, partial, d_val, d_st, st, fo, timed);
+  if (mode == HELIO_MODE_SCORE && fo.edges == nullptr && fo.nv == nullptr && ctx->score_gen)
+    launch_score_mode<HELIO_MODE_SCORE, true>(ctx, set, d_pl, B, partial, d_val, d_st, st, fo, timed);
+  else if (mode == HELIO_MODE_SCORE && fo.edges == nullptr && fo.nv == nullptr)
+    launch_score_mode<HELIO_MODE_SCORE, false>(ctx, set, d_pl, B, partial, d_val, d_st, st, fo, timed);
   else
     launch_score_mode<HELIO_MODE_PARITY>(ctx, set, d_pl, B, partial, d_val, d_st, st, fo, timed);
   CK(cudaGetLastError());
@@ -876,6 +921,7 @@ int helio_gpu_set_cluster(helio_gpu_ctx* ctx, const helio_cluster_desc* d, int32
   ctx->kv_token_layer_bytes =
       d->kv_bytes_per_token_layer > 0 ? d->kv_bytes_per_token_layer : 2.0 * d->activation_bytes;
   ctx->has_cluster = true;
+  ctx->score_gen = 2 * N + 2 > 128;
   int rc = configure_layouts(ctx);
   if (rc) {
     ctx->has_cluster = false;

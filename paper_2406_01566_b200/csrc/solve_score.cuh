@@ -306,17 +306,40 @@ __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, c
       int v = -1;
       if (u >= 0) {
         e = g.ex[u];
-        if (e > 0.0)
-          for (; a < ae; ++a) {
-            const int w = g.to[a];
-            if (g.h[w] == hu - 1) {
-              c = g.cap[a];
-              if (c > FLOW_EPS) {
-                v = w;
-                break;
-              }
+        if (e > 0.0) {
+          // the first admissible arc at or after `a`, four arcs per step:
+          // their loads are independent, so one step costs two shared-memory
+          // round trips instead of two per arc
+          const int hw = hu - 1;
+          while (a < ae) {
+            const int n4 = min(4, ae - a);
+            int w[4], hh[4];
+            double cc[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              w[k] = k < n4 ? g.to[a + k] : 0;
+              cc[k] = k < n4 ? g.cap[a + k] : 0.0;
             }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) hh[k] = k < n4 ? g.h[w[k]] : -2;
+            int kk = -1, vk = -1;
+            double ck = 0.0;
+#pragma unroll
+            for (int k = 3; k >= 0; --k)
+              if (hh[k] == hw && cc[k] > FLOW_EPS) {
+                kk = k;
+                vk = w[k];
+                ck = cc[k];
+              }
+            if (kk >= 0) {
+              a += kk;
+              v = vk;
+              c = ck;
+              break;
+            }
+            a += n4;
           }
+        }
       }
       const unsigned pm = __ballot_sync(FULL, v >= 0);
       if (pm == 0u) break;
@@ -351,8 +374,19 @@ __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, c
     int nl = -1;
     if (u >= 0 && g.ex[u] > 0.0) {
       int best = n;
-      for (int b2 = g.abeg[u]; b2 < ae; ++b2)
-        if (g.cap[b2] > FLOW_EPS) best = min(best, g.h[g.to[b2]] + 1);
+      for (int b2 = g.abeg[u]; b2 < ae; b2 += 4) {  // four independent arcs per step
+        const int n4 = min(4, ae - b2);
+        int w[4];
+        double cc[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          w[k] = k < n4 ? g.to[b2 + k] : 0;
+          cc[k] = k < n4 ? g.cap[b2 + k] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (cc[k] > FLOW_EPS) best = min(best, g.h[w[k]] + 1);
+      }
       nl = best;
     }
     __syncwarp();
