@@ -365,6 +365,150 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
   return 0;
 }
 
+// The round-1 general builder (one out-link per step), kept for the combined
+// small-cluster kernel, whose register allocation is tuned with it.
+__device__ int build_graph_score_r1(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
+                                 int partial, int lane, int& V, int& E) {
+  const int N = cd.N, L = cd.L;
+  int bad = INT_MAX;
+  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = __ldg(row32 + k);
+    const int s = (int16_t)(w & 0xffff);
+    const int e = (int16_t)(w >> 16);
+    g.ps[k] = (int16_t)s;
+    g.pe[k] = (int16_t)e;
+    if (e > s) {
+      int code = 0;
+      if (s < 0 || e > L) code = 2;
+      else if (e - s > __ldg(cd.kmax + k)) code = 3;
+      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
+    }
+  }
+  bad = __reduce_min_sync(FULL, bad);
+  if (bad != INT_MAX) return bad & 3;
+  V = 2 + 2 * N;
+  if (V > lay.V) return ST_OVERFLOW;
+  __syncwarp();
+  // degrees: in_k = compute + valid in-links + source arc; out_k = compute +
+  // valid out-links + sink arc.  One pass over the out-lists: a valid link
+  // k -> j adds to out_k here and to in_j through a shared atomic.
+  int nedges = 0, dsrc = 0, dsink = 0;
+  int* fill = reinterpret_cast<int*>(g.ex);  // int counters per vertex during the build
+  for (int x = lane; x < V; x += 32) fill[x] = 0;
+  __syncwarp();
+  for (int k = lane; k < N; k += 32) {
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    int din = 1, dout = 1;
+    ++nedges;
+    for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
+      const int j = __ldg(&cd.out_list[p].x);
+      const int sj = g.ps[j], ej = g.pe[j];
+      if (ej > sj && edge_ok(e, sj, ej, partial)) {
+        ++dout;
+        atomicAdd(&fill[2 + 2 * j], 1);
+      }
+    }
+    nedges += dout - 1;  // each link edge counted once, at its source
+    if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
+      ++din;
+      ++dsrc;
+      ++nedges;
+    }
+    if (e == L && __ldg(cd.cin_link + k) >= 0) {
+      ++dout;
+      ++dsink;
+      ++nedges;
+    }
+    atomicAdd(&fill[2 + 2 * k], din);
+    fill[3 + 2 * k] = dout;  // only this lane touches an out-vertex's count
+  }
+  nedges = __reduce_add_sync(FULL, nedges);
+  dsrc = __reduce_add_sync(FULL, dsrc);
+  dsink = __reduce_add_sync(FULL, dsink);
+  E = nedges;
+  if (2 * E > lay.A) return ST_OVERFLOW;
+  if (lane == 0) {
+    fill[0] = dsrc;
+    fill[1] = dsink;
+  }
+  __syncwarp();
+  // arc ranges; each used node's compute pair takes slot 0 of both its
+  // vertices (so the pair arc of x >= 2 is arc abeg[x]), the rest fill in.
+  int run = 0;
+  for (int x0 = 0; x0 < V; x0 += 32) {
+    const int x = x0 + lane;
+    const int d = x < V ? fill[x] : 0;
+    int incl = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (x < V) {
+      g.abeg[x] = (int16_t)(run + incl - d);
+      fill[x] = (x >= 2 && d > 0) ? 1 : 0;
+    }
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) g.abeg[V] = (int16_t)run;
+  __syncwarp();
+  // arcs: each lane places its node's compute pair and every edge it
+  // sources; the paired reverse arc takes the next free slot at its head.
+  for (int k = lane; k < N; k += 32) {
+    const int s = g.ps[k], e = g.pe[k];
+    if (e <= s) continue;
+    const int vi = 2 + 2 * k, vo = vi + 1;
+    const int ai = g.abeg[vi];
+    const int ao = g.abeg[vo];
+    g.to[ai] = (int16_t)vo;
+    g.rv[ai] = (int16_t)ao;
+    g.cap[ai] = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
+    g.to[ao] = (int16_t)vi;
+    g.rv[ao] = (int16_t)ai;
+    g.cap[ao] = 0.0;
+    for (int p = __ldg(cd.out_beg + k), pe_ = __ldg(cd.out_beg + k + 1); p < pe_; ++p) {
+      const int2 jl = __ldg(&cd.out_list[p]);
+      const int sj = g.ps[jl.x], ej = g.pe[jl.x];
+      if (!(ej > sj && edge_ok(e, sj, ej, partial))) continue;
+      const int vj = 2 + 2 * jl.x;
+      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+      const int ra = g.abeg[vj] + atomicAdd(&fill[vj], 1);
+      g.to[fa] = (int16_t)vj;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + jl.y);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    const int lc = __ldg(cd.cout_link + k);
+    if (s == 0 && lc >= 0) {
+      const int fa = g.abeg[0] + atomicAdd(&fill[0], 1);
+      const int ra = g.abeg[vi] + atomicAdd(&fill[vi], 1);
+      g.to[fa] = (int16_t)vi;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lc);
+      g.to[ra] = 0;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+    const int lk = __ldg(cd.cin_link + k);
+    if (e == L && lk >= 0) {
+      const int fa = g.abeg[vo] + atomicAdd(&fill[vo], 1);
+      const int ra = g.abeg[1] + atomicAdd(&fill[1], 1);
+      g.to[fa] = 1;
+      g.rv[fa] = (int16_t)ra;
+      g.cap[fa] = __ldg(cd.link_cap + lk);
+      g.to[ra] = (int16_t)vo;
+      g.rv[ra] = (int16_t)fa;
+      g.cap[ra] = 0.0;
+    }
+  }
+  __syncwarp();
+  return 0;
+}
+
 // SCORE builder for N <= 64: node sets are 64-bit words.  cover[l] = nodes
 // whose interval contains layer l, start[l] = nodes starting at l.  Node i's
 // valid successors are (partial ? cover[e_i] : start[e_i]) & out_mask[i]

@@ -95,10 +95,17 @@ struct helio_gpu_ctx {
   // to release the SMs, never holds up the following H2D), plus kApiSet for
   // the device-pointer entries and search.cu
   static constexpr int kPipeSets = 3, kApiSet = 3, kSets = 4;
-  unsigned long long* d_work = nullptr;  // [32]: raw [0], split.cu [8]/[9], set k [16+3k, 16+3k+2]
-  unsigned int* d_ovf_count = nullptr;   // [2 * kSets]: small -> mid, mid -> big
+  unsigned long long* d_work = nullptr;  // [32]: raw [0], split.cu [8]/[9], set k [16+4k, 16+4k+3]
+  unsigned int* d_ovf_count = nullptr;   // [3 * kSets]: small -> mid, mid -> big, big -> global
   int64_t* d_ovf[kSets] = {nullptr, nullptr, nullptr, nullptr};   // small-slot overflows
   int64_t* d_ovf2[kSets] = {nullptr, nullptr, nullptr, nullptr};  // mid-slot overflows
+  int64_t* d_ovf3[kSets] = {nullptr, nullptr, nullptr, nullptr};  // big-slot overflows (global tier)
+  // global-memory tier: per-mode slot for the structural maximum when the big
+  // slot cannot hold it; one slot per warp of glob_warps one-warp CTAs
+  helio_engine::Layout slot_glob[2]{};
+  bool glob_ok[2] = {false, false};
+  int glob_warps = 0;
+  char* d_glob = nullptr;
   int64_t ovf_cap[kSets] = {0, 0, 0, 0};
   double* d_pv = nullptr;      // argmax partials: kSets + 1 scratch rows of 4096
   long long* d_pi = nullptr;

@@ -10,7 +10,7 @@
 //
 // Kernels here (SIMT; the path is FP64 min/add/compare graph work — no tensor
 // cores):
-//   score_kernel_{parity,small,gen} (score_body<MODE, GEN>)
+//   score_kernel<MODE, GEN>
 //                       placement rows -> graph -> max-flow value, one warp per
 //                       graph, persistent CTAs pulling work from an atomic
 //                       counter; graphs whose arcs exceed the small slot are
@@ -63,41 +63,49 @@ struct FlowOut {
   int max_e;
 };
 
-// Persistent: every warp loops fetching candidate indices.  tier 0: all B
-// candidates, graphs whose arcs exceed the slot appended to ovf; tier 1: the
-// ovf list, overflows appended to ovf2 when it is given (middle slot) or
-// reported HELIO_CAND_TOO_LARGE (big slot); tier 2: the ovf2 list (big slot).
+// Persistent: every warp loops fetching candidate indices — all B of them
+// (in_list == nullptr) or the *in_count entries of in_list.  Graphs whose arcs
+// exceed this launch's slot are appended to out_list for the next tier, or
+// reported HELIO_CAND_TOO_LARGE when there is none.  Tiers (launch_score_mode):
+// small slot -> middle slot -> big slot (one warp per CTA, every declared link)
+// -> a slot in global memory (gbase != nullptr: clusters whose structural
+// maximum does not fit one SM's shared memory; L1/L2 cached).
 // GEN (SCORE only): an instantiation with only the general builder and the
 // push-relabel solver, for clusters whose split graphs exceed 128 vertices
 // (N >= 64), so that path's register allocation is its own; the default one
 // keeps both paths (het42 runs it at 64 registers, 8 CTAs per SM).
-template <int MODE, bool GEN>
-__device__ __forceinline__ void score_body(ClusterDev cd, Layout lay, const int16_t* __restrict__ pl, int64_t B,
-                             int partial, double* __restrict__ values, int32_t* __restrict__ status,
-                             unsigned long long* work, int64_t* ovf, int64_t* ovf2, unsigned int* ovf_count,
-                             int tier, FlowOut fo) {
+template <int MODE, bool GEN, bool GLOBAL = false>
+__global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restrict__ pl, int64_t B,
+                                           int partial, double* __restrict__ values, int32_t* __restrict__ status,
+                                           unsigned long long* work, const int64_t* in_list,
+                                           const unsigned int* in_count, int64_t* out_list, unsigned int* out_count,
+                                           char* gbase, FlowOut fo) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const Gs g = slot_view(smem + wib * lay.bytes, lay);
-  const int64_t total = tier ? (int64_t)ovf_count[tier - 1] : B;
+  // GLOBAL is a template parameter so the shared-memory instantiations keep
+  // statically shared addressing (32-bit LDS/STS, not generic 64-bit)
+  char* slot = GLOBAL ? gbase + ((size_t)blockIdx.x * (blockDim.x >> 5) + wib) * lay.bytes : smem + wib * lay.bytes;
+  const Gs g = slot_view(slot, lay);
+  const int64_t total = in_list ? (int64_t)*in_count : B;
   for (;;) {
     unsigned long long w = 0;
     if (lane == 0) w = atomicAdd(work, 1ull);
     w = __shfl_sync(FULL, w, 0);
     if ((int64_t)w >= total) break;
-    const int64_t b = tier == 0 ? (int64_t)w : (tier == 1 ? ovf : ovf2)[w];
+    const int64_t b = in_list ? in_list[w] : (int64_t)w;
     int V = 0, E = 0;
     double cut = 1.0e300;  // SCORE, N <= 64: the builder's layer cut (an upper bound to stop at)
     int st = MODE == HELIO_MODE_SCORE
                  ? (!GEN && cd.out_mask ? build_graph_score_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E, cut)
-                                        : build_graph_score(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E))
+                 : GEN                  ? build_graph_score(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
+                                        : build_graph_score_r1(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E))
                  : (cd.less_cout && !fo.edges
                         ? build_graph_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
                         : build_graph(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E));
     if (st == ST_OVERFLOW) {
-      if (tier == 0 || (tier == 1 && ovf2)) {
-        if (lane == 0) (tier == 0 ? ovf : ovf2)[atomicAdd(ovf_count + tier, 1u)] = b;
+      if (out_list) {
+        if (lane == 0) out_list[atomicAdd(out_count, 1u)] = b;
         continue;
       }
       st = HELIO_CAND_TOO_LARGE;
@@ -106,7 +114,7 @@ __device__ __forceinline__ void score_body(ClusterDev cd, Layout lay, const int1
     if (st == 0 && MODE == HELIO_MODE_SCORE) {
       value = !GEN && V <= 128  ? solve_ek_bits(g, V, 0, 1, lane, cut)
               : cd.large_solver ? solve_ek_batched(g, V, 0, 1, lane)
-                                : solve_pr(g, V, 0, 1, lane, cd.pr_gr);
+                                : solve_pr<GEN>(g, V, 0, 1, lane, cd.pr_gr);
     } else if (st == 0) {
       solve_fifo2(g, V, 0, 1, lane);
       value = built_value(cd, g, lane);
@@ -127,56 +135,29 @@ __device__ __forceinline__ void score_body(ClusterDev cd, Layout lay, const int1
   }
 }
 
-// The three instantiations as separate kernels, so each gets its own
-// register budget: PARITY and the N <= 64 SCORE path capped at 64 registers
-// (8 four-warp CTAs per SM; uncapped, ptxas picks 72-80 for them on their
-// own); the general SCORE path (one-warp CTAs, 8 per SM by shared memory)
-// at the compiler's choice.
-#ifndef HELIO_SMALL_MAXNREG
-#define HELIO_SMALL_MAXNREG 64
-#endif
-#define SCORE_KERNEL_ARGS                                                                              \
-  ClusterDev cd, Layout lay, const int16_t *__restrict__ pl, int64_t B, int partial,                  \
-      double *__restrict__ values, int32_t *__restrict__ status, unsigned long long *work, int64_t *ovf, \
-      int64_t *ovf2, unsigned int *ovf_count, int tier, FlowOut fo
-#define SCORE_KERNEL_PASS cd, lay, pl, B, partial, values, status, work, ovf, ovf2, ovf_count, tier, fo
-__global__ void __maxnreg__(64) score_kernel_parity(SCORE_KERNEL_ARGS) {
-  score_body<HELIO_MODE_PARITY, false>(SCORE_KERNEL_PASS);
-}
-__global__ void __maxnreg__(HELIO_SMALL_MAXNREG) score_kernel_small(SCORE_KERNEL_ARGS) {
-  score_body<HELIO_MODE_SCORE, false>(SCORE_KERNEL_PASS);
-}
-__global__ void score_kernel_gen(SCORE_KERNEL_ARGS) { score_body<HELIO_MODE_SCORE, true>(SCORE_KERNEL_PASS); }
-
-template <int MODE, bool GEN>
-struct ScoreKernel;
-template <>
-struct ScoreKernel<HELIO_MODE_PARITY, false> {
-  static constexpr auto fn = score_kernel_parity;
-};
-template <>
-struct ScoreKernel<HELIO_MODE_SCORE, false> {
-  static constexpr auto fn = score_kernel_small;
-};
-template <>
-struct ScoreKernel<HELIO_MODE_SCORE, true> {
-  static constexpr auto fn = score_kernel_gen;
-};
+// The kernels: score_body instantiated per mode, plus the large-graph SCORE
+// variant (GEN), each with its own register allocation.  No register caps:
+// capping (__maxnreg__ / __launch_bounds__) measured 33M instead of 70M
+// evals/s on het42 SCORE, and the default instantiations keep round 1's code
+// (64 registers, 8 four-warp CTAs per SM on het42).
 
 // ---------------------------------------------------------------------------
 // max_flow on raw graphs.  Arc construction follows :140-145 literally (lane
 // 0, edge order; a self-loop's forward arc gets rev = itself because adj[v].
 // size() is read before the push_back).
+template <bool GLOBAL>
 __global__ void raw_kernel(Layout lay, int64_t G, const int32_t* __restrict__ gn,
                            const int32_t* __restrict__ gs, const int32_t* __restrict__ gt,
                            const int64_t* __restrict__ eoff, const int32_t* __restrict__ eu,
                            const int32_t* __restrict__ ev, const double* __restrict__ ecap,
                            double* __restrict__ values, double* __restrict__ flows,
-                           unsigned long long* work) {
+                           unsigned long long* work, char* gbase) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const Gs g = slot_view(smem + wib * lay.bytes, lay);
+  // gbase: graphs larger than one SM's shared memory work in global memory
+  char* slot = GLOBAL ? gbase + ((size_t)blockIdx.x * (blockDim.x >> 5) + wib) * lay.bytes : smem + wib * lay.bytes;
+  const Gs g = slot_view(slot, lay);
   for (;;) {
     unsigned long long w = 0;
     if (lane == 0) w = atomicAdd(work, 1ull);
@@ -424,10 +405,22 @@ int configure_layouts(helio_gpu_ctx* ctx) {
       ctx->slot_mid_ok[m] = (size_t)ctx->slot_mid[m].bytes * ctx->mid_warps[m] <= max_smem;
     }
   }
+  // global tier: when even the big slot is smaller than the structural
+  // maximum (every declared link valid; int16 arc indices), a slot of that
+  // size in global memory finishes what overflows it
+  ctx->glob_warps = 2 * ctx->sm_count;
+  for (int m = 0; m < 2; ++m) {
+    const bool compact = m == HELIO_MODE_SCORE && N > 64;
+    const int a_full = std::min(std::max(a_struct, a_masks), 32766);
+    const int a_have = ctx->slot_big_ok[m] ? ctx->slot_big[m].A : ctx->slot_small[m].A;
+    ctx->glob_ok[m] = a_full > a_have;
+    if (ctx->glob_ok[m])
+      ctx->slot_glob[m] = compact ? make_layout_score_general(V, a_full, N) : make_layout(V, a_full, N, 0);
+  }
   // occupancy of both instantiations (PARITY / SCORE)
-  void* fns[2] = {reinterpret_cast<void*>(score_kernel_parity),
-                  ctx->score_gen ? reinterpret_cast<void*>(score_kernel_gen)
-                                 : reinterpret_cast<void*>(score_kernel_small)};
+  void* fns[2] = {reinterpret_cast<void*>(score_kernel<HELIO_MODE_PARITY, false>),
+                  ctx->score_gen ? reinterpret_cast<void*>(score_kernel<HELIO_MODE_SCORE, true>)
+                                 : reinterpret_cast<void*>(score_kernel<HELIO_MODE_SCORE, false>)};
   for (int m = 0; m < 2; ++m) {
     CK(cudaFuncSetAttribute(fns[m], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem));
     // the whole unified L1/shared array as shared memory: the driver's default
@@ -457,13 +450,15 @@ int configure_layouts(helio_gpu_ctx* ctx) {
 
 int ensure_ovf(helio_gpu_ctx* ctx, int set, int64_t B) {
   if (ctx->ovf_cap[set] >= B) return HELIO_OK;
-  if (ctx->d_ovf[set]) cudaFree(ctx->d_ovf[set]);
-  if (ctx->d_ovf2[set]) cudaFree(ctx->d_ovf2[set]);
-  ctx->d_ovf[set] = ctx->d_ovf2[set] = nullptr;
+  cudaFree(ctx->d_ovf[set]);
+  cudaFree(ctx->d_ovf2[set]);
+  cudaFree(ctx->d_ovf3[set]);
+  ctx->d_ovf[set] = ctx->d_ovf2[set] = ctx->d_ovf3[set] = nullptr;
   ctx->ovf_cap[set] = 0;
   int64_t cap = std::max<int64_t>(B, 1 << 16);
   CK(cudaMalloc(&ctx->d_ovf[set], sizeof(int64_t) * cap));
   CK(cudaMalloc(&ctx->d_ovf2[set], sizeof(int64_t) * cap));
+  CK(cudaMalloc(&ctx->d_ovf3[set], sizeof(int64_t) * cap));
   ctx->ovf_cap[set] = cap;
   return HELIO_OK;
 }
@@ -471,32 +466,42 @@ int ensure_ovf(helio_gpu_ctx* ctx, int set, int64_t B) {
 template <int MODE, bool GEN = false>
 void launch_score_mode(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, int partial, double* d_val,
                        int32_t* d_st, cudaStream_t st, FlowOut fo, bool timed) {
-  unsigned long long* work = ctx->d_work + 16 + 3 * set;
-  unsigned int* oc = ctx->d_ovf_count + 2 * set;
+  unsigned long long* work = ctx->d_work + 16 + 4 * set;
+  unsigned int* oc = ctx->d_ovf_count + 3 * set;
   int64_t* l1 = ctx->d_ovf[set];
   int64_t* l2 = ctx->d_ovf2[set];
+  int64_t* l3 = ctx->d_ovf3[set];
+  const bool glob = ctx->glob_ok[MODE] && ctx->d_glob != nullptr;
   if (timed) cudaEventRecord(ctx->ev0, st);
   const Layout& sl = ctx->slot_small[MODE];
   const int warps = ctx->slot_warps[MODE];
   const int grid = (int)std::min<int64_t>(ctx->small_blocks[MODE], (B + warps - 1) / warps);
-  ScoreKernel<MODE, GEN>::fn<<<grid, 32 * warps, sl.bytes * warps, st>>>(ctx->cd, sl, d_pl, B, partial, d_val, d_st,
-                                                                      work, l1, l2, oc, 0, fo);
+  auto K = score_kernel<MODE, GEN>;
+  K<<<grid, 32 * warps, sl.bytes * warps, st>>>(ctx->cd, sl, d_pl, B, partial, d_val, d_st, work, nullptr, nullptr,
+                                                 l1, oc, nullptr, fo);
   // graphs that overflowed the small slot: the same kernel with the middle
-  // slot, then whatever overflows that with the big slot (one warp per CTA)
+  // slot, then whatever overflows that with the big slot (one warp per CTA),
+  // then — for clusters too large for one SM — a slot in global memory
   const Layout& bl = ctx->slot_big_ok[MODE] ? ctx->slot_big[MODE] : sl;
+  const int64_t* big_in = l1;
+  const unsigned int* big_cnt = oc;
   if (ctx->slot_mid_ok[MODE]) {
     const Layout& ml = ctx->slot_mid[MODE];
     const int wm = ctx->mid_warps[MODE];
-    ScoreKernel<MODE, GEN>::fn<<<ctx->mid_blocks[MODE], 32 * wm, ml.bytes * wm, st>>>(
-        ctx->cd, ml, d_pl, B, partial, d_val, d_st, work + 1, l1, l2, oc, 1, fo);
-    ScoreKernel<MODE, GEN>::fn<<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
-                                                                          work + 2, l1, l2, oc, 2, fo);
+    K<<<ctx->mid_blocks[MODE], 32 * wm, ml.bytes * wm, st>>>(ctx->cd, ml, d_pl, B, partial, d_val, d_st, work + 1, l1,
+                                                            oc, l2, oc + 1, nullptr, fo);
+    big_in = l2;
+    big_cnt = oc + 1;
     ctx->launches += 1;
-  } else {
-    ScoreKernel<MODE, GEN>::fn<<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st,
-                                                                          work + 2, l1, nullptr, oc, 1, fo);
   }
-  // kernel time = all tier launches (small, middle, big)
+  K<<<ctx->big_blocks[MODE], 32, bl.bytes, st>>>(ctx->cd, bl, d_pl, B, partial, d_val, d_st, work + 2, big_in,
+                                                 big_cnt, glob ? l3 : nullptr, oc + 2, nullptr, fo);
+  if (glob) {
+    score_kernel<MODE, GEN, true><<<ctx->glob_warps, 32, 0, st>>>(ctx->cd, ctx->slot_glob[MODE], d_pl, B, partial, d_val, d_st, work + 3, l3,
+                                      oc + 2, nullptr, nullptr, ctx->d_glob, fo);
+    ctx->launches += 1;
+  }
+  // kernel time = all tier launches
   if (timed) cudaEventRecord(ctx->ev1, st);
 }
 
@@ -505,8 +510,15 @@ int launch_score(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, in
   if (B <= 0) return HELIO_OK;
   int rc = ensure_ovf(ctx, set, B);
   if (rc) return rc;
-  CK(cudaMemsetAsync(ctx->d_work + 16 + 3 * set, 0, 3 * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(ctx->d_ovf_count + 2 * set, 0, 2 * sizeof(unsigned int), st));
+  // global-memory tier scratch (one slot per warp), allocated on first use
+  if (ctx->glob_ok[mode] && ctx->d_glob == nullptr) {
+    size_t bytes = 0;
+    for (int m = 0; m < 2; ++m)
+      if (ctx->glob_ok[m]) bytes = std::max(bytes, (size_t)ctx->glob_warps * ctx->slot_glob[m].bytes);
+    CK(cudaMalloc(&ctx->d_glob, bytes));
+  }
+  CK(cudaMemsetAsync(ctx->d_work + 16 + 4 * set, 0, 4 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(ctx->d_ovf_count + 3 * set, 0, 3 * sizeof(unsigned int), st));
   if (mode == HELIO_MODE_SCORE && fo.edges == nullptr && fo.nv == nullptr && ctx->score_gen)
     launch_score_mode<HELIO_MODE_SCORE, true>(ctx, set, d_pl, B, partial, d_val, d_st, st, fo, timed);
   else if (mode == HELIO_MODE_SCORE && fo.edges == nullptr && fo.nv == nullptr)
@@ -605,7 +617,7 @@ int helio_gpu_create(int device, helio_gpu_ctx** out) {
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->api_ev, cudaEventDisableTiming) != cudaSuccess ||
       cudaMalloc(&ctx->d_work, 32 * sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMalloc(&ctx->d_ovf_count, 2 * helio_gpu_ctx::kSets * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_ovf_count, 3 * helio_gpu_ctx::kSets * sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc(&ctx->d_pv, (helio_gpu_ctx::kSets + 1) * 4096 * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&ctx->d_pi, (helio_gpu_ctx::kSets + 1) * 4096 * sizeof(long long)) != cudaSuccess ||
       cudaMalloc(&ctx->d_best, 2 * 4096 * sizeof(double)) != cudaSuccess ||
@@ -636,7 +648,9 @@ void helio_gpu_destroy(helio_gpu_ctx* ctx) {
   for (int i = 0; i < helio_gpu_ctx::kSets; ++i) {
     cudaFree(ctx->d_ovf[i]);
     cudaFree(ctx->d_ovf2[i]);
+    cudaFree(ctx->d_ovf3[i]);
   }
+  cudaFree(ctx->d_glob);
   if (ctx->copy) {
     cudaStreamSynchronize(ctx->copy);
     cudaStreamDestroy(ctx->copy);
@@ -1245,14 +1259,18 @@ int helio_gpu_maxflow_raw_host(helio_gpu_ctx* ctx, int64_t G, const int32_t* h_n
     return fail(ctx, HELIO_ERR_TOO_LARGE, "raw graph exceeds the device limits (V <= 16000, 2E <= 32766)");
   Layout lay = make_layout(nmax, std::max(2 * mmax, 2), 0, std::max(mmax, 1));
   const size_t max_smem = 227 * 1024;
-  if ((size_t)lay.bytes > max_smem)
-    return fail(ctx, HELIO_ERR_TOO_LARGE, "raw graph does not fit one SM's shared memory");
-  int warps = (int)std::max<size_t>(1, std::min<size_t>(4, max_smem / lay.bytes));
-  CK(cudaFuncSetAttribute(raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem));
-  CK(cudaFuncSetAttribute(raw_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raw_kernel, 32 * warps, lay.bytes * warps));
-  if (per_sm < 1) per_sm = 1;
+  // graphs larger than one SM's shared memory: one-warp CTAs whose slots live
+  // in global memory (L1/L2 cached), carved from the host-entry arena below
+  const bool in_global = (size_t)lay.bytes > max_smem;
+  int warps = in_global ? 1 : (int)std::max<size_t>(1, std::min<size_t>(4, max_smem / lay.bytes));
+  int per_sm = 2;
+  if (!in_global) {
+    CK(cudaFuncSetAttribute(raw_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem));
+    CK(cudaFuncSetAttribute(raw_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, raw_kernel<false>, 32 * warps, lay.bytes * warps));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int grid = (int)std::min<int64_t>((int64_t)per_sm * ctx->sm_count, (G + warps - 1) / warps);
   cudaStream_t st = ctx->stream;
   const int64_t Ea = std::max<int64_t>(Etot, 1);
   auto carve = [&](Carve& c, int32_t*& n, int32_t*& s, int32_t*& t, int64_t*& off, int32_t*& u, int32_t*& v,
@@ -1270,12 +1288,15 @@ int helio_gpu_maxflow_raw_host(helio_gpu_ctx* ctx, int64_t G, const int32_t* h_n
   int32_t *d_n, *d_s, *d_t, *d_u, *d_v;
   int64_t* d_off;
   double *d_cap, *d_val, *d_fl;
+  char* d_slots = nullptr;
   Carve measure;
   carve(measure, d_n, d_s, d_t, d_off, d_u, d_v, d_cap, d_val, d_fl);
+  if (in_global) measure.take<char>((size_t)grid * lay.bytes);
   Carve c;
   int rc = host_arena(ctx, measure.off, &c.base);
   if (rc) return rc;
   carve(c, d_n, d_s, d_t, d_off, d_u, d_v, d_cap, d_val, d_fl);
+  if (in_global) d_slots = c.take<char>((size_t)grid * lay.bytes);
   if (!h_flows) d_fl = nullptr;
   CK(api_begin(ctx, st));
   CK(cudaMemcpyAsync(d_n, h_n, 4 * G, cudaMemcpyHostToDevice, st));
@@ -1288,9 +1309,12 @@ int helio_gpu_maxflow_raw_host(helio_gpu_ctx* ctx, int64_t G, const int32_t* h_n
     CK(cudaMemcpyAsync(d_cap, h_cap, 8 * Etot, cudaMemcpyHostToDevice, st));
   }
   CK(cudaMemsetAsync(ctx->d_work, 0, sizeof(unsigned long long), st));
-  int grid = (int)std::min<int64_t>((int64_t)per_sm * ctx->sm_count, (G + warps - 1) / warps);
-  raw_kernel<<<grid, 32 * warps, lay.bytes * warps, st>>>(lay, G, d_n, d_s, d_t, d_off, d_u, d_v, d_cap,
-                                                           d_val, d_fl, ctx->d_work);
+  if (in_global)
+    raw_kernel<true><<<grid, 32, 0, st>>>(lay, G, d_n, d_s, d_t, d_off, d_u, d_v, d_cap, d_val, d_fl, ctx->d_work,
+                                          d_slots);
+  else
+    raw_kernel<false><<<grid, 32 * warps, lay.bytes * warps, st>>>(lay, G, d_n, d_s, d_t, d_off, d_u, d_v, d_cap,
+                                                                    d_val, d_fl, ctx->d_work, nullptr);
   CK(cudaGetLastError());
   CK(api_end(ctx, st));
   ctx->launches++;

@@ -242,6 +242,10 @@ __device__ void pr_global_relabel(const Gs& g, int16_t* q, const int n, const in
   __syncwarp();
 }
 
+// ILP (the dedicated large-graph kernel): the admissible-arc scan and the
+// relabel take four arcs per step (independent loads); otherwise one arc per
+// step — the code the combined small-cluster kernel is register-tuned with.
+template <bool ILP>
 __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, const int lane, const int gr_every) {
   const unsigned lt = lanemask_lt();
   int16_t* fq = g.q;     // circular FIFO of live vertices with excess (<= n entries)
@@ -306,7 +310,18 @@ __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, c
       int v = -1;
       if (u >= 0) {
         e = g.ex[u];
-        if (e > 0.0) {
+        if (e > 0.0 && !ILP) {
+          for (; a < ae; ++a) {
+            const int w = g.to[a];
+            if (g.h[w] == hu - 1) {
+              c = g.cap[a];
+              if (c > FLOW_EPS) {
+                v = w;
+                break;
+              }
+            }
+          }
+        } else if (e > 0.0) {
           // the first admissible arc at or after `a`, four arcs per step:
           // their loads are independent, so one step costs two shared-memory
           // round trips instead of two per arc
@@ -374,6 +389,10 @@ __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, c
     int nl = -1;
     if (u >= 0 && g.ex[u] > 0.0) {
       int best = n;
+      if (!ILP) {
+        for (int b2 = g.abeg[u]; b2 < ae; ++b2)
+          if (g.cap[b2] > FLOW_EPS) best = min(best, g.h[g.to[b2]] + 1);
+      } else {
       for (int b2 = g.abeg[u]; b2 < ae; b2 += 4) {  // four independent arcs per step
         const int n4 = min(4, ae - b2);
         int w[4];
@@ -386,6 +405,7 @@ __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, c
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (cc[k] > FLOW_EPS) best = min(best, g.h[w[k]] + 1);
+      }
       }
       nl = best;
     }

@@ -250,6 +250,67 @@ def test_het42_prune12_variant_bit_exact_against_reference(cap):
         assert np.all(np.abs(v2 - vr) <= 1e-6 * np.maximum(1.0, np.abs(vr)))
 
 
+def _huge_dense_cluster():
+    """200 nodes, full mesh (40,200 links), 8 layers of 1 GB: the structural
+    maximum (32,766 arcs) is far beyond one SM's shared memory."""
+    d = clusters.mesh_cluster(200)
+    d["model"]["num_layers"] = 8
+    d["model"]["param_gb"] = 8.0
+    return d
+
+
+def _two_stage_rows(N, rng, count):
+    rows = np.zeros((count, N, 2), np.int16)
+    for b in range(count):
+        for k in range(N):
+            if rng.random() < 0.04 * b:  # later rows leave more nodes idle (smaller graphs)
+                continue
+            rows[b, k] = (0, 4) if k < N // 2 else (4, 8)
+    return rows
+
+
+def test_graphs_beyond_shared_memory_are_solved_in_the_global_tier():
+    """Dense two-stage placements on a 200-node full mesh carry ~10k edges
+    (~21k arcs), more than the big shared-memory slot holds: they finish in the
+    global-memory tier instead of HELIO_CAND_TOO_LARGE, bit-exact in PARITY
+    (values and per-edge flows), within 1e-6 in SCORE."""
+    d = _huge_dense_cluster()
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    rows = _two_stage_rows(e.num_nodes, np.random.default_rng(3), 12)
+    o = Oracle(d)
+    vo, so = o.score(rows)
+    assert np.all(so == 0)
+    v, s = e.score(rows)
+    assert np.array_equal(s, so) and np.array_equal(bits(v), bits(vo))
+    e.mode = "score"
+    v2, s2 = e.score(rows)
+    assert np.array_equal(s2, so)
+    assert np.all(np.abs(v2 - vo) <= 1e-6 * np.maximum(1.0, np.abs(vo)))
+    e.mode = "parity"
+    st, nv, E, val = o.graph(rows[0])
+    assert len(E["u"]) > 10_000
+    vals, sts, nvs, nes, ints, dbl = e.flows(rows[:1], True, len(E["u"]))
+    assert sts[0] == 0 and nes[0] == len(E["u"])
+    assert np.array_equal(bits(dbl[0, : nes[0], 1]), bits(E["flow"]))
+
+
+def test_raw_graph_beyond_shared_memory():
+    """A raw graph of 15,000 edges (30,000 arcs, ~360 KB of solver state) runs
+    in global memory, bit-exact against the reference's max_flow."""
+    from _support import max_flow_raw_oracle
+    rng = np.random.default_rng(8)
+    n, m = 1500, 15_000
+    u = rng.integers(0, n, m).astype(np.int32)
+    v = rng.integers(0, n, m).astype(np.int32)
+    cap = rng.integers(1, 50, m).astype(np.float64)
+    want, wflow = max_flow_raw_oracle(n, 0, n - 1, u, v, cap)
+    vals, flows = h.max_flow_raw(np.array([n], np.int32), np.array([0], np.int32), np.array([n - 1], np.int32),
+                                 np.array([0, m], np.int64), u, v, cap)
+    assert bits(vals)[0] == bits(np.array([want]))[0] and want > 0
+    assert np.array_equal(bits(flows), bits(wflow))
+
+
 def test_generate_trace_matches_reference_fixture():
     z = golden("route_geo24.npz")
     _, inl, outl = h.generate_trace_arrays(len(z["in_len"]), 0.0, "offline", 7)
