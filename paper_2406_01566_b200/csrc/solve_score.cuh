@@ -307,7 +307,7 @@ __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, c
     __syncwarp();
     for (;;) {
       double e = 0.0, c = 0.0;
-      int v = -1;
+      int v = -1, r = -1;  // ILP: r = the chosen arc's reverse, loaded with the scan
       if (u >= 0) {
         e = g.ex[u];
         if (e > 0.0 && !ILP) {
@@ -337,7 +337,10 @@ __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, c
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) hh[k] = k < n4 ? g.h[w[k]] : -2;
-            int kk = -1, vk = -1;
+            int rr[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) rr[k] = k < n4 ? g.rv[a + k] : 0;
+            int kk = -1, vk = -1, rk = -1;
             double ck = 0.0;
 #pragma unroll
             for (int k = 3; k >= 0; --k)
@@ -345,16 +348,28 @@ __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, c
                 kk = k;
                 vk = w[k];
                 ck = cc[k];
+                rk = rr[k];
               }
             if (kk >= 0) {
               a += kk;
               v = vk;
               c = ck;
+              r = rk;
               break;
             }
             a += n4;
           }
         }
+      }
+      // ILP: the reverse arc's residual and the target's queue flag are read
+      // before the ballots — within a round only this lane touches that arc
+      // (lowest lane per target; v cannot push back along it, h[v] < h[u]),
+      // and only the lane depositing into v appends it
+      double rc = 0.0;
+      bool vq = false;
+      if (ILP && v >= 0) {
+        rc = g.cap[r];
+        vq = v != t && inq[v];
       }
       const unsigned pm = __ballot_sync(FULL, v >= 0);
       if (pm == 0u) break;
@@ -365,13 +380,16 @@ __device__ double solve_pr(const Gs& g, const int n, const int s, const int t, c
       if (go) {
         d = ref_min(e, c);
         g.cap[a] = c - d;
-        g.cap[g.rv[a]] += d;
+        if (ILP)
+          g.cap[r] = rc + d;
+        else
+          g.cap[g.rv[a]] += d;
         g.ex[u] = e - d;
         if (v == t) sink += d;
         if (d == c) ++a;  // saturated (else u is drained)
       }
       __syncwarp();
-      const bool app = go && v != t && !inq[v];
+      const bool app = go && v != t && (ILP ? !vq : !inq[v]);
       if (go && v != t) g.ex[v] += d;
       const unsigned am = __ballot_sync(FULL, app);
       if (app) {
