@@ -65,7 +65,7 @@ def env_int(k, d):
 # committed ncu --set full captures of one score_kernel launch (tools/profile_score.py):
 # (config, mode) -> (file under profiles/, candidates in the profiled launch)
 PROFILES = {
-    ("het42-70b", "score"): ("r01_score_mode_raw.csv", 200_000),
+    ("het42-70b", "score"): ("r02_het42_score_raw.csv", 200_000),
     ("het42-70b", "parity"): ("r01_parity_mode_raw.csv", 200_000),
     ("syn256-120l", "score"): ("r01_syn256_score_raw.csv", 20_000),
 }

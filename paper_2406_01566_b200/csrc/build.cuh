@@ -365,6 +365,197 @@ __device__ int build_graph_score(const ClusterDev& cd, const Gs& g, const Layout
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// SCORE builder for large sparse networks (GEN kernel): the split network with
+// every series vertex contracted away.  A vertex other than s, t with exactly
+// one in-arc and one out-arc (an in-vertex with one in-edge — its only
+// out-edge is the compute edge; an out-vertex with one out-edge) carries the
+// same flow on both, so u -> x -> w becomes u -> w with capacity min of the
+// two; chains of such vertices collapse into one edge.  The max-flow value is
+// unchanged (min is exact), so SCORE's guarantees hold.  On syn256 link walks
+// this takes V 514 -> ~248 and E 699 -> ~433, and the push-relabel solver's
+// global-relabel BFS depth with it (367 -> 128 BFS steps per graph, modelled).
+//
+// din/dout: in-degree of in_k / out-degree of out_k (links + source / sink
+// arcs); vin/vout: contracted vertex ids (-1 = contracted away); succ: the
+// unique out-link of out_k when dout == 1 (the node -> coordinator link for
+// the sink arc).
+__device__ __forceinline__ int contract_walk(const ClusterDev& cd, const int32_t* pse, const int16_t* vin,
+                                             const int16_t* vout, const int32_t* succ, int j, bool at_out,
+                                             double& c) {
+  for (int guard = 0; guard < 2 * cd.N + 2; ++guard) {
+    if (!at_out) {
+      const int x = vin[j];
+      if (x >= 0) return x;
+      const int32_t w = pse[j];  // in_j contracted away: through its compute edge
+      const int s = (int16_t)(w & 0xffff), e = (int16_t)(w >> 16);
+      c = ref_min(c, __ldg(cd.cap_tab + __ldg(cd.cap_off + j) + (e - s) - 1));
+      at_out = true;
+    } else {
+      const int x = vout[j];
+      if (x >= 0) return x;
+      const int link = succ[j];  // out_j contracted away: its unique out-edge
+      c = ref_min(c, __ldg(cd.link_cap + link));
+      const int m = (int)(__ldg(cd.link_pack + link) >> 16) - 1;
+      if (m < 0) return 1;  // the sink
+      j = m;
+      at_out = false;
+    }
+  }
+  return -1;  // unreachable on a DAG
+}
+
+__device__ int build_graph_score_contract(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,
+                                          int partial, int lane, int& V, int& E) {
+  const int N = cd.N, L = cd.L;
+  int32_t* pse = reinterpret_cast<int32_t*>(g.ps);
+  int32_t* din = reinterpret_cast<int32_t*>(g.efwd);
+  int32_t* dout = din + N;
+  int16_t* vin = g.vin;
+  int16_t* vout = g.vin + N;
+  int32_t* succ = reinterpret_cast<int32_t*>(g.unode);
+  int bad = INT_MAX;
+  const int32_t* row32 = reinterpret_cast<const int32_t*>(row);
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = __ldg(row32 + k);
+    const int s = (int16_t)(w & 0xffff);
+    const int e = (int16_t)(w >> 16);
+    pse[k] = w;
+    din[k] = 0;
+    if (e > s) {
+      int code = 0;
+      if (s < 0 || e > L) code = 2;
+      else if (e - s > __ldg(cd.kmax + k)) code = 3;
+      if (code) bad = min(bad, __ldg(cd.lexrank + k) * 4 + code);
+    }
+  }
+  bad = __reduce_min_sync(FULL, bad);
+  if (bad != INT_MAX) return bad & 3;
+  __syncwarp();
+  // degrees, and each out-vertex's last valid out-link (its only one when dout == 1)
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = pse[k];
+    const int s = (int16_t)(w & 0xffff), e = (int16_t)(w >> 16);
+    if (e <= s) continue;
+    int nout = 0, last = -1;
+    for_valid_out_links(cd, pse, k, e, partial, [&](int j, int link) {
+      ++nout;
+      last = link;
+      atomicAdd(&din[j], 1);
+    });
+    if (s == 0 && __ldg(cd.cout_link + k) >= 0) atomicAdd(&din[k], 1);
+    const int lk = __ldg(cd.cin_link + k);
+    const bool snk = e == L && lk >= 0;
+    dout[k] = nout + (snk ? 1 : 0);
+    succ[k] = snk ? lk : last;
+  }
+  __syncwarp();
+  // kept vertices, numbered in node order after s = 0, t = 1
+  int run = 2;
+  for (int k0 = 0; k0 < N; k0 += 32) {
+    const int k = k0 + lane;
+    bool kin = false, kout = false;
+    if (k < N) {
+      const int32_t w = pse[k];
+      const bool used = (int16_t)(w >> 16) > (int16_t)(w & 0xffff);
+      kin = used && din[k] != 1;
+      kout = used && dout[k] != 1;
+    }
+    const int cnt = (kin ? 1 : 0) + (kout ? 1 : 0);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (k < N) {
+      const int base = run + incl - cnt;
+      vin[k] = (int16_t)(kin ? base : -1);
+      vout[k] = (int16_t)(kout ? base + (kin ? 1 : 0) : -1);
+    }
+    run += __shfl_sync(FULL, incl, 31);
+  }
+  V = run;
+  if (V > lay.V) return ST_OVERFLOW;
+  int* fill = reinterpret_cast<int*>(g.ex);  // per contracted vertex: degree, then slot counter
+  for (int x = lane; x < V; x += 32) fill[x] = 0;
+  __syncwarp();
+  // every contracted edge starts at a kept vertex: s (source arcs), a kept
+  // in-vertex (its compute edge), a kept out-vertex (valid out-links and the
+  // sink arc).  Pass 0 counts degrees, pass 1 places the arcs.
+  int nedges = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    auto emit = [&](int a, int b, double c) {
+      if (pass == 0) {
+        ++nedges;
+        atomicAdd(&fill[a], 1);
+        atomicAdd(&fill[b], 1);
+      } else {
+        const int fa = g.abeg[a] + atomicAdd(&fill[a], 1);
+        const int ra = g.abeg[b] + atomicAdd(&fill[b], 1);
+        g.to[fa] = (int16_t)b;
+        g.rv[fa] = (int16_t)ra;
+        g.cap[fa] = c;
+        g.to[ra] = (int16_t)a;
+        g.rv[ra] = (int16_t)fa;
+        g.cap[ra] = 0.0;
+      }
+    };
+    for (int k = lane; k < N; k += 32) {
+      const int32_t w = pse[k];
+      const int s = (int16_t)(w & 0xffff), e = (int16_t)(w >> 16);
+      if (e <= s) continue;
+      const int lc = __ldg(cd.cout_link + k);
+      if (s == 0 && lc >= 0) {
+        double c = __ldg(cd.link_cap + lc);
+        const int b = contract_walk(cd, pse, vin, vout, succ, k, false, c);
+        emit(0, b, c);
+      }
+      const int xi = vin[k];
+      if (xi >= 0) {
+        double c = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
+        const int b = contract_walk(cd, pse, vin, vout, succ, k, true, c);
+        emit(xi, b, c);
+      }
+      const int xo = vout[k];
+      if (xo >= 0) {
+        for_valid_out_links(cd, pse, k, e, partial, [&](int j, int link) {
+          double c = __ldg(cd.link_cap + link);
+          const int b = contract_walk(cd, pse, vin, vout, succ, j, false, c);
+          emit(xo, b, c);
+        });
+        const int lk = __ldg(cd.cin_link + k);
+        if (e == L && lk >= 0) emit(xo, 1, __ldg(cd.link_cap + lk));
+      }
+    }
+    __syncwarp();
+    if (pass == 0) {
+      nedges = __reduce_add_sync(FULL, nedges);
+      if (2 * nedges > lay.A) return ST_OVERFLOW;
+      int r2 = 0;
+      for (int x0 = 0; x0 < V; x0 += 32) {
+        const int x = x0 + lane;
+        const int d = x < V ? fill[x] : 0;
+        int incl = d;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (x < V) {
+          g.abeg[x] = (int16_t)(r2 + incl - d);
+          fill[x] = 0;
+        }
+        r2 += __shfl_sync(FULL, incl, 31);
+      }
+      if (lane == 0) g.abeg[V] = (int16_t)r2;
+      __syncwarp();
+    }
+  }
+  E = nedges;
+  return 0;
+}
+
 // The round-1 general builder (one out-link per step), kept for the combined
 // small-cluster kernel, whose register allocation is tuned with it.
 __device__ int build_graph_score_r1(const ClusterDev& cd, const Gs& g, const Layout& lay, const int16_t* row,

@@ -71,6 +71,42 @@ Layout make_layout_score_general(int V, int A, int N) {
   return l;
 }
 
+// SCORE layout of the large-graph path (GEN kernel; series-contracted
+// networks, build_graph_score_contract): V and A count the CONTRACTED graph.
+// The builder's per-node scratch sits behind the solver arrays: packed
+// intervals (4N), int32 in/out degrees (8N; the solver's FIFO flags reuse it),
+// int16 kept-vertex ids (4N), int32 unique out-link of a removed out-vertex
+// (4N).  12A + 16V + 20N bytes.
+Layout make_layout_contract(int V, int A, int N) {
+  Layout l;
+  l.V = V; l.A = A; l.N = N; l.M = 0;
+  int o = 0;
+  auto take = [&](int bytes, int align) {
+    o = (o + align - 1) / align * align;
+    int r = o;
+    o += bytes;
+    return r;
+  };
+  l.o_cap = take(8 * A, 16);
+  l.o_ex = take(8 * V, 16);  // builder: int degree / slot counters per contracted vertex
+  l.o_vs = l.o_ex;
+  l.o_to = take(2 * A, 2);
+  l.o_rv = take(2 * A, 2);
+  l.o_abeg = take(2 * (V + 1), 2);
+  l.o_h = take(2 * V, 2);
+  l.o_cur = take(2 * V, 2);
+  l.o_q = take(2 * V, 2);
+  l.o_cnt = l.o_q;
+  l.o_ps = take(4 * N, 4);
+  l.o_pe = l.o_ps + 2 * N;
+  l.o_efwd = take(8 * N, 8);  // din [N], dout [N] (int32)
+  l.o_inq = l.o_efwd;         // V <= 2N + 2 <= 8N bytes
+  l.o_vin = take(4 * N, 4);   // vin [N], vout [N] (int16, -1 = contracted away)
+  l.o_unode = take(4 * N, 4); // succ [N] (int32 link index)
+  l.bytes = (o + 15) / 16 * 16;
+  return l;
+}
+
 // PARITY per-vertex solver state, one 16-byte shared-memory record so a
 // discharge loads it with a single LDS.128.
 struct __align__(16) VState {

@@ -98,7 +98,7 @@ __global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restric
     double cut = 1.0e300;  // SCORE, N <= 64: the builder's layer cut (an upper bound to stop at)
     int st = MODE == HELIO_MODE_SCORE
                  ? (!GEN && cd.out_mask ? build_graph_score_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E, cut)
-                 : GEN                  ? build_graph_score(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
+                 : GEN                  ? build_graph_score_contract(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
                                         : build_graph_score_r1(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E))
                  : (cd.less_cout && !fo.edges
                         ? build_graph_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
@@ -388,19 +388,46 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   ctx->slot_warps[HELIO_MODE_PARITY] = ctx->small_warps;
   ctx->slot_big_ok[HELIO_MODE_PARITY] = ctx->big_ok;
   // SCORE: N <= 64 runs the cover-mask builder and bitset solver on the full
-  // layout (residual rows in the VState bytes); larger clusters the compact one
-  plan(N > 64, small_arcs(N > 64 ? 32 : 16), ctx->slot_small[HELIO_MODE_SCORE], ctx->slot_big[HELIO_MODE_SCORE],
-       ctx->slot_warps[HELIO_MODE_SCORE], ctx->slot_big_ok[HELIO_MODE_SCORE]);
+  // layout (residual rows in the VState bytes); the large-graph kernel
+  // (score_gen) builds series-contracted networks (make_layout_contract: V, A
+  // count contracted vertices / arcs; the small slot holds 5N/4 + 8 vertices
+  // and 4N arcs — syn256 link walks contract to p99 277 / 986)
+  if (ctx->score_gen) {
+    const int Vs = std::min(V, 5 * N / 4 + 8);
+    const int As = std::min(std::max(a_struct, a_masks), std::max(4 * N, 2 * ctx->L + 2));
+    Layout& sm = ctx->slot_small[HELIO_MODE_SCORE];
+    Layout& bg = ctx->slot_big[HELIO_MODE_SCORE];
+    sm = make_layout_contract(Vs, As, N);
+    ctx->slot_warps[HELIO_MODE_SCORE] = best_warps(sm);
+    int a_big = std::min(std::max(a_struct, a_masks), 32766);
+    bg = make_layout_contract(V, a_big, N);
+    if ((size_t)bg.bytes > max_smem) {
+      int lo = 2, hi = a_big;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) / 2;
+        if ((size_t)make_layout_contract(V, mid, N).bytes <= max_smem) lo = mid;
+        else hi = mid - 1;
+      }
+      bg = make_layout_contract(V, lo, N);
+    }
+    ctx->slot_big_ok[HELIO_MODE_SCORE] = (size_t)bg.bytes <= max_smem;
+  } else {
+    plan(N > 64, small_arcs(N > 64 ? 32 : 16), ctx->slot_small[HELIO_MODE_SCORE], ctx->slot_big[HELIO_MODE_SCORE],
+         ctx->slot_warps[HELIO_MODE_SCORE], ctx->slot_big_ok[HELIO_MODE_SCORE]);
+  }
   // middle tier: twice the small slot's arcs (placements with replicated
   // stages — the heuristics' petals/swarm layouts carry ~5N edges on het42),
   // with its own warps per CTA; skipped when it would not beat the big slot
+  auto mk_mode = [&](int m, int a) {
+    if (m == HELIO_MODE_SCORE && ctx->score_gen) return make_layout_contract(V, a, N);
+    return m == HELIO_MODE_SCORE && N > 64 ? make_layout_score_general(V, a, N) : make_layout(V, a, N, 0);
+  };
   for (int m = 0; m < 2; ++m) {
-    const bool compact = m == HELIO_MODE_SCORE && N > 64;
     const int a_small = ctx->slot_small[m].A;
     const int a_mid = std::min(2 * a_small, ctx->slot_big[m].A);
     ctx->slot_mid_ok[m] = false;
-    if (ctx->slot_big_ok[m] && a_mid > a_small && a_mid < ctx->slot_big[m].A) {
-      ctx->slot_mid[m] = compact ? make_layout_score_general(V, a_mid, N) : make_layout(V, a_mid, N, 0);
+    if (ctx->slot_big_ok[m] && a_mid < ctx->slot_big[m].A && (a_mid > a_small || ctx->slot_small[m].V < V)) {
+      ctx->slot_mid[m] = mk_mode(m, a_mid);
       ctx->mid_warps[m] = best_warps(ctx->slot_mid[m]);
       ctx->slot_mid_ok[m] = (size_t)ctx->slot_mid[m].bytes * ctx->mid_warps[m] <= max_smem;
     }
@@ -410,12 +437,10 @@ int configure_layouts(helio_gpu_ctx* ctx) {
   // size in global memory finishes what overflows it
   ctx->glob_warps = 2 * ctx->sm_count;
   for (int m = 0; m < 2; ++m) {
-    const bool compact = m == HELIO_MODE_SCORE && N > 64;
     const int a_full = std::min(std::max(a_struct, a_masks), 32766);
     const int a_have = ctx->slot_big_ok[m] ? ctx->slot_big[m].A : ctx->slot_small[m].A;
     ctx->glob_ok[m] = a_full > a_have;
-    if (ctx->glob_ok[m])
-      ctx->slot_glob[m] = compact ? make_layout_score_general(V, a_full, N) : make_layout(V, a_full, N, 0);
+    if (ctx->glob_ok[m]) ctx->slot_glob[m] = mk_mode(m, a_full);
   }
   // occupancy of both instantiations (PARITY / SCORE)
   void* fns[2] = {reinterpret_cast<void*>(score_kernel<HELIO_MODE_PARITY, false>),

@@ -163,6 +163,48 @@ def test_scoring_is_deterministic_at_full_size():
     assert np.array_equal(bits(v1.cpu().numpy()[sub]), bits(vo))
 
 
+@pytest.mark.parametrize("cap", ["int", "float"])
+def test_syn256_at_scale_is_deterministic_and_matches_the_reference(cap):
+    """configs[4] at scale: 1M syn256 link walks in SCORE mode (the large-graph
+    kernel, all slot tiers) — repeat-run identity, every status OK, the argmax
+    equal to the first maximum of the returned values, and a seeded subsample
+    against the reference's own build_flow_graph + max_flow (bit-exact on
+    integer capacities, 1e-6 relative on float)."""
+    import torch
+    from _support import RefCluster, ref_available
+    d = clusters.CONFIGS["syn256-120l"](cap)
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    e.mode = "score"
+    B = 1_000_000
+    pl = torch.empty((B, e.num_nodes, 2), dtype=torch.int16, device="cuda")
+    e.generate_walk_device(99, 0, B, pl.data_ptr(), 0)
+    v1 = torch.empty(B, dtype=torch.float64, device="cuda")
+    v2 = torch.empty(B, dtype=torch.float64, device="cuda")
+    st = torch.empty(B, dtype=torch.int32, device="cuda")
+    best = torch.empty(1, dtype=torch.float64, device="cuda")
+    idx = torch.empty(1, dtype=torch.int64, device="cuda")
+    e.score_device(pl.data_ptr(), B, v1.data_ptr(), st.data_ptr(), True, 0)
+    e.score_device(pl.data_ptr(), B, v2.data_ptr(), st.data_ptr(), True, 0)
+    e.argmax_device(v1.data_ptr(), st.data_ptr(), B, 0, best.data_ptr(), idx.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert torch.equal(v1.view(torch.int64), v2.view(torch.int64))
+    assert int((st != 0).sum()) == 0
+    vh = v1.cpu().numpy()
+    assert int(idx.item()) == int(np.argmax(vh)) and float(best.item()) == float(vh.max())
+    sub = np.random.default_rng(2).choice(B, 300, replace=False)
+    rows = pl.cpu().numpy()[sub]
+    if ref_available():
+        vo, so = RefCluster(d).score(rows, True, 8)
+    else:
+        vo, so = Oracle(d).score(rows)
+    assert np.all(so == 0)
+    if cap == "int":
+        assert np.array_equal(bits(vh[sub]), bits(vo))
+    else:
+        assert np.all(np.abs(vh[sub] - vo) <= 1e-6 * np.maximum(1.0, np.abs(vo)))
+
+
 @pytest.mark.parametrize("tag", ["geo24", "fan3", "kvmask"])
 def test_routes_bit_exact(tag):
     z = golden(f"route_{tag}.npz")
