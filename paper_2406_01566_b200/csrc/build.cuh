@@ -478,80 +478,99 @@ __device__ int build_graph_score_contract(const ClusterDev& cd, const Gs& g, con
   V = run;
   if (V > lay.V) return ST_OVERFLOW;
   int* fill = reinterpret_cast<int*>(g.ex);  // per contracted vertex: degree, then slot counter
-  for (int x = lane; x < V; x += 32) fill[x] = 0;
-  __syncwarp();
-  // every contracted edge starts at a kept vertex: s (source arcs), a kept
-  // in-vertex (its compute edge), a kept out-vertex (valid out-links and the
-  // sink arc).  Pass 0 counts degrees, pass 1 places the arcs.
-  int nedges = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    auto emit = [&](int a, int b, double c) {
-      if (pass == 0) {
-        ++nedges;
-        atomicAdd(&fill[a], 1);
-        atomicAdd(&fill[b], 1);
-      } else {
-        const int fa = g.abeg[a] + atomicAdd(&fill[a], 1);
-        const int ra = g.abeg[b] + atomicAdd(&fill[b], 1);
-        g.to[fa] = (int16_t)b;
-        g.rv[fa] = (int16_t)ra;
-        g.cap[fa] = c;
-        g.to[ra] = (int16_t)a;
-        g.rv[ra] = (int16_t)fa;
-        g.cap[ra] = 0.0;
-      }
-    };
-    for (int k = lane; k < N; k += 32) {
-      const int32_t w = pse[k];
-      const int s = (int16_t)(w & 0xffff), e = (int16_t)(w >> 16);
-      if (e <= s) continue;
-      const int lc = __ldg(cd.cout_link + k);
-      if (s == 0 && lc >= 0) {
-        double c = __ldg(cd.link_cap + lc);
-        const int b = contract_walk(cd, pse, vin, vout, succ, k, false, c);
-        emit(0, b, c);
-      }
-      const int xi = vin[k];
-      if (xi >= 0) {
-        double c = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
-        const int b = contract_walk(cd, pse, vin, vout, succ, k, true, c);
-        emit(xi, b, c);
-      }
-      const int xo = vout[k];
-      if (xo >= 0) {
-        for_valid_out_links(cd, pse, k, e, partial, [&](int j, int link) {
-          double c = __ldg(cd.link_cap + link);
-          const int b = contract_walk(cd, pse, vin, vout, succ, j, false, c);
-          emit(xo, b, c);
-        });
-        const int lk = __ldg(cd.cin_link + k);
-        if (e == L && lk >= 0) emit(xo, 1, __ldg(cd.link_cap + lk));
-      }
+  // Degrees need no walks: every original edge into a kept vertex ends
+  // exactly one contracted edge there, and every contracted edge starts at a
+  // kept vertex — s (source arcs), a kept in-vertex (its compute edge) or a
+  // kept out-vertex (its dout out-edges).  So deg(in_k) = din + 1,
+  // deg(out_k) = 1 + dout, deg(s) = #source arcs, deg(t) = #sink arcs.
+  int nedges = 0, nsrc = 0, nsnk = 0;
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = pse[k];
+    const int s = (int16_t)(w & 0xffff), e = (int16_t)(w >> 16);
+    if (e <= s) continue;
+    if (s == 0 && __ldg(cd.cout_link + k) >= 0) {
+      ++nsrc;
+      ++nedges;
     }
-    __syncwarp();
-    if (pass == 0) {
-      nedges = __reduce_add_sync(FULL, nedges);
-      if (2 * nedges > lay.A) return ST_OVERFLOW;
-      int r2 = 0;
-      for (int x0 = 0; x0 < V; x0 += 32) {
-        const int x = x0 + lane;
-        const int d = x < V ? fill[x] : 0;
-        int incl = d;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(FULL, incl, o);
-          if (lane >= o) incl += y;
-        }
-        if (x < V) {
-          g.abeg[x] = (int16_t)(r2 + incl - d);
-          fill[x] = 0;
-        }
-        r2 += __shfl_sync(FULL, incl, 31);
-      }
-      if (lane == 0) g.abeg[V] = (int16_t)r2;
-      __syncwarp();
+    if (e == L && __ldg(cd.cin_link + k) >= 0) ++nsnk;
+    const int xi = vin[k], xo = vout[k];
+    if (xi >= 0) {
+      fill[xi] = din[k] + 1;
+      ++nedges;
+    }
+    if (xo >= 0) {
+      fill[xo] = 1 + dout[k];
+      nedges += dout[k];
     }
   }
+  nedges = __reduce_add_sync(FULL, nedges);
+  nsrc = __reduce_add_sync(FULL, nsrc);
+  nsnk = __reduce_add_sync(FULL, nsnk);
+  if (2 * nedges > lay.A) return ST_OVERFLOW;
+  if (lane == 0) {
+    fill[0] = nsrc;
+    fill[1] = nsnk;
+  }
+  __syncwarp();
+  {
+    int r2 = 0;
+    for (int x0 = 0; x0 < V; x0 += 32) {
+      const int x = x0 + lane;
+      const int d = x < V ? fill[x] : 0;
+      int incl = d;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (x < V) {
+        g.abeg[x] = (int16_t)(r2 + incl - d);
+        fill[x] = 0;
+      }
+      r2 += __shfl_sync(FULL, incl, 31);
+    }
+    if (lane == 0) g.abeg[V] = (int16_t)r2;
+  }
+  __syncwarp();
+  // one walk per contracted edge: forward arc at its start, reverse at its end
+  auto emit = [&](int a, int b, double c) {
+    const int fa = g.abeg[a] + atomicAdd(&fill[a], 1);
+    const int ra = g.abeg[b] + atomicAdd(&fill[b], 1);
+    g.to[fa] = (int16_t)b;
+    g.rv[fa] = (int16_t)ra;
+    g.cap[fa] = c;
+    g.to[ra] = (int16_t)a;
+    g.rv[ra] = (int16_t)fa;
+    g.cap[ra] = 0.0;
+  };
+  for (int k = lane; k < N; k += 32) {
+    const int32_t w = pse[k];
+    const int s = (int16_t)(w & 0xffff), e = (int16_t)(w >> 16);
+    if (e <= s) continue;
+    const int lc = __ldg(cd.cout_link + k);
+    if (s == 0 && lc >= 0) {
+      double c = __ldg(cd.link_cap + lc);
+      const int b = contract_walk(cd, pse, vin, vout, succ, k, false, c);
+      emit(0, b, c);
+    }
+    const int xi = vin[k];
+    if (xi >= 0) {
+      double c = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
+      const int b = contract_walk(cd, pse, vin, vout, succ, k, true, c);
+      emit(xi, b, c);
+    }
+    const int xo = vout[k];
+    if (xo >= 0) {
+      for_valid_out_links(cd, pse, k, e, partial, [&](int j, int link) {
+        double c = __ldg(cd.link_cap + link);
+        const int b = contract_walk(cd, pse, vin, vout, succ, j, false, c);
+        emit(xo, b, c);
+      });
+      const int lk = __ldg(cd.cin_link + k);
+      if (e == L && lk >= 0) emit(xo, 1, __ldg(cd.link_cap + lk));
+    }
+  }
+  __syncwarp();
   E = nedges;
   return 0;
 }
