@@ -67,7 +67,7 @@ def env_int(k, d):
 PROFILES = {
     ("het42-70b", "score"): ("r02_het42_score_raw.csv", 200_000),
     ("het42-70b", "parity"): ("r01_parity_mode_raw.csv", 200_000),
-    ("syn256-120l", "score"): ("r01_syn256_score_raw.csv", 20_000),
+    ("syn256-120l", "score"): ("r02_syn256_score_raw.csv", 20_000),
 }
 
 

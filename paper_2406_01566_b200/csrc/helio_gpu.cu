@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <thread>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -602,6 +603,26 @@ int ensure_stage(helio_gpu_ctx* ctx, int64_t chunk) {
   return HELIO_OK;
 }
 
+// Pageable <-> pinned staging copies: large ones are split over a few host
+// threads (one thread copies ~10 GB/s; het42's 256k-row chunk is 43 MB).
+void stage_copy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kPart = size_t(8) << 20;
+  const int nt = (int)std::min<size_t>(8, bytes / kPart);
+  if (nt < 2) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const size_t step = (bytes + nt - 1) / nt;
+  for (int t = 1; t < nt; ++t) {
+    const size_t lo = t * step, hi = std::min(bytes, lo + step);
+    if (lo < hi)
+      pool.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo); });
+  }
+  std::memcpy(dst, src, std::min(bytes, step));
+  for (auto& th : pool) th.join();
+}
+
 bool is_pinned(const void* p) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -1139,13 +1160,13 @@ int score_host_impl(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allo
       CK(cudaStreamSynchronize(st));
       if (want_vals && !pin_out) {
         const int64_t plo = clo[c - helio_gpu_ctx::kPipeSets], pn = cn[c - helio_gpu_ctx::kPipeSets];
-        std::memcpy(h_values + plo, ctx->h_val_pin[s], sizeof(double) * pn);
-        std::memcpy(h_status + plo, ctx->h_st_pin[s], sizeof(int32_t) * pn);
+        stage_copy(h_values + plo, ctx->h_val_pin[s], sizeof(double) * pn);
+        stage_copy(h_status + plo, ctx->h_st_pin[s], sizeof(int32_t) * pn);
       }
     }
     const void* src = h_pl + lo * 2 * ctx->N;
     if (!pin_in) {
-      std::memcpy(ctx->h_pl_pin[s], src, row * n);
+      stage_copy(ctx->h_pl_pin[s], src, row * n);
       src = ctx->h_pl_pin[s];
     }
     CK(cudaMemcpyAsync(ctx->d_pl[s], src, row * n, cudaMemcpyHostToDevice, st));
@@ -1169,8 +1190,8 @@ int score_host_impl(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t B, int allo
     CK(cudaStreamSynchronize(ctx->pipe[s]));
     if (want_vals && !pin_out) {
       const int64_t lo = clo[c], n = cn[c];
-      std::memcpy(h_values + lo, ctx->h_val_pin[s], sizeof(double) * n);
-      std::memcpy(h_status + lo, ctx->h_st_pin[s], sizeof(int32_t) * n);
+      stage_copy(h_values + lo, ctx->h_val_pin[s], sizeof(double) * n);
+      stage_copy(h_status + lo, ctx->h_st_pin[s], sizeof(int32_t) * n);
     }
   }
   if (h_best) {
