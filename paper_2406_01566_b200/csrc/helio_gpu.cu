@@ -75,8 +75,16 @@ struct FlowOut {
 // push-relabel solver, for clusters whose split graphs exceed 128 vertices
 // (N >= 64), so that path's register allocation is its own; the default one
 // keeps both paths (het42 runs it at 64 registers, 8 CTAs per SM).
+// HELIO_PARITY_DIAG_MINB (diagnostic builds only): cap the PARITY kernel's
+// registers through __launch_bounds__(128, n) — the configuration that faults
+// (see DESIGN.md §4), for bounds-checked reproduction with HELIO_BOUNDS.
+#ifdef HELIO_PARITY_DIAG_MINB
+#define HELIO_SCORE_BOUNDS __launch_bounds__(128, MODE == HELIO_MODE_PARITY ? HELIO_PARITY_DIAG_MINB : 1)
+#else
+#define HELIO_SCORE_BOUNDS
+#endif
 template <int MODE, bool GEN, bool GLOBAL = false>
-__global__ void score_kernel(ClusterDev cd, Layout lay, const int16_t* __restrict__ pl, int64_t B,
+__global__ void HELIO_SCORE_BOUNDS score_kernel(ClusterDev cd, Layout lay, const int16_t* __restrict__ pl, int64_t B,
                                            int partial, double* __restrict__ values, int32_t* __restrict__ status,
                                            unsigned long long* work, const int64_t* in_list,
                                            const unsigned int* in_count, int64_t* out_list, unsigned int* out_count,

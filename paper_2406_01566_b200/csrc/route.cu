@@ -131,9 +131,20 @@ __global__ void route_apply(int64_t R, int x, int L, int max_hops, const int32_t
 // (it does not depend on it).  A deferred request leaves the positions it
 // advanced, as IwrrPicker::next does (scheduler.cpp:165-168 rolls back only
 // the KV charges).
-// REG: every vertex's (cycle base, cycle length, position) lives in the
-// registers of lane x (plans with at most 32 vertices — one coordinator plus
-// up to 31 placed nodes); otherwise in shared memory.
+// One 32-byte record per cycle slot: the slot's edge (threshold 0.9 *
+// kv_cap[dst] — +inf for the coordinator — and exec length as doubles; dst,
+// exec range, node of dst) plus the cycle geometry (next slot, the cycle's
+// base and length), so a pick is one shuffle (the vertex's current slot) and
+// one record load.
+struct alignas(16) SlotRec {
+  double thr, len;
+  int16_t next, base, W, dst;
+  int16_t es, ee, node, pad;
+};
+
+// REG: vertex x's current absolute slot lives in lane x's register (plans up
+// to 32 vertices — the coordinator plus up to 31 placed nodes); otherwise in
+// shared memory.
 template <bool REG>
 __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double kvb,
                                   const int32_t* __restrict__ obeg, const int32_t* __restrict__ odst,
@@ -145,35 +156,28 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
                                   long long* deferred, int* err) {
   extern __shared__ __align__(16) char sm[];
   const int lane = threadIdx.x;
-  // Slot-ordered records: vertex x's cycle occupies slots [base_x, base_x +
-  // W_x); slot k carries its edge's (threshold, exec length) as doubles and
-  // (dst, exec_start, exec_end, node of dst) as int16, so a pick costs one
-  // slot load.  Threshold = 0.9 * kv_cap[dst]; the coordinator never masks.
-  int32_t* vstate = reinterpret_cast<int32_t*>(sm);  // [nv][4]: base, W, pos, -
-  double2* srec = reinterpret_cast<double2*>(sm + (((size_t)16 * nv + 15) & ~size_t(15)));
-  int W_tot = 0;
-  int my_base = 0, my_W = 0, my_pos = 0;
-  for (int x = 0; x < nv; ++x) {
-    const int W = obeg[x + 1] > obeg[x] ? cyc_len[x] : 0;
-    if (REG && lane == x) {
-      my_base = W_tot;
-      my_W = W;
-    }
-    if (!REG && lane == 0) {
-      vstate[4 * x] = W_tot;
-      vstate[4 * x + 1] = W;
-      vstate[4 * x + 2] = 0;
-    }
-    W_tot += W;
-  }
-  short4* smeta = reinterpret_cast<short4*>(srec + W_tot);
+  int32_t* vcur = reinterpret_cast<int32_t*>(sm);  // [nv] current slot (-1: no out-edges)
+  SlotRec* rec = reinterpret_cast<SlotRec*>(sm + (((size_t)4 * nv + 15) & ~size_t(15)));
+  int my_cur = -1;
   for (int x = 0, base = 0; x < nv; ++x) {
     const int W = obeg[x + 1] > obeg[x] ? cyc_len[x] : 0;
+    if (REG && lane == x) my_cur = W ? base : -1;
+    if (!REG && lane == 0) vcur[x] = W ? base : -1;
     for (int k = lane; k < W; k += 32) {
       const int e = obeg[x] + cyc[32 * obeg[x] + k];
       const int d = odst[e];
-      srec[base + k] = make_double2(d == 0 ? 1.0e308 : 0.9 * kv_cap[d], (double)(oee[e] - oes[e]));
-      smeta[base + k] = make_short4((short)d, (short)oes[e], (short)oee[e], (short)node_of[d]);
+      SlotRec r;
+      r.thr = d == 0 ? 1.0e308 : 0.9 * kv_cap[d];
+      r.len = (double)(oee[e] - oes[e]);
+      r.next = (int16_t)(k + 1 == W ? base : base + k + 1);
+      r.base = (int16_t)base;
+      r.W = (int16_t)W;
+      r.dst = (int16_t)d;
+      r.es = (int16_t)oes[e];
+      r.ee = (int16_t)oee[e];
+      r.node = (int16_t)node_of[d];
+      r.pad = 0;
+      rec[base + k] = r;
     }
     base += W;
   }
@@ -192,27 +196,17 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
       int v = 0, covered = 0, h = 0;
       bool ok = true;
       do {
-        int base, W, p;
-        if (REG) {
-          base = __shfl_sync(0xffffffffu, my_base, v);
-          W = __shfl_sync(0xffffffffu, my_W, v);
-          p = __shfl_sync(0xffffffffu, my_pos, v);
-        } else {
-          const int4 vs = reinterpret_cast<const int4*>(vstate)[v];
-          base = vs.x;
-          W = vs.y;
-          p = vs.z;
-        }
-        if (W == 0) {  // no out-edges: IwrrPicker::next returns -1
+        const int slot = REG ? __shfl_sync(0xffffffffu, my_cur, v) : vcur[v];
+        if (slot < 0) {  // no out-edges: IwrrPicker::next returns -1
           ok = false;
           break;
         }
-        // the slot at the current position first (the common case), then
-        // the rest of one full cycle 32 slots at a time
-        int slot = base + p, np = p + 1 == W ? 0 : p + 1;
-        const double2 rc = srec[slot];
-        if (!(tk * rc.y <= rc.x)) {
-          slot = -1;
+        SlotRec rc = rec[slot];
+        int nxt = rc.next;
+        if (!(tk * rc.len <= rc.thr)) {
+          // the rest of one full cycle, 32 slots at a time
+          const int base = rc.base, W = rc.W, p = slot - base;
+          int pick = -1;
           for (int k0 = 1; k0 < W; k0 += 32) {
             const int k = k0 + lane;
             bool el = false;
@@ -220,46 +214,42 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
             if (k < W) {
               const int q = p + k;
               sl = base + (q >= W ? q - W : q);
-              const double2 x = srec[sl];
-              el = tk * x.y <= x.x;
+              el = tk * rec[sl].len <= rec[sl].thr;
             }
             const unsigned m = __ballot_sync(0xffffffffu, el);
             if (m) {
-              const int jl = __ffs(m) - 1;
-              slot = __shfl_sync(0xffffffffu, sl, jl);
-              int q = p + k0 + jl + 1;
-              while (q >= W) q -= W;
-              np = q;
+              pick = __shfl_sync(0xffffffffu, sl, __ffs(m) - 1);
               break;
             }
           }
-          if (slot < 0) {  // one full cycle with nothing eligible: position unchanged
+          if (pick < 0) {  // one full cycle with nothing eligible: position unchanged
             ok = false;
             break;
           }
+          rc = rec[pick];
+          nxt = rc.next;
         }
-        const short4 mt = smeta[slot];
-        if (mt.x == 0 || mt.y != covered) {  // scheduler.cpp:170-171
+        if (rc.dst == 0 || rc.es != covered) {  // scheduler.cpp:170-171
           if (lane == 0) atomicExch(err, 1);
           return;
         }
         if (REG) {
-          if (lane == v) my_pos = np;
+          if (lane == v) my_cur = nxt;
         } else {
-          if (lane == 0) vstate[4 * v + 2] = np;
+          if (lane == 0) vcur[v] = nxt;
           __syncwarp();
         }
         if (store_hops && lane == 0 && h < max_hops) {
           const int64_t at = (r0 + j) * max_hops + h;
-          hop_node[at] = mt.w;
+          hop_node[at] = rc.node;
           if (hop_s) {
-            hop_s[at] = mt.y;
-            hop_e[at] = mt.z;
+            hop_s[at] = rc.es;
+            hop_e[at] = rc.ee;
           }
         }
         ++h;
-        covered = mt.z;
-        v = mt.x;
+        covered = rc.ee;
+        v = rc.dst;
       } while (covered < L);
       if (ok) {  // complete(): the running mean (scheduler.cpp:183-190)
         const int out = __shfl_sync(0xffffffffu, my_out, j);
@@ -483,9 +473,22 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
     }
   } else if (!rc && R > 0) {
     {
-      // slot records: 24 bytes per slot; every cycle fits 32 slots per edge
-      const size_t smem = (((size_t)16 * nv + 15) & ~size_t(15)) + (size_t)cyc_off[nv] * 24 + 16;
-      if (smem > 227 * 1024) {
+      // slot records: 32 bytes per slot (int16 slot indices); every cycle
+      // fits 32 slots per edge — when that bound does not fit shared memory,
+      // read the actual cycle lengths back
+      int64_t slots = cyc_off[nv];
+      const size_t head = ((size_t)4 * nv + 15) & ~size_t(15);
+      if (head + (size_t)slots * sizeof(SlotRec) > 227 * 1024) {
+        std::vector<int32_t> cl(nv);
+        if (cudaMemcpyAsync(cl.data(), d_cyclen, 4 * nv, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+          rc = fail(ctx, HELIO_ERR_CUDA, "route: cycle lengths read-back failed");
+        slots = 0;
+        for (int x = 0; x < nv; ++x) slots += obeg[x + 1] > obeg[x] ? cl[x] : 0;
+      }
+      const size_t smem = head + (size_t)slots * sizeof(SlotRec) + 16;
+      if (rc) {
+      } else if (smem > 227 * 1024 || slots > 32767) {
         rc = fail(ctx, HELIO_ERR_TOO_LARGE, "plan too large for the masked routing kernel's shared memory");
       } else {
         auto kern = nv <= 32 ? route_masked_warp<true> : route_masked_warp<false>;

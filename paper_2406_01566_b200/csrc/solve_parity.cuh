@@ -25,6 +25,22 @@ namespace {
 // (every lane holds the same two 64-bit words, so the enqueue test is a
 // uniform register test), and a failed scan of the last arc chunk falls
 // straight into the relabel instead of taking another loop trip.
+// HELIO_BOUNDS (diagnostic builds only): trap on an out-of-range slot index.
+#ifdef HELIO_BOUNDS
+#define HB_CHECK(idx, lim, tag)                                                                    \
+  do {                                                                                             \
+    if ((unsigned)(idx) >= (unsigned)(lim)) {                                                      \
+      printf("HELIO_BOUNDS %s idx=%d lim=%d block=%d lane=%d\n", tag, (int)(idx), (int)(lim),       \
+             (int)blockIdx.x, (int)(threadIdx.x & 31));                                            \
+      __trap();                                                                                    \
+    }                                                                                              \
+  } while (0)
+#else
+#define HB_CHECK(idx, lim, tag) \
+  do {                          \
+  } while (0)
+#endif
+
 __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, const int lane) {
   VState* vs = g.vs;
   for (int x = lane; x < n; x += 32) {
@@ -84,6 +100,7 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
   while (qcount > 0) {
     __syncwarp();
     const int u = g.q[head];
+    HB_CHECK(u, n, "queue vertex");
     head = head + 1 == n ? 0 : head + 1;
     --qcount;
     const VState su = vs[u];
@@ -105,6 +122,7 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
         ca = g.cap[a];
         ta = g.to[a];
         ra = g.rv[a];
+        HB_CHECK(ta, n, "fast arc head");
         hp1 = vs[ta].h + 1;
       }
       bool live = inr && ca > FLOW_EPS;  // residual arc: changes only when this lane pushes
@@ -123,10 +141,12 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
             g.cap[b + j] = ca;
             g.cap[ra] += amt;
           }
+          HB_CHECK(tj, n, "fast push target");
           if (lane == 0) vs[tj].ex += amt;
           ex -= amt;
           if (tj != s && tj != t && !in_queue(tj)) {
             mark(tj, true);
+            HB_CHECK(tail, n, "fast tail");
             if (lane == 0) g.q[tail] = (int16_t)tj;
             tail = tail + 1 == n ? 0 : tail + 1;
             ++qcount;
@@ -136,6 +156,8 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
         // relabel (:180-199)
         const int old = hu;
         const int best = __reduce_min_sync(FULL, live ? hp1 : two_n);
+        HB_CHECK(best, two_n + 1, "fast best");
+        HB_CHECK(old, two_n + 1, "fast old");
         hu = best;
         cu = 0;
         int cold = 0;
