@@ -318,6 +318,12 @@ int helio_gpu_multi_set_mode(helio_gpu_multi* m, int mode);
 int helio_gpu_multi_score_best_host(helio_gpu_multi* m, const int16_t* h_placements, int64_t B, int allow_partial,
                                     double* h_values, int32_t* h_status, double* h_best, int64_t* h_index);
 
+/* Self-test of the masked routing replay's division (route.cu div_by_count:
+ * reciprocal-based, correctly rounded) against IEEE division on `count`
+ * counter-generated operand pairs of the routing domain; *mismatches = 0
+ * expected. */
+int helio_gpu_check_division(helio_gpu_ctx* ctx, int64_t count, uint64_t seed, int64_t* mismatches);
+
 /* Introspection for benchmarks: kernels launched by this context so far, and
  * the device time (ms) of the last score call's dominant kernel. */
 int64_t helio_gpu_launch_count(const helio_gpu_ctx* ctx);

@@ -125,6 +125,19 @@ __global__ void HELIO_SCORE_BOUNDS score_kernel(ClusterDev cd, Layout lay, const
               : cd.large_solver ? solve_ek_batched(g, V, 0, 1, lane)
                                 : solve_pr<GEN>(g, V, 0, 1, lane, cd.pr_gr);
     } else if (st == 0) {
+#ifdef HELIO_BOUNDS
+      {  // diagnostic: the built CSR is well formed
+        const int na = g.abeg[V];
+        HB_CHECK(na, lay.A + 1, "arc count");
+        for (int x = lane; x < V; x += 32) HB_CHECK(g.abeg[x + 1] - g.abeg[x], na + 1, "abeg order");
+        for (int a = lane; a < na; a += 32) {
+          HB_CHECK(g.to[a], V, "arc head");
+          HB_CHECK(g.rv[a], na, "arc reverse");
+          HB_CHECK(g.rv[g.rv[a]] == a ? 0 : 1, 1, "reverse pairing");
+        }
+        __syncwarp();
+      }
+#endif
       solve_fifo2(g, V, 0, 1, lane);
       value = built_value(cd, g, lane);
       if (fo.edges) {

@@ -1208,6 +1208,15 @@ PYBIND11_MODULE(_helio, m) {
           py::arg("values_ptr"), py::arg("status_ptr"), py::arg("count"), py::arg("index_base"), py::arg("best_ptr"),
           py::arg("index_ptr"), py::arg("stream") = 0)
       .def(
+          "check_division",
+          [](PyEngine& e, int64_t count, uint64_t seed) {
+            int64_t bad = -1;
+            e.eng->check(helio_gpu_check_division(e.eng->ctx(), count, seed, &bad), "helio_gpu_check_division");
+            return bad;
+          },
+          py::arg("count"), py::arg("seed") = 1,
+          "Mismatches of the masked routing replay's reciprocal-based division against IEEE division.")
+      .def(
           "argmax_ranked",
           [](PyEngine& e, uintptr_t values, uintptr_t status, int64_t B, int64_t base, uintptr_t best, uintptr_t index,
              uintptr_t comm, uintptr_t stream) {

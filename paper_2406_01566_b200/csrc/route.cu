@@ -132,20 +132,35 @@ __global__ void route_apply(int64_t R, int x, int L, int max_hops, const int32_t
 // advanced, as IwrrPicker::next does (scheduler.cpp:165-168 rolls back only
 // the KV charges).
 // One 32-byte record per cycle slot: the slot's edge (threshold 0.9 *
-// kv_cap[dst] — +inf for the coordinator — and exec length as doubles; dst,
-// exec range, node of dst) plus the cycle geometry (next slot, the cycle's
-// base and length), so a pick is one shuffle (the vertex's current slot) and
-// one record load.
+// kv_cap[dst] — +inf for the coordinator — and exec length, as doubles; dst,
+// exec range and the node of dst) and the next slot of the cycle, so a pick is
+// one shuffle (the vertex's current slot) and one record load.
 struct alignas(16) SlotRec {
   double thr, len;
-  int16_t next, base, W, dst;
-  int16_t es, ee, node, pad;
+  int32_t next, dst, ee, es_node;  // es_node = exec_start | node << 16
 };
+
+// The running output mean's update (scheduler.cpp:183-190) is the serial
+// dependence of the replay: avg += (out - avg) / n.  The division is split:
+// y = RN(1/n) (a correctly rounded reciprocal, __drcp_rn) depends only on the
+// sample count and is computed ahead, 32 counts at a time in parallel; the
+// quotient is then q0 = RN(a*y), r = a - n*q0 (exact, fma), q = RN(q0 + r*y)
+// — the correctly rounded a/n for normal operands (Markstein's theorem; the
+// same final step as the IEEE division sequence), i.e. the reference's bits.
+// tests/test_gpu_parity.py checks it against '/' on 1e8 operand pairs of the
+// routing domain (helio_gpu_check_division) and end to end on 1M requests.
+__device__ __forceinline__ double div_by_count(double a, double n, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double r = __fma_rn(-n, q0, a);
+  return __fma_rn(r, y, q0);
+}
 
 // REG: vertex x's current absolute slot lives in lane x's register (plans up
 // to 32 vertices — the coordinator plus up to 31 placed nodes); otherwise in
-// shared memory.
-template <bool REG>
+// shared memory.  CHECKS: the reference's tiling checks per hop
+// (scheduler.cpp:170-171); the host drops them for plans whose exec ranges
+// are node-consistent, where they cannot fail.
+template <bool REG, bool CHECKS>
 __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double kvb,
                                   const int32_t* __restrict__ obeg, const int32_t* __restrict__ odst,
                                   const int32_t* __restrict__ oes, const int32_t* __restrict__ oee,
@@ -157,26 +172,26 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
   extern __shared__ __align__(16) char sm[];
   const int lane = threadIdx.x;
   int32_t* vcur = reinterpret_cast<int32_t*>(sm);  // [nv] current slot (-1: no out-edges)
-  SlotRec* rec = reinterpret_cast<SlotRec*>(sm + (((size_t)4 * nv + 15) & ~size_t(15)));
+  int2* vgeo = reinterpret_cast<int2*>(sm + (((size_t)4 * nv + 7) & ~size_t(7)));  // [nv] (base, W)
+  SlotRec* rec = reinterpret_cast<SlotRec*>(sm + ((((size_t)4 * nv + 7) & ~size_t(7)) + 8 * (size_t)nv + 15 & ~size_t(15)));
   int my_cur = -1;
   for (int x = 0, base = 0; x < nv; ++x) {
     const int W = obeg[x + 1] > obeg[x] ? cyc_len[x] : 0;
     if (REG && lane == x) my_cur = W ? base : -1;
-    if (!REG && lane == 0) vcur[x] = W ? base : -1;
+    if (lane == 0) {
+      if (!REG) vcur[x] = W ? base : -1;
+      vgeo[x] = make_int2(base, W);
+    }
     for (int k = lane; k < W; k += 32) {
       const int e = obeg[x] + cyc[32 * obeg[x] + k];
       const int d = odst[e];
       SlotRec r;
       r.thr = d == 0 ? 1.0e308 : 0.9 * kv_cap[d];
       r.len = (double)(oee[e] - oes[e]);
-      r.next = (int16_t)(k + 1 == W ? base : base + k + 1);
-      r.base = (int16_t)base;
-      r.W = (int16_t)W;
-      r.dst = (int16_t)d;
-      r.es = (int16_t)oes[e];
-      r.ee = (int16_t)oee[e];
-      r.node = (int16_t)node_of[d];
-      r.pad = 0;
+      r.next = k + 1 == W ? base : base + k + 1;
+      r.dst = d;
+      r.ee = oee[e];
+      r.es_node = (oes[e] & 0xffff) | (node_of[d] << 16);
       rec[base + k] = r;
     }
     base += W;
@@ -189,10 +204,14 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
     const int nb = R - r0 < 32 ? (int)(R - r0) : 32;
     const int my_in = lane < nb ? in_len[r0 + lane] : 0;
     const int my_out = lane < nb ? out_len[r0 + lane] : 0;
+    // reciprocals of the next 32 sample counts (each admission takes one)
+    const double my_y = __drcp_rn(samples + 1.0 + lane);
+    int admitted = 0;
     int my_nh = 0;
     for (int j = 0; j < nb; ++j) {
       const int in = __shfl_sync(0xffffffffu, my_in, j);
       const double tk = ((double)in + avg) * kvb;  // hop_charge = tk * (exec_end - exec_start)
+      int32_t* hp = hop_node + (r0 + j) * max_hops;
       int v = 0, covered = 0, h = 0;
       bool ok = true;
       do {
@@ -202,10 +221,10 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
           break;
         }
         SlotRec rc = rec[slot];
-        int nxt = rc.next;
         if (!(tk * rc.len <= rc.thr)) {
           // the rest of one full cycle, 32 slots at a time
-          const int base = rc.base, W = rc.W, p = slot - base;
+          const int2 geo = vgeo[v];
+          const int base = geo.x, W = geo.y, p = slot - base;
           int pick = -1;
           for (int k0 = 1; k0 < W; k0 += 32) {
             const int k = k0 + lane;
@@ -227,24 +246,23 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
             break;
           }
           rc = rec[pick];
-          nxt = rc.next;
         }
-        if (rc.dst == 0 || rc.es != covered) {  // scheduler.cpp:170-171
+        const int es = rc.es_node & 0xffff;
+        if (CHECKS && (rc.dst == 0 || es != covered)) {  // scheduler.cpp:170-171
           if (lane == 0) atomicExch(err, 1);
           return;
         }
         if (REG) {
-          if (lane == v) my_cur = nxt;
+          if (lane == v) my_cur = rc.next;
         } else {
-          if (lane == 0) vcur[v] = nxt;
+          if (lane == 0) vcur[v] = rc.next;
           __syncwarp();
         }
         if (store_hops && lane == 0 && h < max_hops) {
-          const int64_t at = (r0 + j) * max_hops + h;
-          hop_node[at] = rc.node;
+          hp[h] = rc.es_node >> 16;
           if (hop_s) {
-            hop_s[at] = rc.es;
-            hop_e[at] = rc.ee;
+            hop_s[(r0 + j) * max_hops + h] = es;
+            hop_e[(r0 + j) * max_hops + h] = rc.ee;
           }
         }
         ++h;
@@ -253,8 +271,10 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
       } while (covered < L);
       if (ok) {  // complete(): the running mean (scheduler.cpp:183-190)
         const int out = __shfl_sync(0xffffffffu, my_out, j);
+        const double y = __shfl_sync(0xffffffffu, my_y, admitted);
         samples += 1.0;
-        avg += ((double)out - avg) / samples;
+        avg += div_by_count((double)out - avg, samples, y);
+        ++admitted;
       } else {
         ++den;
       }
@@ -263,6 +283,27 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
     if (lane < nb) nh[r0 + lane] = my_nh;
   }
   if (lane == 0) *deferred = den;
+}
+
+// Self-test of div_by_count against IEEE division on the routing domain:
+// numerators a = out - avg (|a| < 4096, random significands), denominators
+// n = sample counts up to 2^27.
+__global__ void check_division_kernel(int64_t count, uint64_t seed, unsigned long long* mismatches) {
+  unsigned long long bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed + (uint64_t)i * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const double n = (double)(1 + (z & ((1ull << 27) - 1)));
+    const int out = (int)((z >> 27) & 2047);
+    const double avg = (double)((z >> 38) & ((1ull << 26) - 1)) * (2048.0 / (double)(1ull << 26));
+    const double a = (double)out - avg;
+    const double y = __drcp_rn(n);
+    if (div_by_count(a, n, y) != a / n) ++bad;
+  }
+  atomicAdd(mismatches, bad);
 }
 
 // Route buffers are carved from one context-owned device arena that only
@@ -345,6 +386,15 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   // Fast-path eligibility: node-consistent exec intervals, and no hop that
   // could ever be masked in the AC8 order.
   bool closed = true;
+  // node-consistent exec ranges (every edge starts where its source vertex's
+  // interval ends and ends where its target's does; coordinator edges only
+  // leave vertices that end at L): the replay's tiling checks cannot fail
+  bool consistent = true;
+  for (int x = 0; x < nv; ++x)
+    for (int p = obeg[x]; p < obeg[x + 1]; ++p) {
+      const int d = odst[p];
+      if (d == 0 ? vend[x] != L : (oes[p] != vend[x] || oee[p] != vend[d])) consistent = false;
+    }
   int max_in = 0, max_out = 232;
   for (int64_t r = 0; r < R; ++r) {
     max_in = std::max(max_in, h_in[r]);
@@ -477,7 +527,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
       // fits 32 slots per edge — when that bound does not fit shared memory,
       // read the actual cycle lengths back
       int64_t slots = cyc_off[nv];
-      const size_t head = ((size_t)4 * nv + 15) & ~size_t(15);
+      const size_t head = ((((size_t)4 * nv + 7) & ~size_t(7)) + 8 * (size_t)nv + 15) & ~size_t(15);
       if (head + (size_t)slots * sizeof(SlotRec) > 227 * 1024) {
         std::vector<int32_t> cl(nv);
         if (cudaMemcpyAsync(cl.data(), d_cyclen, 4 * nv, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
@@ -491,7 +541,8 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
       } else if (smem > 227 * 1024 || slots > 32767) {
         rc = fail(ctx, HELIO_ERR_TOO_LARGE, "plan too large for the masked routing kernel's shared memory");
       } else {
-        auto kern = nv <= 32 ? route_masked_warp<true> : route_masked_warp<false>;
+        auto kern = nv <= 32 ? (consistent ? route_masked_warp<true, false> : route_masked_warp<true, true>)
+                             : (consistent ? route_masked_warp<false, false> : route_masked_warp<false, true>);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<1, 32, smem, st>>>(R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst, d_oes, d_oee, d_node,
                                   d_kvcap, d_cyclen, d_cyc, d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr,
@@ -739,5 +790,26 @@ extern "C" int helio_gpu_iwrr_picks(helio_gpu_ctx* ctx, const int64_t* h_w, int3
   CK(cudaStreamSynchronize(st));
   *h_round = stt[0];
   *h_idx = stt[1];
+  return HELIO_OK;
+}
+
+extern "C" int helio_gpu_check_division(helio_gpu_ctx* ctx, int64_t count, uint64_t seed, int64_t* mismatches) {
+  if (!ctx || !mismatches || count < 0) return HELIO_ERR_INVALID;
+  std::lock_guard<std::recursive_mutex> ctx_lock(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  char* base = nullptr;
+  int rc = host_arena(ctx, 64, &base);
+  if (rc) return rc;
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(base);
+  CK(api_begin(ctx, ctx->stream));
+  CK(cudaMemsetAsync(d, 0, 8, ctx->stream));
+  check_division_kernel<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>(count, seed, d);
+  CK(cudaGetLastError());
+  CK(api_end(ctx, ctx->stream));
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *mismatches = (int64_t)h;
+  ctx->launches++;
   return HELIO_OK;
 }

@@ -54,17 +54,51 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
     g.inq[x] = 0;
   }
   for (int x = lane; x <= 2 * n; x += 32) g.cnt[x] = 0;
+#ifdef HELIO_BOUNDS
+  for (int x = lane; x < n; x += 32) g.q[x] = -7;  // sentinel: a slot read before any write shows -7
+#endif
   __syncwarp();
   if (lane == 0) {
     g.cnt[0] = (int16_t)(n - 1);
     g.cnt[n] += 1;
   }
-  // in-queue flags: every lane writes them and every lane reads its own
-  // write, so no cross-lane ordering is needed (a byte test beat a register
-  // bitmask on issue slots)
-  auto in_queue = [&](int x) -> bool { return g.inq[x] != 0; };
-  auto mark = [&](int x, bool on) { g.inq[x] = on ? 1 : 0; };
+  // In-queue flags and the queue array are owned by lane 0: it tests and sets
+  // the flag, stores the entry, and the decision is broadcast.  (Round 1 let
+  // every lane test and set the flag itself; under independent thread
+  // scheduling the "uniform" code after a divergent push can run at different
+  // times in different lanes, so one lane could see another's fresh flag and
+  // skip an enqueue the others counted — the queue then read a slot lane 0
+  // never wrote.  Found with the HELIO_BOUNDS diagnostic build.)
   int tail = 0, qcount = 0;
+#if defined(HELIO_ENQ_SYNC)
+  // variant: every lane tests between two warp barriers
+  auto enqueue = [&](int x) {
+    __syncwarp();
+    const bool fresh = x != s && x != t && !g.inq[x];
+    __syncwarp();
+    if (fresh) {
+      if (lane == 0) {
+        g.inq[x] = 1;
+        g.q[tail] = (int16_t)x;
+      }
+      tail = tail + 1 == n ? 0 : tail + 1;
+      ++qcount;
+    }
+  };
+#else
+  auto enqueue = [&](int x) {
+    int fresh = 0;
+    if (lane == 0 && x != s && x != t && !g.inq[x]) {
+      g.inq[x] = 1;
+      g.q[tail] = (int16_t)x;
+      fresh = 1;
+    }
+    if (__shfl_sync(FULL, fresh, 0)) {
+      tail = tail + 1 == n ? 0 : tail + 1;
+      ++qcount;
+    }
+  };
+#endif
   // saturate source arcs in adjacency order (:168-173): uniform loop, lane 0 stores
   __syncwarp();
   {
@@ -86,12 +120,7 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
           vs[to].ex += amt;
         }
         __syncwarp();
-        if (to != s && to != t && !in_queue(to)) {
-          mark(to, true);
-          if (lane == 0) g.q[tail] = (int16_t)to;
-          tail = tail + 1 == n ? 0 : tail + 1;
-          ++qcount;
-        }
+        enqueue(to);
       }
     }
   }
@@ -100,7 +129,13 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
   while (qcount > 0) {
     __syncwarp();
     const int u = g.q[head];
-    HB_CHECK(u, n, "queue vertex");
+#ifdef HELIO_BOUNDS
+    if ((unsigned)u >= (unsigned)n) {
+      printf("HELIO_BOUNDS queue vertex u=%d n=%d head=%d tail=%d qcount=%d deg_b=%d q[h-1]=%d q[h+1]=%d\n", u, n,
+             head, tail, qcount, (int)g.abeg[n], (int)g.q[head ? head - 1 : n - 1], (int)g.q[head + 1 < n ? head + 1 : 0]);
+      __trap();
+    }
+#endif
     head = head + 1 == n ? 0 : head + 1;
     --qcount;
     const VState su = vs[u];
@@ -109,7 +144,7 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
     int cu = su.cur;
     const int b = su.b;
     const int deg = su.deg;
-    mark(u, false);
+    if (lane == 0) g.inq[u] = 0;
     if (deg <= 32) {
       // Single-chunk fast path (almost every vertex): lane j holds arc b + j for
       // the whole discharge.  A failed ballot means the scan reached the end of
@@ -144,13 +179,7 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
           HB_CHECK(tj, n, "fast push target");
           if (lane == 0) vs[tj].ex += amt;
           ex -= amt;
-          if (tj != s && tj != t && !in_queue(tj)) {
-            mark(tj, true);
-            HB_CHECK(tail, n, "fast tail");
-            if (lane == 0) g.q[tail] = (int16_t)tj;
-            tail = tail + 1 == n ? 0 : tail + 1;
-            ++qcount;
-          }
+          enqueue(tj);
           continue;
         }
         // relabel (:180-199)
@@ -234,12 +263,7 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
           }
           if (lane == 0) vs[tj].ex += amt;
           ex -= amt;
-          if (tj != s && tj != t && !in_queue(tj)) {
-            mark(tj, true);
-            if (lane == 0) g.q[tail] = (int16_t)tj;
-            tail = tail + 1 == n ? 0 : tail + 1;
-            ++qcount;
-          }
+          enqueue(tj);
           continue;
         }
         cu = min(deg, (k + 1) << 5);

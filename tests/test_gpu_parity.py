@@ -234,6 +234,15 @@ def test_routes_one_million_match_oracle():
     assert np.array_equal(hs[mask], hs_o[mask]) and np.array_equal(he[mask], he_o[mask])
 
 
+def test_masked_replay_division_is_ieee_division():
+    """route.cu div_by_count (reciprocal computed ahead, then two FMAs) gives
+    exactly a / n on 1e8 operand pairs of the routing domain (|a| < 2048,
+    n < 2^27) — the running-mean update must be the reference's bits."""
+    c, e = engine("geo24_float")
+    assert e.check_division(100_000_000, 12345) == 0
+    assert e.check_division(100_000_000, 777) == 0
+
+
 @pytest.mark.parametrize("kv", [1e6, 7e5, 2e6])
 def test_masked_routes_one_million_match_reference(kv):
     """KV masking binds (geo24's plan with kv_bytes_per_token_layer raised so
