@@ -62,16 +62,17 @@ __device__ void solve_fifo2(const Gs& g, const int n, const int s, const int t, 
     g.cnt[0] = (int16_t)(n - 1);
     g.cnt[n] += 1;
   }
-  // In-queue flags and the queue array are owned by lane 0: it tests and sets
-  // the flag, stores the entry, and the decision is broadcast.  (Round 1 let
+  // In-queue flags and the queue array are written by lane 0 only, and the
+  // flag is tested by all lanes between two warp barriers.  (Round 1 let
   // every lane test and set the flag itself; under independent thread
   // scheduling the "uniform" code after a divergent push can run at different
   // times in different lanes, so one lane could see another's fresh flag and
   // skip an enqueue the others counted — the queue then read a slot lane 0
   // never wrote.  Found with the HELIO_BOUNDS diagnostic build.)
   int tail = 0, qcount = 0;
-#if defined(HELIO_ENQ_SYNC)
-  // variant: every lane tests between two warp barriers
+#if !defined(HELIO_ENQ_SHFL)
+  // every lane tests the flag between two warp barriers (so all lanes see the
+  // same state), lane 0 alone sets it and stores the entry
   auto enqueue = [&](int x) {
     __syncwarp();
     const bool fresh = x != s && x != t && !g.inq[x];
