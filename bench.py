@@ -754,6 +754,13 @@ def main():
     from paper_2406_01566_b200 import clusters
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    # the JSON line is this process's only stdout: library chatter (NCCL's
+    # version banner at communicator init) goes to stderr
+    json_out = sys.stdout
+    if world > 1:
+        sys.stdout.flush()
+        json_out = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -1035,7 +1042,7 @@ def main():
             "search": search,
             "clocks": clocks,
         }
-        print(json.dumps(out))
+        print(json.dumps(out), file=json_out, flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

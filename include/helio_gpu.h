@@ -317,6 +317,12 @@ int helio_gpu_multi_set_cluster(helio_gpu_multi* m, const helio_cluster_desc* de
 int helio_gpu_multi_set_mode(helio_gpu_multi* m, int mode);
 int helio_gpu_multi_score_best_host(helio_gpu_multi* m, const int16_t* h_placements, int64_t B, int allow_partial,
                                     double* h_values, int32_t* h_status, double* h_best, int64_t* h_index);
+/* helio_gpu_sampled_search with every round's mutants split over the devices:
+ * the same mutants, the same first-maximum tie-break — the same result as one
+ * device. */
+int helio_gpu_multi_sampled_search(helio_gpu_multi* m, const int16_t* h_seed, int allow_partial, int32_t iterations,
+                                   int64_t batch, int32_t max_changes, uint64_t rng_seed, double* h_value,
+                                   int16_t* h_row, int32_t* h_improvements, int64_t* h_scored);
 
 /* Self-test of the masked routing replay's division (route.cu div_by_count:
  * reciprocal-based, correctly rounded) against IEEE division on `count`

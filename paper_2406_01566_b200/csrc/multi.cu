@@ -26,11 +26,15 @@
 #include <vector>
 
 #include "engine.h"
+#include "gen.h"
 
 using namespace helio_engine;
 
 int helio_engine_argmax(helio_gpu_ctx* ctx, const double* d_values, const int32_t* d_status, int64_t B,
                         int64_t index_base, double* d_best, int64_t* d_index, cudaStream_t st);
+int helio_engine_sampled_round(helio_gpu_ctx* ctx, const int32_t* d_cur, const int32_t* d_kmax, uint64_t round_key,
+                               int64_t first, int64_t n, int max_changes, int allow_partial, int32_t* d_rows,
+                               double* d_val, int32_t* d_st, double* d_best, int64_t* d_bidx, cudaStream_t st);
 
 namespace {
 
@@ -276,3 +280,151 @@ int helio_gpu_multi_score_best_host(helio_gpu_multi* m, const int16_t* h_pl, int
 }
 
 }  // extern "C"
+
+// Sampled multi-node search (helio_gpu_sampled_search) over several devices:
+// each round's `batch` counter-drawn mutants are split into contiguous slices,
+// one per device, every device scores its slice and reduces its first
+// maximum, and the host merges them in index order — the same mutants and the
+// same tie-break as one device, so the same search path and result.
+extern "C" int helio_gpu_multi_sampled_search(helio_gpu_multi* m, const int16_t* h_seed, int allow_partial,
+                                              int32_t iterations, int64_t batch, int32_t max_changes,
+                                              uint64_t rng_seed, double* h_value, int16_t* h_row,
+                                              int32_t* h_improvements, int64_t* h_scored) {
+  if (!m) return HELIO_ERR_INVALID;
+  std::lock_guard<std::mutex> lock(m->mu);
+  if (m->N <= 0) {
+    m->err = "no cluster set";
+    return HELIO_ERR_NO_CLUSTER;
+  }
+  if (!h_seed || !h_value || !h_row || iterations < 0 || batch < 1 || max_changes < 1) {
+    m->err = "bad arguments";
+    return HELIO_ERR_INVALID;
+  }
+  const int nd = (int)m->ctx.size(), N = m->N;
+  struct Dev {
+    int32_t *cur = nullptr, *kmax = nullptr, *rows = nullptr, *st = nullptr;
+    double *val = nullptr, *best = nullptr;
+    int64_t* bidx = nullptr;
+    int64_t lo = 0, n = 0;
+    int rc = HELIO_OK;
+    double hb = 0;
+    int64_t hi = -1;
+  };
+  std::vector<Dev> dv(nd);
+  std::vector<int32_t> cur(N);
+  for (int i = 0; i < N; ++i)
+    cur[i] = (int32_t)(uint16_t)h_seed[2 * i] | (int32_t)((uint32_t)(uint16_t)h_seed[2 * i + 1] << 16);
+  int rc = HELIO_OK;
+  auto fail_m = [&](int code, const std::string& msg) {
+    m->err = msg;
+    return code;
+  };
+  for (int d = 0; d < nd && !rc; ++d) {
+    helio_gpu_ctx* c = m->ctx[d];
+    Dev& x = dv[d];
+    x.lo = batch * d / nd;
+    x.n = batch * (d + 1) / nd - x.lo;
+    if (cudaSetDevice(c->device) != cudaSuccess ||
+        cudaMalloc(&x.cur, 4 * N) != cudaSuccess || cudaMalloc(&x.kmax, 4 * N) != cudaSuccess ||
+        cudaMalloc(&x.rows, 4 * (size_t)N * std::max<int64_t>(x.n, 1)) != cudaSuccess ||
+        cudaMalloc(&x.val, 8 * std::max<int64_t>(x.n, 1)) != cudaSuccess ||
+        cudaMalloc(&x.st, 4 * std::max<int64_t>(x.n, 1)) != cudaSuccess || cudaMalloc(&x.best, 8) != cudaSuccess ||
+        cudaMalloc(&x.bidx, 8) != cudaSuccess ||
+        cudaMemcpy(x.cur, cur.data(), 4 * N, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(x.kmax, c->h_kmax.data(), 4 * N, cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = fail_m(HELIO_ERR_CUDA, "multi sampled search: allocation failed");
+  }
+  // the seed's value on device 0
+  double value = 0.0;
+  if (!rc) {
+    helio_gpu_ctx* c = m->ctx[0];
+    int32_t s0 = 0;
+    rc = helio_gpu_score(c, reinterpret_cast<const int16_t*>(dv[0].cur), 1, allow_partial, dv[0].val, dv[0].st,
+                         c->stream);
+    if (!rc && (cudaMemcpy(&value, dv[0].val, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+                cudaMemcpy(&s0, dv[0].st, 4, cudaMemcpyDeviceToHost) != cudaSuccess))
+      rc = HELIO_ERR_CUDA;
+    if (rc) m->err = helio_gpu_last_error(c);
+    if (!rc && s0 != 0) rc = fail_m(HELIO_ERR_INVALID, "seed placement fails validation");
+  }
+  double best_value = value;
+  std::vector<int32_t> keep = cur;
+  int32_t improvements = 0;
+  int64_t scored = 1;
+  for (int32_t it = 0; !rc && it < iterations; ++it) {
+    const uint64_t key = hg_key(rng_seed, (uint64_t)it);
+    std::vector<std::thread> pool;
+    for (int d = 0; d < nd; ++d) {
+      if (dv[d].n == 0) continue;
+      pool.emplace_back([&, d] {
+        helio_gpu_ctx* c = m->ctx[d];
+        Dev& x = dv[d];
+        std::lock_guard<std::recursive_mutex> ctx_lock(c->mu);
+        cudaSetDevice(c->device);
+        x.rc = helio_engine_sampled_round(c, x.cur, x.kmax, key, x.lo, x.n, max_changes, allow_partial, x.rows, x.val,
+                                          x.st, x.best, x.bidx, c->stream);
+        if (!x.rc && (cudaMemcpyAsync(&x.hb, x.best, 8, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+                      cudaMemcpyAsync(&x.hi, x.bidx, 8, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+                      cudaStreamSynchronize(c->stream) != cudaSuccess))
+          x.rc = HELIO_ERR_CUDA;
+      });
+    }
+    for (auto& t : pool) t.join();
+    double best = 0.0;
+    int64_t bi = -1;
+    int owner = -1;
+    for (int d = 0; d < nd && !rc; ++d) {  // slices in index order: strict '>' keeps the first maximum
+      if (dv[d].n == 0) continue;
+      if (dv[d].rc) {
+        rc = dv[d].rc;
+        m->err = helio_gpu_last_error(m->ctx[d]);
+        break;
+      }
+      if (dv[d].hi >= 0 && (bi < 0 || dv[d].hb > best)) {
+        best = dv[d].hb;
+        bi = dv[d].hi;
+        owner = d;
+      }
+    }
+    if (rc) break;
+    scored += batch;
+    if (bi >= 0 && best >= value) {  // equal values: a sideways move along the plateau
+      Dev& o = dv[owner];
+      cudaSetDevice(m->ctx[owner]->device);
+      if (cudaMemcpy(cur.data(), o.rows + (bi - o.lo) * N, 4 * N, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        rc = fail_m(HELIO_ERR_CUDA, "multi sampled search: row read-back failed");
+        break;
+      }
+      if (best > best_value) {
+        best_value = best;
+        ++improvements;
+        keep = cur;
+      }
+      value = best;
+      for (int d = 0; d < nd && !rc; ++d) {
+        cudaSetDevice(m->ctx[d]->device);
+        if (cudaMemcpy(dv[d].cur, cur.data(), 4 * N, cudaMemcpyHostToDevice) != cudaSuccess)
+          rc = fail_m(HELIO_ERR_CUDA, "multi sampled search: update failed");
+      }
+    }
+  }
+  for (int d = 0; d < nd; ++d) {
+    cudaSetDevice(m->ctx[d]->device);
+    cudaFree(dv[d].cur);
+    cudaFree(dv[d].kmax);
+    cudaFree(dv[d].rows);
+    cudaFree(dv[d].val);
+    cudaFree(dv[d].st);
+    cudaFree(dv[d].best);
+    cudaFree(dv[d].bidx);
+  }
+  if (rc) return rc;
+  *h_value = best_value;
+  for (int i = 0; i < N; ++i) {
+    h_row[2 * i] = (int16_t)(keep[i] & 0xffff);
+    h_row[2 * i + 1] = (int16_t)((uint32_t)keep[i] >> 16);
+  }
+  if (h_improvements) *h_improvements = improvements;
+  if (h_scored) *h_scored = scored;
+  return HELIO_OK;
+}

@@ -1079,7 +1079,30 @@ PYBIND11_MODULE(_helio, m) {
             return py::make_tuple(best, idx);
           },
           py::arg("placements_ptr"), py::arg("count"), py::arg("values_ptr"), py::arg("status_ptr"),
-          py::arg("allow_partial") = true);
+          py::arg("allow_partial") = true)
+      .def(
+          "sampled_search",
+          [](PyMulti& p, py::array_t<int16_t, py::array::c_style | py::array::forcecast> seed, bool allow_partial,
+             int32_t iterations, int64_t batch, int32_t max_changes, uint64_t rng_seed) {
+            if (seed.ndim() != 2 || seed.shape(0) != p.N || seed.shape(1) != 2)
+              throw py::value_error("seed must be int16 [num_nodes, 2]");
+            py::array_t<int16_t> row({(py::ssize_t)p.N, (py::ssize_t)2});
+            double value = 0;
+            int32_t improvements = 0;
+            int64_t scored = 0;
+            int rc;
+            {
+              py::gil_scoped_release rel;
+              rc = helio_gpu_multi_sampled_search(p.m, seed.data(), allow_partial ? 1 : 0, iterations, batch,
+                                                  max_changes, rng_seed, &value, row.mutable_data(), &improvements,
+                                                  &scored);
+            }
+            if (rc != HELIO_OK) throw InternalError(helio_gpu_multi_last_error(p.m));
+            return py::make_tuple(value, row, improvements, scored);
+          },
+          py::arg("seed"), py::arg("allow_partial") = true, py::arg("iterations") = 20,
+          py::arg("batch") = 1 << 20, py::arg("max_changes") = 3, py::arg("rng_seed") = 1,
+          "Engine.sampled_search with each round's mutants split over the devices (same result as one device).");
 
   py::class_<PyEngine>(m, "Engine")
       .def(py::init([](const ClusterSpec& c, int device) {

@@ -374,10 +374,12 @@ __global__ void copy_rows(const int32_t* __restrict__ cur, int N, int64_t B, int
     rows[q] = __ldg(cur + (q % N));
 }
 
+// Mutant b of a round is drawn from hg_key(seed, first + b): a round's
+// 'batch' mutants are one counter range, so devices can split it.
 __global__ void mutate_rows(const int32_t* __restrict__ cur, const int32_t* __restrict__ kmax, int N, int L,
-                            uint64_t seed, int64_t B, int max_changes, int32_t* __restrict__ rows) {
+                            uint64_t seed, int64_t first, int64_t B, int max_changes, int32_t* __restrict__ rows) {
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t key = hg_key(seed, (uint64_t)b);
+    const uint64_t key = hg_key(seed, (uint64_t)(first + b));
     const int c = 1 + (int)hg_uniform(hg_draw(key, 0), (uint32_t)max_changes);
     for (int j = 0; j < c; ++j) {
       const uint64_t d0 = hg_draw(key, 1 + 4 * j), d1 = hg_draw(key, 2 + 4 * j), d2 = hg_draw(key, 3 + 4 * j),
@@ -491,7 +493,7 @@ extern "C" int helio_gpu_sampled_search(helio_gpu_ctx* ctx, const int16_t* h_see
   const int grid_b = (int)std::min<int64_t>((batch + 255) / 256, 16 * ctx->sm_count);
   for (int32_t it = 0; !rc && it < iterations; ++it) {
     copy_rows<<<grid_w, 256, 0, st>>>(d_cur, N, batch, d_rows);
-    mutate_rows<<<grid_b, 256, 0, st>>>(d_cur, d_kmax, N, L, hg_key(rng_seed, (uint64_t)it), batch, max_changes,
+    mutate_rows<<<grid_b, 256, 0, st>>>(d_cur, d_kmax, N, L, hg_key(rng_seed, (uint64_t)it), 0, batch, max_changes,
                                         d_rows);
     ctx->launches += 2;
     rc = helio_gpu_score(ctx, reinterpret_cast<const int16_t*>(d_rows), batch, allow_partial, d_val, d_st, st);
@@ -530,4 +532,21 @@ extern "C" int helio_gpu_sampled_search(helio_gpu_ctx* ctx, const int16_t* h_see
   if (h_improvements) *h_improvements = improvements;
   if (h_scored) *h_scored = scored;
   return HELIO_OK;
+}
+
+// One sampled-search round on a slice [first, first + n) of the round's
+// mutants (csrc/multi.cu's multi-device search): rows = mutants of d_cur,
+// scored, and the slice's first maximum (global index) in d_best / d_bidx.
+int helio_engine_sampled_round(helio_gpu_ctx* ctx, const int32_t* d_cur, const int32_t* d_kmax, uint64_t round_key,
+                               int64_t first, int64_t n, int max_changes, int allow_partial, int32_t* d_rows,
+                               double* d_val, int32_t* d_st, double* d_best, int64_t* d_bidx, cudaStream_t st) {
+  const int N = ctx->N, L = ctx->L;
+  const int grid_w = (int)std::min<int64_t>(((int64_t)N * n + 255) / 256, 16 * ctx->sm_count);
+  const int grid_b = (int)std::min<int64_t>((n + 255) / 256, 16 * ctx->sm_count);
+  copy_rows<<<grid_w, 256, 0, st>>>(d_cur, N, n, d_rows);
+  mutate_rows<<<grid_b, 256, 0, st>>>(d_cur, d_kmax, N, L, round_key, first, n, max_changes, d_rows);
+  ctx->launches += 2;
+  int rc = helio_gpu_score(ctx, reinterpret_cast<const int16_t*>(d_rows), n, allow_partial, d_val, d_st, st);
+  if (rc) return rc;
+  return helio_gpu_argmax(ctx, d_val, d_st, n, first, d_best, d_bidx, st);
 }

@@ -61,6 +61,24 @@ def test_multi_engine_equals_one_engine(mode):
     assert it == 0 and bt == v1[1]
 
 
+def test_multi_device_sampled_search_equals_one_device():
+    """helio_gpu_multi_sampled_search splits every round's mutants over the
+    devices and merges first maxima in index order: same rounds, same moves,
+    same placement and value bits as Engine.sampled_search on one device."""
+    d = clusters.CONFIGS["het42-70b"]("float")
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    e.mode = "score"
+    devs = [0, 1] if _gpus() >= 2 else [0, 0]
+    m = h.MultiEngine(c, devs)
+    m.mode = "score"
+    placement, _ = h.heuristic_placement(c, "petals")
+    seed = h.placement_rows(c, [{k: tuple(v) for k, v in placement.items()}])[0]
+    v1, r1, i1, s1 = e.sampled_search(seed, True, 6, 1 << 16, 2, 7)
+    v2, r2, i2, s2 = m.sampled_search(seed, True, 6, 1 << 16, 2, 7)
+    assert bits([v1])[0] == bits([v2])[0] and np.array_equal(r1, r2) and (i1, s1) == (i2, s2)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
