@@ -82,6 +82,12 @@ HELIO_PLANNER_API int helio_planner_upper_bound(const void* cluster, double* out
 
 HELIO_PLANNER_API void helio_planner_free(char* p);
 
+/* sizeof (ClusterSpec, PlacementPlan, FlowGraph, Scheduler, IwrrPicker, Rng)
+ * and alignof(Scheduler) as the reference's headers lay them out, into
+ * sizes[0..n); returns how many there are.  The bindings compare them with
+ * this repo's declarations before passing objects across. */
+HELIO_PLANNER_API int helio_planner_layout(int64_t* sizes, int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

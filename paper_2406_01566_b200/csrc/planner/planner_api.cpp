@@ -10,6 +10,7 @@
 #include "../../../include/helio_planner.h"
 #include "helio/errors.hpp"
 #include "helio/placement.hpp"
+#include "helio/scheduler.hpp"
 #include "helio/sim.hpp"
 #include "json.hpp"
 
@@ -156,5 +157,14 @@ int helio_planner_upper_bound(const void* cluster, double* out, char* err, int32
 }
 
 void helio_planner_free(char* p) { delete[] p; }
+
+int helio_planner_layout(int64_t* sizes, int32_t n) {
+  const int64_t v[] = {(int64_t)sizeof(ClusterSpec), (int64_t)sizeof(PlacementPlan), (int64_t)sizeof(FlowGraph),
+                       (int64_t)sizeof(Scheduler), (int64_t)sizeof(IwrrPicker), (int64_t)sizeof(Rng),
+                       (int64_t)alignof(Scheduler)};
+  const int32_t m = (int32_t)(sizeof(v) / sizeof(v[0]));
+  for (int32_t i = 0; i < n && i < m; ++i) sizes[i] = v[i];
+  return m;
+}
 
 }  // extern "C"

@@ -377,6 +377,7 @@ struct Planner {
   decltype(&helio_planner_prune_links) prune_links = nullptr;
   decltype(&helio_planner_upper_bound) upper_bound = nullptr;
   decltype(&helio_planner_free) free = nullptr;
+  decltype(&helio_planner_layout) layout = nullptr;
 };
 
 const Planner& planner() {
@@ -400,7 +401,19 @@ const Planner& planner() {
       p.prune_links = reinterpret_cast<decltype(p.prune_links)>(dlsym(h, "helio_planner_prune_links"));
       p.upper_bound = reinterpret_cast<decltype(p.upper_bound)>(dlsym(h, "helio_planner_upper_bound"));
       p.free = reinterpret_cast<decltype(p.free)>(dlsym(h, "helio_planner_free"));
-      if (!p.plan_milp || !p.simulate || !p.prune_links || !p.upper_bound || !p.free) error = "missing symbols";
+      p.layout = reinterpret_cast<decltype(p.layout)>(dlsym(h, "helio_planner_layout"));
+      if (!p.plan_milp || !p.simulate || !p.prune_links || !p.upper_bound || !p.free || !p.layout) {
+        error = "missing symbols";
+      } else {
+        // objects cross this boundary by pointer: the reference's layouts must be ours
+        int64_t theirs[8] = {0};
+        const int64_t ours[] = {(int64_t)sizeof(ClusterSpec), (int64_t)sizeof(PlacementPlan),
+                                (int64_t)sizeof(FlowGraph), (int64_t)sizeof(Scheduler), (int64_t)sizeof(IwrrPicker),
+                                (int64_t)sizeof(Rng), (int64_t)alignof(Scheduler)};
+        const int n = p.layout(theirs, 8);
+        for (int i = 0; i < 7 && error.empty(); ++i)
+          if (n < 7 || theirs[i] != ours[i]) error = "type layouts differ from the reference's (field " + std::to_string(i) + ")";
+      }
     }
   }
   if (!error.empty())
