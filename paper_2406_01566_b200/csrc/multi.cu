@@ -341,8 +341,10 @@ extern "C" int helio_gpu_multi_sampled_search(helio_gpu_multi* m, const int16_t*
     int32_t s0 = 0;
     rc = helio_gpu_score(c, reinterpret_cast<const int16_t*>(dv[0].cur), 1, allow_partial, dv[0].val, dv[0].st,
                          c->stream);
-    if (!rc && (cudaMemcpy(&value, dv[0].val, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
-                cudaMemcpy(&s0, dv[0].st, 4, cudaMemcpyDeviceToHost) != cudaSuccess))
+    // read back on the context's (non-blocking) stream the score ran on
+    if (!rc && (cudaMemcpyAsync(&value, dv[0].val, 8, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+                cudaMemcpyAsync(&s0, dv[0].st, 4, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+                cudaStreamSynchronize(c->stream) != cudaSuccess))
       rc = HELIO_ERR_CUDA;
     if (rc) m->err = helio_gpu_last_error(c);
     if (!rc && s0 != 0) rc = fail_m(HELIO_ERR_INVALID, "seed placement fails validation");
