@@ -17,11 +17,15 @@
 // charge is released before the next admit, so the host checks that bound with
 // the largest possible running mean of output lengths.  If it may bind (or the
 // plan's exec intervals are not node-consistent) the exact replay runs instead:
-// one warp walking the device-built cycles with the state in shared memory
-// (route_masked_warp).
+// for node-consistent plans the chunked parallel replay (route_masked_spec),
+// otherwise one warp walking the device-built cycles with the state in shared
+// memory (route_masked_warp).
 #include <cub/cub.cuh>
+#include <cuda/atomic>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <cmath>
 #include <vector>
@@ -285,6 +289,503 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
   if (lane == 0) *deferred = den;
 }
 
+// ---------------------------------------------------------------------------
+// The masked replay in parallel (plans with node-consistent exec ranges).
+//
+// Requests are taken in chunks of kSpecChunk.  Inside a chunk the serial
+// coupling is (1) each vertex's picker position and (2) the running output
+// mean, which depends on which requests get deferred.  A pass routes the
+// chunk for a GUESSED set of deferrals:
+//  * warp 0 runs the division chain from the guess and publishes every
+//    request's tokens, 32 requests (a "group") at a time;
+//  * every other warp owns plan vertices and walks them group by group: a
+//    vertex may take group g once the chain and every vertex with an edge into
+//    it have finished g (a plan edge always ends at a later layer than it
+//    starts, so this is a wavefront over the plan DAG).  Inside a group the
+//    arrivals pick in request order.
+// If the deferrals found equal the guess, every token was right and the chunk
+// is the reference's.  Otherwise let f be the first request whose guess was
+// wrong: everything before f was exact (tokens and positions), so the next
+// pass guesses the deferrals found and restarts from f's group with the
+// positions and chain state saved at that group's start; f moves forward every
+// pass, and after kSpecPasses the chunk is replayed serially instead.  The
+// first pass of a chunk takes every token from the chunk-start mean (no chain:
+// the mean drifts by a fraction of a token over a chunk), which gives the
+// exact pass a guess that is almost always right.
+//
+// Picks.  Eligibility of an edge, RN(tk * len) <= thr, is monotone in tk, so
+// each edge has an exact cut-off te (the largest double passing; bisection
+// over the bit patterns) and the eligible edges of a vertex are always the c
+// edges of largest te — its "class" c, counted per arrival in parallel.  A
+// class-deg arrival takes the current slot; a masked one (0 < c < deg) takes
+// nxt[c][p], a per-vertex table of the first slot at or after p whose edge is
+// among the top c (built at launch); class 0 is deferred with the position
+// unchanged.  So a pick is one shared-memory load whatever the mask.
+constexpr int kSpecChunk = 2048, kSpecGroups = kSpecChunk / 32, kSpecThreads = 1024, kSpecPasses = 8;
+#ifndef SPEC_APPROX
+#define SPEC_APPROX 1
+#endif
+constexpr bool kSpecApprox = SPEC_APPROX;
+
+#ifndef SPEC_SYNC
+#define SPEC_SYNC 0
+#endif
+__device__ __forceinline__ int spec_acquire(int* p) {
+#if SPEC_SYNC == 2
+  return *reinterpret_cast<volatile int*>(p);
+#else
+  return cuda::atomic_ref<int, cuda::thread_scope_block>(*p).load(cuda::memory_order_acquire);
+#endif
+}
+// Spin until *p >= need.  The wavefront cannot deadlock (every wait is on a
+// vertex earlier in end-layer order, or on the chain); the bound turns a bug
+// into a launch error instead of a hung device.
+#ifndef SPEC_SLEEP
+#define SPEC_SLEEP 32
+#endif
+__device__ __forceinline__ void spec_wait(int* p, int need) {
+  // back off between polls so waiting warps leave the issue slots to the
+  // working ones
+  for (unsigned n = 0; spec_acquire(p) < need; ++n) {
+    if (SPEC_SLEEP) __nanosleep(SPEC_SLEEP);
+    if (n > (1u << 30)) __trap();
+  }
+#if SPEC_SYNC == 2
+  __threadfence_block();
+#endif
+}
+__device__ __forceinline__ void spec_release(int* p, int v) {
+#if SPEC_SYNC == 2
+  __threadfence_block();
+  *reinterpret_cast<volatile int*>(p) = v;
+#else
+  cuda::atomic_ref<int, cuda::thread_scope_block>(*p).store(v, cuda::memory_order_release);
+#endif
+}
+
+#ifdef SPEC_PROFILE
+__device__ long long spec_prof[8192];
+#define SPEC_PROF(idx) \
+  do {                 \
+    if (c0 == 3 * C) spec_prof[idx] = clock64(); \
+  } while (0)
+#else
+#define SPEC_PROF(idx) \
+  do {                 \
+  } while (0)
+#endif
+
+// One pick on a cycle [base, base + W) from relative position p (serial
+// fallback): the first eligible slot in one full cycle; returns its absolute
+// slot (p advanced past it) or -1 (p unchanged).
+__device__ __forceinline__ int spec_pick(const SlotRec* rec, int base, int W, int& p, double tk) {
+  for (int k = 0; k < W; ++k) {
+    int q = p + k;
+    q -= q >= W ? W : 0;
+    const SlotRec& r = rec[base + q];
+    if (tk * r.len <= r.thr) {
+      p = q + 1 == W ? 0 : q + 1;
+      return base + q;
+    }
+  }
+  return -1;
+}
+
+// meta = [vorder: nvo vertex ids, end-layer order, the coordinator first]
+//        [pred_beg: nvo + 1] [pred: order indices of the vertices with an edge into each]
+__global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
+    int64_t R, int nv, int L, int max_hops, double kvb, const int32_t* __restrict__ obeg,
+    const int32_t* __restrict__ odst, const int32_t* __restrict__ oes, const int32_t* __restrict__ oee,
+    const int32_t* __restrict__ node_of, const double* __restrict__ kv_cap, const int32_t* __restrict__ cyc_len,
+    const int16_t* __restrict__ cyc, int nvo, const int32_t* __restrict__ meta, int nxt_cap,
+    const int32_t* __restrict__ in_len, const int32_t* __restrict__ out_len, int32_t* nh, int32_t* hop_node,
+    int32_t* hop_s, int32_t* hop_e, long long* deferred, int* passes_out) {
+  extern __shared__ __align__(16) char sm[];
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, NW = T >> 5;
+  constexpr int C = kSpecChunk, G1 = kSpecGroups + 1;
+  const unsigned FULL = 0xffffffffu;
+  const int32_t* vorder = meta;
+  const int32_t* pred_beg = meta + nvo;
+  const int32_t* pred = meta + 2 * nvo + 1;
+  size_t o = 0;
+#define take(bytes) (sm + ((o += ((size_t)(bytes) + 15) & ~size_t(15)) - (((size_t)(bytes) + 15) & ~size_t(15))))
+  double* tk = reinterpret_cast<double*>(take(8 * C));
+  double* ytab = reinterpret_cast<double*>(take(8 * C));
+  int32_t* in_s = reinterpret_cast<int32_t*>(take(4 * C));
+  int32_t* out_s = reinterpret_cast<int32_t*>(take(4 * C));
+  int16_t* cur = reinterpret_cast<int16_t*>(take(2 * C));  // vertex the request waits at; -1 = done
+  int16_t* hcnt = reinterpret_cast<int16_t*>(take(2 * C));
+  uint8_t* dguess = reinterpret_cast<uint8_t*>(take(C));
+  uint8_t* dfound = reinterpret_cast<uint8_t*>(take(C));
+  double* a_grp = reinterpret_cast<double*>(take(8 * G1));    // chain state at each group's start
+  int32_t* adm_grp = reinterpret_cast<int32_t*>(take(4 * G1));
+  int16_t* pos_g = reinterpret_cast<int16_t*>(take(2 * (size_t)nvo * G1));  // positions at group starts
+  int32_t* front = reinterpret_cast<int32_t*>(take(4 * (nvo + 1)));         // groups done; [nvo] = chain
+  int32_t* pcur = reinterpret_cast<int32_t*>(take(4 * nvo));
+  int32_t* pos = reinterpret_cast<int32_t*>(take(4 * nv));  // committed relative positions
+  int2* vgeo = reinterpret_cast<int2*>(take(8 * nv));
+  const int ne = obeg[nv];
+  double* tes = reinterpret_cast<double*>(take(8 * (size_t)ne));      // cut-offs per vertex, descending
+  double* te_raw = reinterpret_cast<double*>(take(8 * (size_t)ne));   // cut-off of each edge
+  int16_t* erank = reinterpret_cast<int16_t*>(take(2 * (size_t)ne));  // edge's rank in its vertex
+  int32_t* noff = reinterpret_cast<int32_t*>(take(4 * (nv + 1)));     // next-slot tables per vertex
+  uint8_t* wscr = reinterpret_cast<uint8_t*>(take(32 * NW));          // per-warp classes
+  int16_t* wslot = reinterpret_cast<int16_t*>(take(64 * NW));         // per-warp picked slots
+  int16_t* nxt = reinterpret_cast<int16_t*>(take(2 * (size_t)nxt_cap));
+  int32_t* scal = reinterpret_cast<int32_t*>(take(16));
+  double* scal_d = reinterpret_cast<double*>(take(16));
+  SlotRec* rec = reinterpret_cast<SlotRec*>(take(0));
+#undef take
+  if (tid == 0) {
+    int toff = 0;
+    for (int x = 0, base = 0; x < nv; ++x) {
+      const int deg = obeg[x + 1] - obeg[x];
+      const int W = deg > 0 ? cyc_len[x] : 0;
+      vgeo[x] = make_int2(base, W);
+      pos[x] = 0;
+      base += W;
+      noff[x] = toff;
+      toff += deg > 1 ? (deg - 1) * W : 0;
+    }
+    noff[nv] = toff;
+    scal[2] = 0;  // deferrals of the chunks resolved in parallel
+  }
+  // each edge's cut-off te: the largest double t with RN(t * len) <= thr
+  // (bisection over the bit patterns of the non-negative doubles)
+  for (int e = tid; e < ne; e += T) {
+    const int d = odst[e];
+    const double thr = d == 0 ? 1.0e308 : 0.9 * kv_cap[d], len = (double)(oee[e] - oes[e]);
+    unsigned long long lo = 0, hi = 0x7ff0000000000000ull;  // P(+0) holds (thr >= 0), P(+inf) fails
+    while (hi - lo > 1) {
+      const unsigned long long mid = lo + (hi - lo) / 2;
+      if (__longlong_as_double((long long)mid) * len <= thr) lo = mid;
+      else hi = mid;
+    }
+    te_raw[e] = __longlong_as_double((long long)lo);
+  }
+  __syncthreads();
+  // ranks within each vertex by te descending (ties by edge order)
+  for (int e = tid; e < ne; e += T) {
+    int x = 0;
+    while (obeg[x + 1] <= e) ++x;
+    int r = 0;
+    for (int f = obeg[x]; f < obeg[x + 1]; ++f) r += te_raw[f] > te_raw[e] || (te_raw[f] == te_raw[e] && f < e);
+    erank[e] = (int16_t)r;
+    tes[obeg[x] + r] = te_raw[e];
+  }
+  __syncthreads();
+  if (noff[nv] > nxt_cap) __trap();  // the host sizes nxt_cap from 32 * deg >= W
+  for (int x = wid; x < nv; x += NW) {
+    const int2 geo = vgeo[x];
+    const int b = obeg[x], deg = obeg[x + 1] - b, W = geo.y;
+    for (int k = lane; k < W; k += 32) {
+      const int e = b + cyc[32 * b + k];
+      const int d = odst[e];
+      SlotRec r;
+      r.thr = d == 0 ? 1.0e308 : 0.9 * kv_cap[d];
+      r.len = (double)(oee[e] - oes[e]);
+      r.next = 0;
+      r.dst = d;
+      r.ee = oee[e];
+      r.es_node = (oes[e] & 0xffff) | (node_of[d] << 16);
+      rec[geo.x + k] = r;
+    }
+    // next-slot table of class c (the c edges of largest te eligible):
+    // nxt[c - 1][p] = first slot at or after p (cyclically) whose edge has rank < c
+    for (int c = 1 + lane; c < deg; c += 32) {
+      int16_t* t = nxt + noff[x] + (c - 1) * W;
+      int last = -1;
+      for (int q2 = 2 * W - 1; q2 >= 0; --q2) {
+        const int q = q2 < W ? q2 : q2 - W;
+        if (erank[b + cyc[32 * b + q]] < c) last = q;
+        if (q2 < W) t[q] = (int16_t)last;
+      }
+    }
+  }
+  __syncthreads();
+  double avg = 232.0, samples = 1.0;  // thread 0: the committed running mean
+  long long den = 0;
+  int passes_total = 0;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < R; c0 += C) {
+    const int cn = R - c0 < C ? (int)(R - c0) : C;
+    const int G = (cn + 31) >> 5;
+    if (tid == 0) SPEC_PROF(0);
+    for (int i = tid; i < cn; i += T) {
+      in_s[i] = in_len[c0 + i];
+      out_s[i] = out_len[c0 + i];
+      dguess[i] = 0;
+    }
+    if (tid == 0) {
+      a_grp[0] = avg;
+      adm_grp[0] = 0;
+      scal_d[0] = samples;
+      scal[0] = 0;  // g0
+    }
+    for (int k = tid; k < nvo; k += T) pos_g[k * G1] = (int16_t)pos[vorder[k]];
+    __syncthreads();
+    const double samples0 = scal_d[0];
+    for (int i = tid; i < cn; i += T) ytab[i] = __drcp_rn(samples0 + 1.0 + i);
+    bool converged = false;
+    __syncthreads();
+    if (tid == 0) SPEC_PROF(1);
+    for (int pass = 0; pass < kSpecPasses && !converged; ++pass) {
+      const int g0 = scal[0];
+      const bool approx = kSpecApprox && pass == 0;
+      for (int i = (g0 << 5) + tid; i < cn; i += T) {
+        cur[i] = 0;
+        hcnt[i] = 0;
+        dfound[i] = 0;
+      }
+      for (int k = tid; k < nvo; k += T) {
+        front[k] = g0;
+        pcur[k] = pos_g[k * G1 + g0];
+      }
+      if (tid == 0) {
+        front[nvo] = g0;
+        scal[1] = 0x7fffffff;  // first mismatch
+      }
+      __syncthreads();
+      if (wid == 0) {
+        const unsigned lt = (1u << lane) - 1u;
+        double a = a_grp[g0];
+        int adm = adm_grp[g0];
+        if (approx) {  // pass 0: every token from the chunk-start mean, no chain
+          for (int i = lane; i < cn; i += 32) tk[i] = ((double)in_s[i] + a) * kvb;
+          __syncwarp();
+          if (lane == 0) spec_release(&front[nvo], G);
+        } else {
+          // the division chain over the guessed admissions, 32 requests at a
+          // time: each lane loads its request's operands and reciprocal, the
+          // chain runs on shuffled registers (only the 5 dependent FP64 ops
+          // per admission are serial)
+          for (int g = g0; g < G; ++g) {
+            const int i = (g << 5) + lane;
+            const bool valid = i < cn;
+            const bool ad = valid && !dguess[i];
+            const unsigned am = __ballot_sync(FULL, ad);
+            const double my_out = valid ? (double)out_s[i] : 0.0;
+            const double my_in = valid ? (double)in_s[i] : 0.0;
+            const int r = adm + __popc(am & lt);
+            const double my_y = ad ? ytab[r] : 1.0;
+            const double my_n = samples0 + 1.0 + r;
+            double my_a = a;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const double o = __shfl_sync(FULL, my_out, j);
+              const double y = __shfl_sync(FULL, my_y, j);
+              const double n = __shfl_sync(FULL, my_n, j);
+              if (lane == j) my_a = a;
+              if ((am >> j) & 1u) a += div_by_count(o - a, n, y);
+            }
+            if (valid) tk[i] = (my_in + my_a) * kvb;
+            adm += __popc(am);
+            __syncwarp();
+            if (lane == 0) {
+              if (pass < 4) SPEC_PROF(64 + pass * 1024 + 15 * 64 + g);
+              a_grp[g + 1] = a;
+              adm_grp[g + 1] = adm;
+              spec_release(&front[nvo], g + 1);
+            }
+          }
+        }
+      } else {
+        for (int g = g0; g < G; ++g) {
+          for (int k = wid - 1; k < nvo; k += NW - 1) {
+            const int v = vorder[k];
+            const int need = g + 1;
+#ifdef SPEC_ISOLATE
+            if (k != 0) continue;  // timing experiment only: results are wrong
+#endif
+            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 0);
+            spec_wait(&front[nvo], need);
+            for (int j = pred_beg[k]; j < pred_beg[k + 1]; ++j) spec_wait(&front[pred[j]], need);
+            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 1);
+            int p = pcur[k];
+            if (lane == 0) pos_g[k * G1 + g] = (int16_t)p;
+            const int i = (g << 5) + lane;
+            int hop_h = -1, hop_es_node = 0, hop_ee = 0;
+            const bool arr = i < cn && cur[i] == v;
+            const unsigned am = __ballot_sync(FULL, arr);
+            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 2);
+            if (am) {
+              const int2 geo = vgeo[v];
+              const int base = geo.x, W = geo.y;
+              const int eb = obeg[v], deg = obeg[v + 1] - eb;
+              int slot = -1;
+                if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 6);
+              if (W > 0) {
+                // class: how many of the vertex's edges are eligible (a
+                // prefix of the te-descending order)
+                int c = 0;
+                if (arr) {
+                  const double t = tk[i];
+                  for (int j = 0; j < deg; ++j) c += t <= tes[eb + j];
+                }
+                if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 7);
+                const unsigned fm = __ballot_sync(FULL, arr && c == deg);
+                if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 8);
+                const unsigned lt = (1u << lane) - 1u;
+                if (fm == am) {  // every arrival takes the next slot
+                  const int r = p + __popc(am & lt);
+                  slot = r < W ? r : r % W;
+                  const int n = p + __popc(am);
+                  p = n < W ? n : n % W;
+                } else {
+                  if (arr) wscr[wid * 32 + lane] = (uint8_t)c;
+                  __syncwarp();
+                if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 9);
+                  if (lane == 0) {  // the picks in request order: one table load per masked arrival
+                    const int16_t* tb = nxt + noff[v] - W;
+                    unsigned rest = am;
+                    while (rest) {
+                      const int j = __ffs(rest) - 1;
+                      rest &= rest - 1u;
+                      const int cj = wscr[wid * 32 + j];
+                      int sl;
+                      if (cj == deg) {
+                        sl = p;
+                      } else if (cj == 0) {
+                        wslot[wid * 32 + j] = -1;  // nothing eligible: deferred, position unchanged
+                        continue;
+                      } else {
+                        sl = tb[cj * W + p];
+                      }
+                      wslot[wid * 32 + j] = (int16_t)sl;
+                      p = sl + 1 == W ? 0 : sl + 1;
+                    }
+                  }
+                  __syncwarp();
+                  if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 3);
+                  p = __shfl_sync(FULL, p, 0);
+                  if (arr) slot = wslot[wid * 32 + lane];
+                }
+              }
+              if (arr) {
+                if (slot < 0) {
+                  dfound[i] = 1;
+                  cur[i] = -1;
+                } else {
+                  const SlotRec& rc = rec[base + slot];
+                  hop_h = hcnt[i];
+                  hop_es_node = rc.es_node;
+                  hop_ee = rc.ee;
+                  hcnt[i] = (int16_t)(hop_h + 1);
+                  cur[i] = (int16_t)(rc.ee >= L ? -1 : rc.dst);
+                }
+              }
+            }
+            if (lane == 0 && pass < 4 && k < 15) SPEC_PROF(64 + pass * 1024 + k * 64 + g);
+            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 4);
+            if (lane == 0) pcur[k] = p;
+#if SPEC_SYNC == 0
+            __threadfence_block();
+            __syncwarp();
+            if (lane == 0) spec_release(&front[k], need);
+#elif SPEC_SYNC == 1
+            __syncwarp();
+            if (lane == 0) spec_release(&front[k], need);
+#else
+            __syncwarp();
+            if (lane == 0) {
+              __threadfence_block();
+              *reinterpret_cast<volatile int*>(&front[k]) = need;
+            }
+#endif
+            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 5);
+            // the hops go to HBM after the release: no consumer reads them
+            if (hop_h >= 0 && hop_h < max_hops) {
+              const int64_t at = (c0 + i) * max_hops + hop_h;
+              hop_node[at] = hop_es_node >> 16;
+              if (hop_s) {
+                hop_s[at] = hop_es_node & 0xffff;
+                hop_e[at] = hop_ee;
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && pass < 4) SPEC_PROF(2 + 2 * pass);
+      for (int i = (g0 << 5) + tid; i < cn; i += T)
+        if (dfound[i] != dguess[i]) atomicMin(&scal[1], i);
+      __syncthreads();
+      if (tid == 0 && pass < 4) SPEC_PROF(3 + 2 * pass);
+      const int f = approx ? 0 : scal[1];
+      if (approx) {  // the deferrals found become the first guess
+        for (int i = tid; i < cn; i += T) dguess[i] = dfound[i];
+        if (tid == 0) scal[0] = 0;
+      } else if (f == 0x7fffffff) {
+        converged = true;
+      } else {
+        for (int i = f + tid; i < cn; i += T) dguess[i] = dfound[i];
+        if (tid == 0) scal[0] = f >> 5;
+      }
+      ++passes_total;
+      __syncthreads();
+    }
+    if (converged) {
+      int local = 0;
+      for (int i = tid; i < cn; i += T) {
+        nh[c0 + i] = dfound[i] ? -1 : hcnt[i];
+        local += dfound[i];
+      }
+      for (int k = tid; k < nvo; k += T) pos[vorder[k]] = pcur[k];
+      for (int d = 16; d; d >>= 1) local += __shfl_xor_sync(FULL, local, d);
+      if (lane == 0) atomicAdd(&scal[2], local);
+      if (tid == 0) {
+        avg = a_grp[G];
+        samples = samples0 + adm_grp[G];
+      }
+    } else if (tid == 0) {
+      // serial replay of the chunk from the committed state
+      for (int i = 0; i < cn; ++i) {
+        const double tki = ((double)in_s[i] + avg) * kvb;
+        int v = 0, covered = 0, h = 0;
+        bool ok = true;
+        while (covered < L) {
+          const int2 geo = vgeo[v];
+          if (geo.y == 0) {
+            ok = false;
+            break;
+          }
+          int p = pos[v];
+          const int s2 = spec_pick(rec, geo.x, geo.y, p, tki);
+          if (s2 < 0) {
+            ok = false;
+            break;
+          }
+          pos[v] = p;
+          const SlotRec& r = rec[s2];
+          if (max_hops > 0 && h < max_hops) {
+            const int64_t at = (c0 + i) * max_hops + h;
+            hop_node[at] = r.es_node >> 16;
+            if (hop_s) {
+              hop_s[at] = r.es_node & 0xffff;
+              hop_e[at] = r.ee;
+            }
+          }
+          ++h;
+          covered = r.ee;
+          v = r.dst;
+        }
+        if (ok) {
+          samples += 1.0;
+          avg += ((double)out_s[i] - avg) / samples;
+        } else {
+          ++den;
+        }
+        nh[c0 + i] = ok ? h : -1;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *deferred = den + scal[2];
+    if (passes_out) *passes_out = passes_total;
+  }
+}
+
 // Self-test of div_by_count against IEEE division on the routing domain:
 // numerators a = out - avg (|a| < 4096, random significands), denominators
 // n = sample counts up to 2^27.
@@ -423,6 +924,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   long long *d_w = nullptr, *d_wmax = nullptr, *d_den = nullptr;
   int16_t *d_cyc = nullptr, *d_cov = nullptr;
   int* d_err = nullptr;
+  int32_t *d_vord = nullptr, *d_passes = nullptr;
   void* d_tmp = nullptr;
   size_t tmp_bytes = 0;
   const size_t HR = (size_t)R * std::max(max_hops, 1);
@@ -459,6 +961,8 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
     TRY(ar.take(&d_he, want_se ? HR : 1));
     TRY(ar.take(&d_err, 1));
     TRY(ar.take(&d_den, 1));
+    TRY(ar.take(&d_vord, 2 * nv + 1 + ne));
+    TRY(ar.take(&d_passes, 1));
     if (closed_path) {
       TRY(ar.take(&d_cur, R));
       TRY(ar.take(&d_cov, R));
@@ -528,8 +1032,9 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
       // read the actual cycle lengths back
       int64_t slots = cyc_off[nv];
       const size_t head = ((((size_t)4 * nv + 7) & ~size_t(7)) + 8 * (size_t)nv + 15) & ~size_t(15);
-      if (head + (size_t)slots * sizeof(SlotRec) > 227 * 1024) {
-        std::vector<int32_t> cl(nv);
+      std::vector<int32_t> cl;
+      if (consistent || head + (size_t)slots * sizeof(SlotRec) > 227 * 1024) {
+        cl.resize(nv);
         if (cudaMemcpyAsync(cl.data(), d_cyclen, 4 * nv, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
             cudaStreamSynchronize(st) != cudaSuccess)
           rc = fail(ctx, HELIO_ERR_CUDA, "route: cycle lengths read-back failed");
@@ -541,12 +1046,89 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
       } else if (smem > 227 * 1024 || slots > 32767) {
         rc = fail(ctx, HELIO_ERR_TOO_LARGE, "plan too large for the masked routing kernel's shared memory");
       } else {
+        // node-consistent plans: the chunked parallel replay (route_masked_spec)
+        // vertices routed from (the coordinator, then every vertex ending
+        // before L) in end-layer order, and each one's predecessors
+        std::vector<int32_t> vo, kof(nv, -1), meta;
+        for (int x = 0; x < nv; ++x)
+          if (x == 0 || vend[x] < L) vo.push_back(x);
+        std::stable_sort(vo.begin(), vo.end(), [&](int a, int b) { return vend[a] < vend[b]; });
+        const int nvo = (int)vo.size();
+        for (int k = 0; k < nvo; ++k) kof[vo[k]] = k;
+        std::vector<std::vector<int32_t>> preds(nvo);
+        for (int x = 0; x < nv; ++x)
+          for (int p = obeg[x]; p < obeg[x + 1]; ++p)
+            if (kof[x] >= 0 && odst[p] != 0 && kof[odst[p]] >= 0) preds[kof[odst[p]]].push_back(kof[x]);
+        meta = vo;
+        meta.push_back(0);
+        for (int k = 0; k < nvo; ++k) {
+          std::sort(preds[k].begin(), preds[k].end());
+          preds[k].erase(std::unique(preds[k].begin(), preds[k].end()), preds[k].end());
+          meta.push_back(meta[nvo + k] + (int32_t)preds[k].size());
+        }
+        for (int k = 0; k < nvo; ++k) meta.insert(meta.end(), preds[k].begin(), preds[k].end());
+        constexpr int G1 = kSpecGroups + 1;
+        auto a16 = [](size_t b) { return (b + 15) & ~size_t(15); };
+        int64_t nxt_cap = 0;  // next-slot tables: (deg - 1) * W per vertex
+        for (int x = 0; x < nv && !cl.empty(); ++x) {
+          const int deg = obeg[x + 1] - obeg[x];
+          if (deg > 1) nxt_cap += (int64_t)(deg - 1) * cl[x];
+        }
+        const int NW = kSpecThreads / 32;
+        const size_t spec_smem = 2 * a16(8 * kSpecChunk) + 2 * a16(4 * kSpecChunk) + 2 * a16(2 * kSpecChunk) +
+                                 2 * a16(kSpecChunk) + a16(8 * G1) + a16(4 * G1) + a16(2 * (size_t)nvo * G1) +
+                                 a16(4 * (nvo + 1)) + a16(4 * nvo) + a16(4 * nv) + a16(8 * nv) +
+                                 2 * a16(8 * (size_t)ne) + a16(2 * (size_t)ne) + a16(4 * (nv + 1)) + a16(32 * NW) +
+                                 a16(64 * NW) + a16(2 * (size_t)nxt_cap) + 32 + (size_t)slots * sizeof(SlotRec);
+        const char* sp_env = getenv("HELIO_ROUTE_SPEC");
+        const bool use_spec = consistent && !cl.empty() && spec_smem <= 227 * 1024 &&
+                              (int)meta.size() <= nv + nv + 1 + ne && !(sp_env && sp_env[0] == '0');
+        if (use_spec) {
+          if (cudaMemcpyAsync(d_vord, meta.data(), 4 * meta.size(), cudaMemcpyHostToDevice, st) != cudaSuccess)
+            rc = fail(ctx, HELIO_ERR_CUDA, "route H2D failed");
+          cudaFuncSetAttribute(route_masked_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spec_smem);
+          const bool diag = getenv("HELIO_ROUTE_DIAG") != nullptr;
+          cudaEvent_t e0 = nullptr, e1 = nullptr;
+          if (diag) {
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0, st);
+          }
+          if (!rc)
+            route_masked_spec<<<1, kSpecThreads, spec_smem, st>>>(
+                R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst, d_oes, d_oee, d_node, d_kvcap,
+                d_cyclen, d_cyc, nvo, d_vord, (int)nxt_cap, d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr,
+                want_se ? d_he : nullptr, d_den, d_passes);
+          ctx->launches++;
+          if (diag) {  // kernel time and passes (tools/route_spec_probe.py)
+            int passes = 0;
+            float ms = 0.f;
+            cudaEventRecord(e1, st);
+            cudaMemcpyAsync(&passes, d_passes, 4, cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            cudaEventElapsedTime(&ms, e0, e1);
+            fprintf(stderr, "route_masked_spec: %lld requests, %d chunk passes, %.3f ms\n", (long long)R, passes, ms);
+#ifdef SPEC_PROFILE
+            {
+              std::vector<long long> pr(8192);
+              cudaMemcpyFromSymbol(pr.data(), spec_prof, 8 * 8192);
+              fprintf(stderr, "SPECPROF nvo=%d", nvo);
+              for (int q = 0; q < 8192; ++q) fprintf(stderr, " %lld", pr[q]);
+              fprintf(stderr, "\n");
+            }
+#endif
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+          }
+        } else {
         auto kern = nv <= 32 ? (consistent ? route_masked_warp<true, false> : route_masked_warp<true, true>)
                              : (consistent ? route_masked_warp<false, false> : route_masked_warp<false, true>);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<1, 32, smem, st>>>(R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst, d_oes, d_oee, d_node,
                                   d_kvcap, d_cyclen, d_cyc, d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr,
                                   want_se ? d_he : nullptr, d_den, d_err);
+        ctx->launches++;
+        }
       }
       if (cudaGetLastError() != cudaSuccess) rc = fail(ctx, HELIO_ERR_CUDA, "route_masked_warp failed");
     }
