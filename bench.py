@@ -351,7 +351,7 @@ def routing_leg(h, clusters, dev, sp, requests, with_reference):
     except Exception as ex:  # reported, never fatal
         out["stateful"] = {"error": str(ex)}
     # KV masking binds: the same plan with kv_bytes_per_token_layer = 1 MB
-    # (~40% of admissions deferred) takes the exact replay kernel
+    # (3% of admissions deferred on this plan) takes the exact replay kernel
     try:
         dm = json.loads(json.dumps(d))
         dm["model"]["kv_bytes_per_token_layer"] = 1e6
@@ -364,7 +364,8 @@ def routing_leg(h, clusters, dev, sp, requests, with_reference):
             mnh, mhn, _, _, mden = em.route(row, pe, pf, inl, outl, 0, False)
             mt.append(time.perf_counter() - t0)
         out["masked"] = {"value": requests / min(mt), "unit": "routes/s", "deferred": int(mden),
-                         "kernel": "route_masked_warp (exact AC8 replay, one warp, state in shared memory)",
+                         "kernel": "route_masked_spec (exact AC8 replay: chunked speculation on the deferral set, "
+                                   "wavefront over the plan DAG, one CTA)",
                          "workload": "same plan and requests, kv_bytes_per_token_layer = 1e6"}
     except Exception as ex:  # reported, never fatal
         out["masked"] = {"error": str(ex)}

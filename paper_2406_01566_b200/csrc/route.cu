@@ -21,7 +21,6 @@
 // otherwise one warp walking the device-built cycles with the state in shared
 // memory (route_masked_warp).
 #include <cub/cub.cuh>
-#include <cuda/atomic>
 
 #include <algorithm>
 #include <cstdio>
@@ -322,45 +321,36 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
 // among the top c (built at launch); class 0 is deferred with the position
 // unchanged.  So a pick is one shared-memory load whatever the mask.
 constexpr int kSpecChunk = 2048, kSpecGroups = kSpecChunk / 32, kSpecThreads = 1024, kSpecPasses = 8;
-#ifndef SPEC_APPROX
-#define SPEC_APPROX 1
-#endif
-constexpr bool kSpecApprox = SPEC_APPROX;
 
-#ifndef SPEC_SYNC
-#define SPEC_SYNC 0
-#endif
-__device__ __forceinline__ int spec_acquire(int* p) {
-#if SPEC_SYNC == 2
-  return *reinterpret_cast<volatile int*>(p);
-#else
-  return cuda::atomic_ref<int, cuda::thread_scope_block>(*p).load(cuda::memory_order_acquire);
-#endif
+// Frontier flags live in shared memory: relaxed CTA-scope loads/stores on
+// the shared window (plain LDS/STS) ordered by acq_rel fences — the fence
+// pattern of the PTX memory model, without the generic-address strong loads
+// cuda::atomic_ref compiles to.
+__device__ __forceinline__ int spec_load(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
 }
+__device__ __forceinline__ void spec_fence() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
 // Spin until *p >= need.  The wavefront cannot deadlock (every wait is on a
 // vertex earlier in end-layer order, or on the chain); the bound turns a bug
 // into a launch error instead of a hung device.
 #ifndef SPEC_SLEEP
 #define SPEC_SLEEP 32
 #endif
-__device__ __forceinline__ void spec_wait(int* p, int need) {
-  // back off between polls so waiting warps leave the issue slots to the
-  // working ones
-  for (unsigned n = 0; spec_acquire(p) < need; ++n) {
-    if (SPEC_SLEEP) __nanosleep(SPEC_SLEEP);
+// (the caller fences once after its waits)
+template <bool SLEEP = true>
+__device__ __forceinline__ void spec_wait(const int* p, int need) {
+  // vertex warps back off between polls so waiting warps leave the issue
+  // slots to the working ones; the chain polls tightly
+  for (unsigned n = 0; spec_load(p) < need; ++n) {
+    if (SLEEP && SPEC_SLEEP) __nanosleep(SPEC_SLEEP);
     if (n > (1u << 30)) __trap();
   }
-#if SPEC_SYNC == 2
-  __threadfence_block();
-#endif
 }
 __device__ __forceinline__ void spec_release(int* p, int v) {
-#if SPEC_SYNC == 2
-  __threadfence_block();
-  *reinterpret_cast<volatile int*>(p) = v;
-#else
-  cuda::atomic_ref<int, cuda::thread_scope_block>(*p).store(v, cuda::memory_order_release);
-#endif
+  spec_fence();
+  asm volatile("st.relaxed.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
 }
 
 #ifdef SPEC_PROFILE
@@ -397,7 +387,7 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
     int64_t R, int nv, int L, int max_hops, double kvb, const int32_t* __restrict__ obeg,
     const int32_t* __restrict__ odst, const int32_t* __restrict__ oes, const int32_t* __restrict__ oee,
     const int32_t* __restrict__ node_of, const double* __restrict__ kv_cap, const int32_t* __restrict__ cyc_len,
-    const int16_t* __restrict__ cyc, int nvo, const int32_t* __restrict__ meta, int nxt_cap,
+    const int16_t* __restrict__ cyc, int nvo, const int32_t* __restrict__ meta, int nxt_cap, int hmax,
     const int32_t* __restrict__ in_len, const int32_t* __restrict__ out_len, int32_t* nh, int32_t* hop_node,
     int32_t* hop_s, int32_t* hop_e, long long* deferred, int* passes_out) {
   extern __shared__ __align__(16) char sm[];
@@ -410,6 +400,8 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
   size_t o = 0;
 #define take(bytes) (sm + ((o += ((size_t)(bytes) + 15) & ~size_t(15)) - (((size_t)(bytes) + 15) & ~size_t(15))))
   double* tk = reinterpret_cast<double*>(take(8 * C));
+  double* tk_exact = reinterpret_cast<double*>(take(8 * C));
+  uint8_t* route_v = reinterpret_cast<uint8_t*>(take((size_t)C * hmax));  // approximate pass: vertices visited
   double* ytab = reinterpret_cast<double*>(take(8 * C));
   int32_t* in_s = reinterpret_cast<int32_t*>(take(4 * C));
   int32_t* out_s = reinterpret_cast<int32_t*>(take(4 * C));
@@ -429,9 +421,9 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
   double* te_raw = reinterpret_cast<double*>(take(8 * (size_t)ne));   // cut-off of each edge
   int16_t* erank = reinterpret_cast<int16_t*>(take(2 * (size_t)ne));  // edge's rank in its vertex
   int32_t* noff = reinterpret_cast<int32_t*>(take(4 * (nv + 1)));     // next-slot tables per vertex
-  uint8_t* wscr = reinterpret_cast<uint8_t*>(take(32 * NW));          // per-warp classes
-  int16_t* wslot = reinterpret_cast<int16_t*>(take(64 * NW));         // per-warp picked slots
   int16_t* nxt = reinterpret_cast<int16_t*>(take(2 * (size_t)nxt_cap));
+  int32_t* wcls = reinterpret_cast<int32_t*>(take(4 * 32 * NW));  // per warp: class * W of each arrival
+  double2* chain_ops = reinterpret_cast<double2*>(take(16 * 32));
   int32_t* scal = reinterpret_cast<int32_t*>(take(16));
   double* scal_d = reinterpret_cast<double*>(take(16));
   SlotRec* rec = reinterpret_cast<SlotRec*>(take(0));
@@ -445,7 +437,7 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
       pos[x] = 0;
       base += W;
       noff[x] = toff;
-      toff += deg > 1 ? (deg - 1) * W : 0;
+      toff += (deg + 1) * W;
     }
     noff[nv] = toff;
     scal[2] = 0;  // deferrals of the chunks resolved in parallel
@@ -490,15 +482,16 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
       r.es_node = (oes[e] & 0xffff) | (node_of[d] << 16);
       rec[geo.x + k] = r;
     }
-    // next-slot table of class c (the c edges of largest te eligible):
-    // nxt[c - 1][p] = first slot at or after p (cyclically) whose edge has rank < c
-    for (int c = 1 + lane; c < deg; c += 32) {
-      int16_t* t = nxt + noff[x] + (c - 1) * W;
+    // position table of class c (the c edges of largest te eligible), c = 0..deg:
+    // nxt[c][p] = the position after the first slot at or after p (cyclically)
+    // whose edge has rank < c; class 0 picks nothing (position unchanged)
+    for (int c = lane; c <= deg; c += 32) {
+      int16_t* t = nxt + noff[x] + c * W;
       int last = -1;
       for (int q2 = 2 * W - 1; q2 >= 0; --q2) {
         const int q = q2 < W ? q2 : q2 - W;
         if (erank[b + cyc[32 * b + q]] < c) last = q;
-        if (q2 < W) t[q] = (int16_t)last;
+        if (q2 < W) t[q] = (int16_t)(c == 0 ? q : (last + 1 == W ? 0 : last + 1));
       }
     }
   }
@@ -531,7 +524,7 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
     if (tid == 0) SPEC_PROF(1);
     for (int pass = 0; pass < kSpecPasses && !converged; ++pass) {
       const int g0 = scal[0];
-      const bool approx = kSpecApprox && pass == 0;
+      const bool approx = hmax > 0 && pass == 0;
       for (int i = (g0 << 5) + tid; i < cn; i += T) {
         cur[i] = 0;
         hcnt[i] = 0;
@@ -550,115 +543,111 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
         const unsigned lt = (1u << lane) - 1u;
         double a = a_grp[g0];
         int adm = adm_grp[g0];
-        if (approx) {  // pass 0: every token from the chunk-start mean, no chain
+        if (approx) {  // pass 0: every token from the chunk-start mean
           for (int i = lane; i < cn; i += 32) tk[i] = ((double)in_s[i] + a) * kvb;
           __syncwarp();
           if (lane == 0) spec_release(&front[nvo], G);
-        } else {
-          // the division chain over the guessed admissions, 32 requests at a
-          // time: each lane loads its request's operands and reciprocal, the
-          // chain runs on shuffled registers (only the 5 dependent FP64 ops
-          // per admission are serial)
-          for (int g = g0; g < G; ++g) {
-            const int i = (g << 5) + lane;
-            const bool valid = i < cn;
-            const bool ad = valid && !dguess[i];
-            const unsigned am = __ballot_sync(FULL, ad);
-            const double my_out = valid ? (double)out_s[i] : 0.0;
-            const double my_in = valid ? (double)in_s[i] : 0.0;
-            const int r = adm + __popc(am & lt);
-            const double my_y = ad ? ytab[r] : 1.0;
-            const double my_n = samples0 + 1.0 + r;
-            double my_a = a;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const double o = __shfl_sync(FULL, my_out, j);
-              const double y = __shfl_sync(FULL, my_y, j);
-              const double n = __shfl_sync(FULL, my_n, j);
-              if (lane == j) my_a = a;
-              if ((am >> j) & 1u) a += div_by_count(o - a, n, y);
-            }
-            if (valid) tk[i] = (my_in + my_a) * kvb;
-            adm += __popc(am);
-            __syncwarp();
-            if (lane == 0) {
-              if (pass < 4) SPEC_PROF(64 + pass * 1024 + 15 * 64 + g);
-              a_grp[g + 1] = a;
-              adm_grp[g + 1] = adm;
-              spec_release(&front[nvo], g + 1);
-            }
+        }
+        // the division chain over the admissions, 32 requests at a time.  An
+        // exact pass takes the guessed deferrals and publishes its tokens for
+        // the vertex warps; the approximate pass runs it right behind the
+        // routing on the deferrals found (every vertex done with the group),
+        // into tk_exact for the verification
+        const uint8_t* dsrc = approx ? dfound : dguess;
+        double* tout = approx ? tk_exact : tk;
+        for (int g = g0; g < G; ++g) {
+          if (approx) {  // the deepest vertices finish a group last
+            for (int k = nvo - 1; k >= 0; --k) spec_wait<false>(&front[k], g + 1);
+            spec_fence();
+          }
+          const int i0 = g << 5, i = i0 + lane;
+          const bool valid = i < cn;
+          const bool ad = valid && !dsrc[i];
+          const unsigned am = __ballot_sync(FULL, ad);
+          const double my_in = valid ? (double)in_s[i] : 0.0;
+          // the group's admissions packed in order: (out, 1/n) per step,
+          // so the loop below is only the 5 dependent FP64 ops per step
+          const int rk = __popc(am & lt), m = __popc(am);
+          if (ad) chain_ops[rk] = make_double2((double)out_s[i], ytab[adm + rk]);
+          __syncwarp();
+          double my_a = a;  // the mean before request i: after its rk admitted predecessors
+#pragma unroll 4
+          for (int k2 = 0; k2 < m; ++k2) {
+            const double2 oy = chain_ops[k2];
+            a += div_by_count(oy.x - a, samples0 + 1.0 + (adm + k2), oy.y);
+            if (k2 + 1 == rk) my_a = a;
+          }
+          __syncwarp();
+          if (valid) tout[i] = (my_in + my_a) * kvb;
+          adm += m;
+          __syncwarp();
+          if (lane == 0) {
+            if (pass < 2) SPEC_PROF(64 + pass * 2048 + 31 * 64 + g);
+            a_grp[g + 1] = a;
+            adm_grp[g + 1] = adm;
+            if (!approx) spec_release(&front[nvo], g + 1);
           }
         }
       } else {
-        for (int g = g0; g < G; ++g) {
-          for (int k = wid - 1; k < nvo; k += NW - 1) {
-            const int v = vorder[k];
+        // vertex warps: each owns vorder[k] for k = wid - 1 (mod NW - 1) and
+        // walks its groups in order (deadlock-free: every wait is on a vertex
+        // earlier in end-layer order, or on the chain)
+        for (int k = wid - 1; k < nvo; k += NW - 1) {
+          const int v = vorder[k];
+          const int2 geo = vgeo[v];
+          const int base = geo.x, W = geo.y;
+          const int eb = obeg[v], deg = obeg[v + 1] - eb;
+          const int pb = pred_beg[k], pe = pred_beg[k + 1];
+          const int16_t* tb = nxt + noff[v];
+          int32_t* wc = wcls + (wid << 5);
+          const unsigned lt = (1u << lane) - 1u;
+          int p = pcur[k];
+          for (int g = g0; g < G; ++g) {
             const int need = g + 1;
-#ifdef SPEC_ISOLATE
-            if (k != 0) continue;  // timing experiment only: results are wrong
-#endif
-            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 0);
             spec_wait(&front[nvo], need);
-            for (int j = pred_beg[k]; j < pred_beg[k + 1]; ++j) spec_wait(&front[pred[j]], need);
-            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 1);
-            int p = pcur[k];
+            for (int j = pb; j < pe; ++j) spec_wait(&front[pred[j]], need);
+            spec_fence();
             if (lane == 0) pos_g[k * G1 + g] = (int16_t)p;
             const int i = (g << 5) + lane;
             int hop_h = -1, hop_es_node = 0, hop_ee = 0;
             const bool arr = i < cn && cur[i] == v;
             const unsigned am = __ballot_sync(FULL, arr);
-            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 2);
             if (am) {
-              const int2 geo = vgeo[v];
-              const int base = geo.x, W = geo.y;
-              const int eb = obeg[v], deg = obeg[v + 1] - eb;
               int slot = -1;
-                if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 6);
+              if (approx && arr) {  // the route, for the verification
+                const int h = hcnt[i];
+                if (h < hmax) route_v[i * hmax + h] = (uint8_t)v;
+              }
               if (W > 0) {
                 // class: how many of the vertex's edges are eligible (a
                 // prefix of the te-descending order)
                 int c = 0;
                 if (arr) {
                   const double t = tk[i];
+#pragma unroll 4
                   for (int j = 0; j < deg; ++j) c += t <= tes[eb + j];
                 }
-                if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 7);
                 const unsigned fm = __ballot_sync(FULL, arr && c == deg);
-                if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 8);
-                const unsigned lt = (1u << lane) - 1u;
                 if (fm == am) {  // every arrival takes the next slot
                   const int r = p + __popc(am & lt);
                   slot = r < W ? r : r % W;
                   const int n = p + __popc(am);
                   p = n < W ? n : n % W;
                 } else {
-                  if (arr) wscr[wid * 32 + lane] = (uint8_t)c;
+                  // the picks in request order: one table load per arrival on
+                  // the serial path (p -> nxt[c][p]); the whole warp walks it
+                  // in lockstep, the class offsets come from shared memory
+                  const int rank = __popc(am & lt), m = __popc(am);
+                  if (arr) wc[rank] = c * W;
                   __syncwarp();
-                if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 9);
-                  if (lane == 0) {  // the picks in request order: one table load per masked arrival
-                    const int16_t* tb = nxt + noff[v] - W;
-                    unsigned rest = am;
-                    while (rest) {
-                      const int j = __ffs(rest) - 1;
-                      rest &= rest - 1u;
-                      const int cj = wscr[wid * 32 + j];
-                      int sl;
-                      if (cj == deg) {
-                        sl = p;
-                      } else if (cj == 0) {
-                        wslot[wid * 32 + j] = -1;  // nothing eligible: deferred, position unchanged
-                        continue;
-                      } else {
-                        sl = tb[cj * W + p];
-                      }
-                      wslot[wid * 32 + j] = (int16_t)sl;
-                      p = sl + 1 == W ? 0 : sl + 1;
-                    }
+                  int my_p = 0;
+#pragma unroll 4
+                  for (int k2 = 0; k2 < m; ++k2) {
+                    p = tb[wc[k2] + p];
+                    if (k2 == rank) my_p = p;
                   }
                   __syncwarp();
-                  if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 3);
-                  p = __shfl_sync(FULL, p, 0);
-                  if (arr) slot = wslot[wid * 32 + lane];
+                  if (arr) slot = c == 0 ? -1 : (my_p == 0 ? W - 1 : my_p - 1);
                 }
               }
               if (arr) {
@@ -670,30 +659,15 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
                   hop_h = hcnt[i];
                   hop_es_node = rc.es_node;
                   hop_ee = rc.ee;
-                  hcnt[i] = (int16_t)(hop_h + 1);
+                  hcnt[i] = (int16_t)(hcnt[i] + 1);
                   cur[i] = (int16_t)(rc.ee >= L ? -1 : rc.dst);
                 }
               }
             }
-            if (lane == 0 && pass < 4 && k < 15) SPEC_PROF(64 + pass * 1024 + k * 64 + g);
-            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 4);
-            if (lane == 0) pcur[k] = p;
-#if SPEC_SYNC == 0
-            __threadfence_block();
+            if (lane == 0 && pass < 2 && k < 31) SPEC_PROF(64 + pass * 2048 + k * 64 + g);
             __syncwarp();
             if (lane == 0) spec_release(&front[k], need);
-#elif SPEC_SYNC == 1
-            __syncwarp();
-            if (lane == 0) spec_release(&front[k], need);
-#else
-            __syncwarp();
-            if (lane == 0) {
-              __threadfence_block();
-              *reinterpret_cast<volatile int*>(&front[k]) = need;
-            }
-#endif
-            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(3000 + (g - 8) * 16 + 5);
-            // the hops go to HBM after the release: no consumer reads them
+            // the hops go to HBM after the release (no consumer reads them)
             if (hop_h >= 0 && hop_h < max_hops) {
               const int64_t at = (c0 + i) * max_hops + hop_h;
               hop_node[at] = hop_es_node >> 16;
@@ -703,18 +677,42 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
               }
             }
           }
+          if (lane == 0) pcur[k] = p;
         }
       }
       __syncthreads();
       if (tid == 0 && pass < 4) SPEC_PROF(2 + 2 * pass);
-      for (int i = (g0 << 5) + tid; i < cn; i += T)
-        if (dfound[i] != dguess[i]) atomicMin(&scal[1], i);
+      if (!approx)
+        for (int i = (g0 << 5) + tid; i < cn; i += T)
+          if (dfound[i] != dguess[i]) atomicMin(&scal[1], i);
       __syncthreads();
       if (tid == 0 && pass < 4) SPEC_PROF(3 + 2 * pass);
-      const int f = approx ? 0 : scal[1];
-      if (approx) {  // the deferrals found become the first guess
+      if (approx) {
+        // verification: the routing with the chunk-start mean is the exact
+        // one up to the first request whose exact tokens put it in another
+        // class at a vertex it visited (by induction over the requests: the
+        // same classes at the same positions pick the same slots)
+        for (int i = tid; i < cn; i += T) {
+          const int nvis = hcnt[i] + dfound[i];
+          bool bad = nvis > hmax;
+          const double t0 = tk[i], t1 = tk_exact[i];
+          for (int h = 0; h < nvis && !bad; ++h) {
+            const int v = route_v[i * hmax + h], eb = obeg[v], deg = obeg[v + 1] - eb;
+            int c0 = 0, c1 = 0;
+            for (int j = 0; j < deg; ++j) {
+              c0 += t0 <= tes[eb + j];
+              c1 += t1 <= tes[eb + j];
+            }
+            bad = c0 != c1;
+          }
+          if (bad) atomicMin(&scal[1], i);
+        }
+        __syncthreads();
+      }
+      const int f = scal[1];
+      if (approx && f != 0x7fffffff) {  // exact passes from f's group, guessing the deferrals found
         for (int i = tid; i < cn; i += T) dguess[i] = dfound[i];
-        if (tid == 0) scal[0] = 0;
+        if (tid == 0) scal[0] = f >> 5;
       } else if (f == 0x7fffffff) {
         converged = true;
       } else {
@@ -1069,17 +1067,30 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
         for (int k = 0; k < nvo; ++k) meta.insert(meta.end(), preds[k].begin(), preds[k].end());
         constexpr int G1 = kSpecGroups + 1;
         auto a16 = [](size_t b) { return (b + 15) & ~size_t(15); };
-        int64_t nxt_cap = 0;  // next-slot tables: (deg - 1) * W per vertex
+        // longest route in picks (vertices of vorder along a path from the
+        // coordinator): the approximate pass records the vertices visited
+        int hmax = 0;
+        {
+          std::vector<int> picks(nvo, 0);
+          for (int k = 0; k < nvo; ++k) {
+            int best = 0;
+            for (int j = meta[nvo + k]; j < meta[nvo + k + 1]; ++j) best = std::max(best, picks[meta[2 * nvo + 1 + j]]);
+            picks[k] = best + 1;
+            hmax = std::max(hmax, picks[k]);
+          }
+          const char* ap = getenv("HELIO_ROUTE_APPROX");
+          if (hmax > 32 || (ap && ap[0] == '0')) hmax = 0;  // exact passes only
+        }
+        int64_t nxt_cap = 0;  // position tables: (deg + 1) * W per vertex
         for (int x = 0; x < nv && !cl.empty(); ++x) {
           const int deg = obeg[x + 1] - obeg[x];
-          if (deg > 1) nxt_cap += (int64_t)(deg - 1) * cl[x];
+          if (deg > 0) nxt_cap += (int64_t)(deg + 1) * cl[x];
         }
-        const int NW = kSpecThreads / 32;
-        const size_t spec_smem = 2 * a16(8 * kSpecChunk) + 2 * a16(4 * kSpecChunk) + 2 * a16(2 * kSpecChunk) +
+        const size_t spec_smem = a16(8 * kSpecChunk) + a16((size_t)kSpecChunk * hmax) + 2 * a16(8 * kSpecChunk) + 2 * a16(4 * kSpecChunk) + 2 * a16(2 * kSpecChunk) +
                                  2 * a16(kSpecChunk) + a16(8 * G1) + a16(4 * G1) + a16(2 * (size_t)nvo * G1) +
                                  a16(4 * (nvo + 1)) + a16(4 * nvo) + a16(4 * nv) + a16(8 * nv) +
-                                 2 * a16(8 * (size_t)ne) + a16(2 * (size_t)ne) + a16(4 * (nv + 1)) + a16(32 * NW) +
-                                 a16(64 * NW) + a16(2 * (size_t)nxt_cap) + 32 + (size_t)slots * sizeof(SlotRec);
+                                 2 * a16(8 * (size_t)ne) + a16(2 * (size_t)ne) + a16(4 * (nv + 1)) +
+                                 a16(2 * (size_t)nxt_cap) + a16(4 * kSpecThreads) + 16 * 32 + 32 + (size_t)slots * sizeof(SlotRec);
         const char* sp_env = getenv("HELIO_ROUTE_SPEC");
         const bool use_spec = consistent && !cl.empty() && spec_smem <= 227 * 1024 &&
                               (int)meta.size() <= nv + nv + 1 + ne && !(sp_env && sp_env[0] == '0');
@@ -1097,7 +1108,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
           if (!rc)
             route_masked_spec<<<1, kSpecThreads, spec_smem, st>>>(
                 R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst, d_oes, d_oee, d_node, d_kvcap,
-                d_cyclen, d_cyc, nvo, d_vord, (int)nxt_cap, d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr,
+                d_cyclen, d_cyc, nvo, d_vord, (int)nxt_cap, hmax, d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr,
                 want_se ? d_he : nullptr, d_den, d_passes);
           ctx->launches++;
           if (diag) {  // kernel time and passes (tools/route_spec_probe.py)

@@ -246,9 +246,8 @@ def test_masked_replay_division_is_ieee_division():
 @pytest.mark.parametrize("kv", [1e6, 7e5, 2e6])
 def test_masked_routes_one_million_match_reference(kv):
     """KV masking binds (geo24's plan with kv_bytes_per_token_layer raised so
-    4-60% of admissions are deferred): the exact replay kernel
-    (route_masked_warp) against the reference's Scheduler::admit/complete on
-    1M requests."""
+    13-96% of admissions are deferred): the exact replay (route_masked_spec)
+    against the reference's Scheduler::admit/complete on 1M requests."""
     import copy
     from _support import RefCluster, ref_available
     if not ref_available():
@@ -263,6 +262,66 @@ def test_masked_routes_one_million_match_reference(kv):
     nh, hn, hs, he, den = e.route(z["row"], pe, z["plan_flow"], inl, outl, c.num_layers)
     den_r, nh_r, hn_r, hs_r, he_r = RefCluster(d).route(z["row"], inl, outl)
     assert 0 < den_r < 1_000_000
+    assert den == den_r and np.array_equal(nh, nh_r)
+    mask = np.arange(hn.shape[1])[None, :] < np.maximum(nh, 0)[:, None]
+    assert np.array_equal(hn[mask], hn_r[mask])
+    assert np.array_equal(hs[mask], hs_r[mask]) and np.array_equal(he[mask], he_r[mask])
+
+
+def _masked_case(kv, plan="golden"):
+    import copy
+    if plan == "golden":
+        z = golden("route_geo24.npz")
+        d = copy.deepcopy(golden_cluster("geo24_float"))
+        row, pf = z["row"], z["plan_flow"]
+        pe = np.stack([z["plan_src"], z["plan_dst"], z["plan_es"], z["plan_ee"]], 1).astype(np.int32)
+    else:  # bench.py routing_leg's plan: first max of 100k geo24 candidates
+        import torch
+        d = clusters.CONFIGS["geo24"]("float")
+        c0 = h.Cluster.from_json(json.dumps(d))
+        e0 = h.Engine(c0)
+        e0.mode = "score"
+        B = 100_000
+        pl = torch.empty((B, e0.num_nodes, 2), dtype=torch.int16, device="cuda:0")
+        sp = torch.cuda.current_stream().cuda_stream
+        e0.generate_device(20240611, 0, B, 0, pl.data_ptr(), sp)
+        v = torch.empty(B, dtype=torch.float64, device="cuda:0")
+        st = torch.empty(B, dtype=torch.int32, device="cuda:0")
+        bv = torch.empty(1, dtype=torch.float64, device="cuda:0")
+        bi = torch.empty(1, dtype=torch.int64, device="cuda:0")
+        e0.score_device(pl.data_ptr(), B, v.data_ptr(), st.data_ptr(), True, sp)
+        e0.argmax_device(v.data_ptr(), st.data_ptr(), B, 0, bv.data_ptr(), bi.data_ptr(), sp)
+        torch.cuda.synchronize()
+        row = pl[int(bi.item())].cpu().numpy()
+        pe, pf, _ = e0.plan_edges(row)
+    d["model"]["kv_bytes_per_token_layer"] = kv
+    return d, row, pe, pf
+
+
+@pytest.mark.parametrize("variant", ["spec", "spec_exact_passes", "warp"])
+@pytest.mark.parametrize("plan,kv", [("golden", 1e6), ("golden", 5e6), ("bench", 1e6), ("bench", 3e6)])
+def test_masked_replay_variants_match_reference(variant, plan, kv, monkeypatch):
+    """The three exact replays of route.cu on the same masked workloads, each
+    against the reference's Scheduler::admit/complete: route_masked_spec
+    (approximate first pass + verification), route_masked_spec with exact
+    passes only (HELIO_ROUTE_APPROX=0: speculation on the deferral set with
+    restarts), and the serial route_masked_warp (HELIO_ROUTE_SPEC=0).  bench
+    is bench.py's routing plan (3% of 1M admissions deferred at kv 1e6)."""
+    from _support import RefCluster, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    if variant == "spec_exact_passes":
+        monkeypatch.setenv("HELIO_ROUTE_APPROX", "0")
+    elif variant == "warp":
+        monkeypatch.setenv("HELIO_ROUTE_SPEC", "0")
+    d, row, pe, pf = _masked_case(kv, plan)
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    R = 1_000_000 if variant == "spec" else 300_000
+    _, inl, outl = h.generate_trace_arrays(R, 0.0, "offline", 7)
+    nh, hn, hs, he, den = e.route(row, pe, pf, inl, outl, c.num_layers)
+    den_r, nh_r, hn_r, hs_r, he_r = RefCluster(d).route(row, inl, outl)
+    assert 0 < den_r
     assert den == den_r and np.array_equal(nh, nh_r)
     mask = np.arange(hn.shape[1])[None, :] < np.maximum(nh, 0)[:, None]
     assert np.array_equal(hn[mask], hn_r[mask])
