@@ -383,6 +383,7 @@ __device__ __forceinline__ int spec_pick(const SlotRec* rec, int base, int W, in
 
 // meta = [vorder: nvo vertex ids, end-layer order, the coordinator first]
 //        [pred_beg: nvo + 1] [pred: order indices of the vertices with an edge into each]
+//        [nleaves] [leaves: order indices of the vertices no routed vertex follows]
 __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
     int64_t R, int nv, int L, int max_hops, double kvb, const int32_t* __restrict__ obeg,
     const int32_t* __restrict__ odst, const int32_t* __restrict__ oes, const int32_t* __restrict__ oee,
@@ -397,6 +398,8 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
   const int32_t* vorder = meta;
   const int32_t* pred_beg = meta + nvo;
   const int32_t* pred = meta + 2 * nvo + 1;
+  const int32_t* leaves = pred + pred_beg[nvo] + 1;
+  const int nleaves = leaves[-1];
   size_t o = 0;
 #define take(bytes) (sm + ((o += ((size_t)(bytes) + 15) & ~size_t(15)) - (((size_t)(bytes) + 15) & ~size_t(15))))
   double* tk = reinterpret_cast<double*>(take(8 * C));
@@ -529,6 +532,7 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
         cur[i] = 0;
         hcnt[i] = 0;
         dfound[i] = 0;
+        if (approx) tk[i] = ((double)in_s[i] + a_grp[0]) * kvb;  // every token from the chunk-start mean
       }
       for (int k = tid; k < nvo; k += T) {
         front[k] = g0;
@@ -543,11 +547,6 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
         const unsigned lt = (1u << lane) - 1u;
         double a = a_grp[g0];
         int adm = adm_grp[g0];
-        if (approx) {  // pass 0: every token from the chunk-start mean
-          for (int i = lane; i < cn; i += 32) tk[i] = ((double)in_s[i] + a) * kvb;
-          __syncwarp();
-          if (lane == 0) spec_release(&front[nvo], G);
-        }
         // the division chain over the admissions, 32 requests at a time.  An
         // exact pass takes the guessed deferrals and publishes its tokens for
         // the vertex warps; the approximate pass runs it right behind the
@@ -556,10 +555,12 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
         const uint8_t* dsrc = approx ? dfound : dguess;
         double* tout = approx ? tk_exact : tk;
         for (int g = g0; g < G; ++g) {
-          if (approx) {  // the deepest vertices finish a group last
-            for (int k = nvo - 1; k >= 0; --k) spec_wait<false>(&front[k], g + 1);
+          if (lane == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6000 + (g - 8) * 8 + 0);
+          if (approx) {  // every vertex done with the group: every leaf is
+            for (int j = 0; j < nleaves; ++j) spec_wait<false>(&front[leaves[j]], g + 1);
             spec_fence();
           }
+          if (lane == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6000 + (g - 8) * 8 + 1);
           const int i0 = g << 5, i = i0 + lane;
           const bool valid = i < cn;
           const bool ad = valid && !dsrc[i];
@@ -570,6 +571,7 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
           const int rk = __popc(am & lt), m = __popc(am);
           if (ad) chain_ops[rk] = make_double2((double)out_s[i], ytab[adm + rk]);
           __syncwarp();
+          if (lane == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6000 + (g - 8) * 8 + 3);
           double my_a = a;  // the mean before request i: after its rk admitted predecessors
 #pragma unroll 4
           for (int k2 = 0; k2 < m; ++k2) {
@@ -578,6 +580,7 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
             if (k2 + 1 == rk) my_a = a;
           }
           __syncwarp();
+          if (lane == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6000 + (g - 8) * 8 + 2);
           if (valid) tout[i] = (my_in + my_a) * kvb;
           adm += m;
           __syncwarp();
@@ -599,19 +602,22 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
           const int eb = obeg[v], deg = obeg[v + 1] - eb;
           const int pb = pred_beg[k], pe = pred_beg[k + 1];
           const int16_t* tb = nxt + noff[v];
-          int32_t* wc = wcls + (wid << 5);
           const unsigned lt = (1u << lane) - 1u;
+          int32_t* wc = wcls + (wid << 5);
           int p = pcur[k];
           for (int g = g0; g < G; ++g) {
             const int need = g + 1;
-            spec_wait(&front[nvo], need);
+            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 0);
+            if (!approx) spec_wait(&front[nvo], need);  // (the approximate tokens are set before the pass)
             for (int j = pb; j < pe; ++j) spec_wait(&front[pred[j]], need);
             spec_fence();
+            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 1);
             if (lane == 0) pos_g[k * G1 + g] = (int16_t)p;
             const int i = (g << 5) + lane;
             int hop_h = -1, hop_es_node = 0, hop_ee = 0;
             const bool arr = i < cn && cur[i] == v;
             const unsigned am = __ballot_sync(FULL, arr);
+            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 2);
             if (am) {
               int slot = -1;
               if (approx && arr) {  // the route, for the verification
@@ -628,6 +634,7 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
                   for (int j = 0; j < deg; ++j) c += t <= tes[eb + j];
                 }
                 const unsigned fm = __ballot_sync(FULL, arr && c == deg);
+                if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 3);
                 if (fm == am) {  // every arrival takes the next slot
                   const int r = p + __popc(am & lt);
                   slot = r < W ? r : r % W;
@@ -650,6 +657,7 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
                   if (arr) slot = c == 0 ? -1 : (my_p == 0 ? W - 1 : my_p - 1);
                 }
               }
+              if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 4);
               if (arr) {
                 if (slot < 0) {
                   dfound[i] = 1;
@@ -665,8 +673,10 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
               }
             }
             if (lane == 0 && pass < 2 && k < 31) SPEC_PROF(64 + pass * 2048 + k * 64 + g);
+            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 5);
             __syncwarp();
             if (lane == 0) spec_release(&front[k], need);
+            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 6);
             // the hops go to HBM after the release (no consumer reads them)
             if (hop_h >= 0 && hop_h < max_hops) {
               const int64_t at = (c0 + i) * max_hops + hop_h;
@@ -959,7 +969,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
     TRY(ar.take(&d_he, want_se ? HR : 1));
     TRY(ar.take(&d_err, 1));
     TRY(ar.take(&d_den, 1));
-    TRY(ar.take(&d_vord, 2 * nv + 1 + ne));
+    TRY(ar.take(&d_vord, 3 * nv + 2 + ne));
     TRY(ar.take(&d_passes, 1));
     if (closed_path) {
       TRY(ar.take(&d_cur, R));
@@ -1065,6 +1075,17 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
           meta.push_back(meta[nvo + k] + (int32_t)preds[k].size());
         }
         for (int k = 0; k < nvo; ++k) meta.insert(meta.end(), preds[k].begin(), preds[k].end());
+        {  // leaves (no successor among the routed vertices): a group is done
+           // everywhere once every leaf is done with it
+          std::vector<char> has_succ(nvo, 0);
+          for (int k = 0; k < nvo; ++k)
+            for (int u : preds[k]) has_succ[u] = 1;
+          std::vector<int32_t> leaves;
+          for (int k = 0; k < nvo; ++k)
+            if (!has_succ[k]) leaves.push_back(k);
+          meta.push_back((int32_t)leaves.size());
+          meta.insert(meta.end(), leaves.begin(), leaves.end());
+        }
         constexpr int G1 = kSpecGroups + 1;
         auto a16 = [](size_t b) { return (b + 15) & ~size_t(15); };
         // longest route in picks (vertices of vorder along a path from the
@@ -1093,7 +1114,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
                                  a16(2 * (size_t)nxt_cap) + a16(4 * kSpecThreads) + 16 * 32 + 32 + (size_t)slots * sizeof(SlotRec);
         const char* sp_env = getenv("HELIO_ROUTE_SPEC");
         const bool use_spec = consistent && !cl.empty() && spec_smem <= 227 * 1024 &&
-                              (int)meta.size() <= nv + nv + 1 + ne && !(sp_env && sp_env[0] == '0');
+                              (int)meta.size() <= 3 * nv + 2 + ne && !(sp_env && sp_env[0] == '0');
         if (use_spec) {
           if (cudaMemcpyAsync(d_vord, meta.data(), 4 * meta.size(), cudaMemcpyHostToDevice, st) != cudaSuccess)
             rc = fail(ctx, HELIO_ERR_CUDA, "route H2D failed");
