@@ -555,12 +555,10 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
         const uint8_t* dsrc = approx ? dfound : dguess;
         double* tout = approx ? tk_exact : tk;
         for (int g = g0; g < G; ++g) {
-          if (lane == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6000 + (g - 8) * 8 + 0);
           if (approx) {  // every vertex done with the group: every leaf is
             for (int j = 0; j < nleaves; ++j) spec_wait<false>(&front[leaves[j]], g + 1);
             spec_fence();
           }
-          if (lane == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6000 + (g - 8) * 8 + 1);
           const int i0 = g << 5, i = i0 + lane;
           const bool valid = i < cn;
           const bool ad = valid && !dsrc[i];
@@ -571,7 +569,6 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
           const int rk = __popc(am & lt), m = __popc(am);
           if (ad) chain_ops[rk] = make_double2((double)out_s[i], ytab[adm + rk]);
           __syncwarp();
-          if (lane == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6000 + (g - 8) * 8 + 3);
           double my_a = a;  // the mean before request i: after its rk admitted predecessors
 #pragma unroll 4
           for (int k2 = 0; k2 < m; ++k2) {
@@ -580,7 +577,6 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
             if (k2 + 1 == rk) my_a = a;
           }
           __syncwarp();
-          if (lane == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6000 + (g - 8) * 8 + 2);
           if (valid) tout[i] = (my_in + my_a) * kvb;
           adm += m;
           __syncwarp();
@@ -607,17 +603,14 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
           int p = pcur[k];
           for (int g = g0; g < G; ++g) {
             const int need = g + 1;
-            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 0);
             if (!approx) spec_wait(&front[nvo], need);  // (the approximate tokens are set before the pass)
             for (int j = pb; j < pe; ++j) spec_wait(&front[pred[j]], need);
             spec_fence();
-            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 1);
             if (lane == 0) pos_g[k * G1 + g] = (int16_t)p;
             const int i = (g << 5) + lane;
             int hop_h = -1, hop_es_node = 0, hop_ee = 0;
             const bool arr = i < cn && cur[i] == v;
             const unsigned am = __ballot_sync(FULL, arr);
-            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 2);
             if (am) {
               int slot = -1;
               if (approx && arr) {  // the route, for the verification
@@ -634,7 +627,6 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
                   for (int j = 0; j < deg; ++j) c += t <= tes[eb + j];
                 }
                 const unsigned fm = __ballot_sync(FULL, arr && c == deg);
-                if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 3);
                 if (fm == am) {  // every arrival takes the next slot
                   const int r = p + __popc(am & lt);
                   slot = r < W ? r : r % W;
@@ -657,7 +649,6 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
                   if (arr) slot = c == 0 ? -1 : (my_p == 0 ? W - 1 : my_p - 1);
                 }
               }
-              if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 4);
               if (arr) {
                 if (slot < 0) {
                   dfound[i] = 1;
@@ -673,10 +664,8 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
               }
             }
             if (lane == 0 && pass < 2 && k < 31) SPEC_PROF(64 + pass * 2048 + k * 64 + g);
-            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 5);
             __syncwarp();
             if (lane == 0) spec_release(&front[k], need);
-            if (lane == 0 && k == 0 && pass == 0 && g >= 8 && g < 12) SPEC_PROF(6100 + (g - 8) * 8 + 6);
             // the hops go to HBM after the release (no consumer reads them)
             if (hop_h >= 0 && hop_h < max_hops) {
               const int64_t at = (c0 + i) * max_hops + hop_h;

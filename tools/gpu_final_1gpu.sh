@@ -14,3 +14,7 @@ timeout 1500 python bench.py --config syn256-120l --steps 5 --warmup 3 > $O/benc
 timeout 900 python bench.py --impl reference --config syn256-120l --steps 5 --warmup 3 > $O/bench_syn256_reference.json 2> $O/bench_syn256_reference.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-configs --no-routing --no-cpu-baseline > $O/ncu_bench.log 2>&1
+# the masked routing kernel: one route_masked_spec launch on bench.py's plan (kv 1e6, 200k requests)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:route_masked_spec -c 1 -o $O/masked_spec \
+  python tools/route_masked_probe.py 200000 bench 1e6 > $O/ncu_masked.log 2>&1
+PROBE_SPEC_ONLY=1 timeout 600 python tools/route_spec_probe.py 1000000 > $O/masked_probe.log 2>&1
