@@ -1089,7 +1089,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
             hmax = std::max(hmax, picks[k]);
           }
           const char* ap = getenv("HELIO_ROUTE_APPROX");
-          if (hmax > 32 || (ap && ap[0] == '0')) hmax = 0;  // exact passes only
+          if (hmax > 32 || nv > 256 || (ap && ap[0] == '0')) hmax = 0;  // exact passes only (route_v is 8-bit)
         }
         int64_t nxt_cap = 0;  // position tables: (deg + 1) * W per vertex
         for (int x = 0; x < nv && !cl.empty(); ++x) {

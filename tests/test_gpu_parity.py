@@ -328,6 +328,42 @@ def test_masked_replay_variants_match_reference(variant, plan, kv, monkeypatch):
     assert np.array_equal(hs[mask], hs_r[mask]) and np.array_equal(he[mask], he_r[mask])
 
 
+def test_masked_replay_many_vertices_matches_reference():
+    """A het42 plan (more routed vertices than the kernel has vertex warps, so
+    warps own several vertices) under KV masking: route_masked_spec against
+    the reference's Scheduler on 200k requests, for several kv sizes."""
+    from _support import RefCluster, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    d = clusters.CONFIGS["het42-70b"]("float")
+    c = h.Cluster.from_json(json.dumps(d))
+    e = h.Engine(c)
+    e.mode = "score"
+    rows = h.generate_host(list(e.kmax), c.num_layers, 5, 0, 20_000, 20_000)
+    v, st = e.score(rows)
+    ok = (st == 0) & (v > 0)
+    # the placement using the most nodes among the good ones
+    used = (rows[:, :, 1] > rows[:, :, 0]).sum(1)
+    cand = np.nonzero(ok & (v >= np.quantile(v[ok], 0.5)))[0]
+    row = rows[cand[np.argmax(used[cand])]]
+    pe, pf, _ = e.plan_edges(row)
+    _, inl, outl = h.generate_trace_arrays(200_000, 0.0, "offline", 7)
+    seen_partial = False
+    for kv in (2e5, 1e6, 5e6):
+        dm = json.loads(json.dumps(d))
+        dm["model"]["kv_bytes_per_token_layer"] = kv
+        cm = h.Cluster.from_json(json.dumps(dm))
+        em = h.Engine(cm)
+        nh, hn, hs, he, den = em.route(row, pe, pf, inl, outl, cm.num_layers)
+        den_r, nh_r, hn_r, hs_r, he_r = RefCluster(dm).route(row, inl, outl)
+        assert den == den_r and np.array_equal(nh, nh_r)
+        mask = np.arange(hn.shape[1])[None, :] < np.maximum(nh, 0)[:, None]
+        assert np.array_equal(hn[mask], hn_r[mask])
+        assert np.array_equal(hs[mask], hs_r[mask]) and np.array_equal(he[mask], he_r[mask])
+        seen_partial |= 0 < den_r < len(inl)
+    assert seen_partial
+
+
 @pytest.mark.parametrize("cap", ["float", "int"])
 def test_het42_prune12_variant_bit_exact_against_reference(cap):
     """het42 after the reference's prune_links(c, 12)
