@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
     int64_t R, int nv, int L, int max_hops, double kvb, const int32_t* __restrict__ obeg,
     const int32_t* __restrict__ odst, const int32_t* __restrict__ oes, const int32_t* __restrict__ oee,
     const int32_t* __restrict__ node_of, const double* __restrict__ kv_cap, const int32_t* __restrict__ cyc_len,
-    const int16_t* __restrict__ cyc, int nvo, const int32_t* __restrict__ meta, int nxt_cap, int hmax,
+    const int16_t* __restrict__ cyc, int nvo, const int32_t* __restrict__ meta, int nxt_cap, int pair_cap, int hmax,
     const int32_t* __restrict__ in_len, const int32_t* __restrict__ out_len, int32_t* nh, int32_t* hop_node,
     int32_t* hop_s, int32_t* hop_e, long long* deferred, int* passes_out) {
   extern __shared__ __align__(16) char sm[];
@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
   int16_t* hcnt = reinterpret_cast<int16_t*>(take(2 * C));
   uint8_t* dguess = reinterpret_cast<uint8_t*>(take(C));
   uint8_t* dfound = reinterpret_cast<uint8_t*>(take(C));
+  uint8_t* cls0 = reinterpret_cast<uint8_t*>(take(C));  // approximate pass: classes at the coordinator
   double* a_grp = reinterpret_cast<double*>(take(8 * G1));    // chain state at each group's start
   int32_t* adm_grp = reinterpret_cast<int32_t*>(take(4 * G1));
   int16_t* pos_g = reinterpret_cast<int16_t*>(take(2 * (size_t)nvo * G1));  // positions at group starts
@@ -420,12 +421,14 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
   int32_t* pos = reinterpret_cast<int32_t*>(take(4 * nv));  // committed relative positions
   int2* vgeo = reinterpret_cast<int2*>(take(8 * nv));
   const int ne = obeg[nv];
+  const int deg0 = obeg[1] - obeg[0];  // vorder[0] is the coordinator (vertex 0, edges from 0)
   double* tes = reinterpret_cast<double*>(take(8 * (size_t)ne));      // cut-offs per vertex, descending
   double* te_raw = reinterpret_cast<double*>(take(8 * (size_t)ne));   // cut-off of each edge
   int16_t* erank = reinterpret_cast<int16_t*>(take(2 * (size_t)ne));  // edge's rank in its vertex
   int32_t* noff = reinterpret_cast<int32_t*>(take(4 * (nv + 1)));     // next-slot tables per vertex
   int16_t* nxt = reinterpret_cast<int16_t*>(take(2 * (size_t)nxt_cap));
-  int32_t* wcls = reinterpret_cast<int32_t*>(take(4 * 32 * NW));  // per warp: class * W of each arrival
+  int32_t* wcls = reinterpret_cast<int32_t*>(take(4 * 32 * NW));  // per warp: class (* W) of each arrival
+  int16_t* nxt2 = reinterpret_cast<int16_t*>(take(2 * (size_t)pair_cap));  // coordinator: two-step table
   double2* chain_ops = reinterpret_cast<double2*>(take(16 * 32));
   int32_t* scal = reinterpret_cast<int32_t*>(take(16));
   double* scal_d = reinterpret_cast<double*>(take(16));
@@ -499,6 +502,18 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
     }
   }
   __syncthreads();
+  // the coordinator (every request's first pick) also gets a two-step table:
+  // nxt2[c1][c2][p] = nxt[c2][nxt[c1][p]], one load per two arrivals
+  if (pair_cap > 0) {
+    const int W0 = vgeo[0].y, D1 = deg0 + 1;
+    if (D1 * D1 * W0 > pair_cap) __trap();  // the host sizes pair_cap
+    const int16_t* t0 = nxt + noff[0];
+    for (int idx = tid; idx < D1 * D1 * W0; idx += T) {
+      const int p0 = idx % W0, cc = idx / W0, c2 = cc % D1, c1 = cc / D1;
+      nxt2[idx] = t0[c2 * W0 + t0[c1 * W0 + p0]];
+    }
+  }
+  __syncthreads();
   double avg = 232.0, samples = 1.0;  // thread 0: the committed running mean
   long long den = 0;
   int passes_total = 0;
@@ -532,7 +547,13 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
         cur[i] = 0;
         hcnt[i] = 0;
         dfound[i] = 0;
-        if (approx) tk[i] = ((double)in_s[i] + a_grp[0]) * kvb;  // every token from the chunk-start mean
+        if (approx) {  // every token from the chunk-start mean; the coordinator's classes up front
+          const double t = ((double)in_s[i] + a_grp[0]) * kvb;
+          tk[i] = t;
+          int c = 0;
+          for (int j = 0; j < deg0; ++j) c += t <= tes[j];
+          cls0[i] = (uint8_t)c;
+        }
       }
       for (int k = tid; k < nvo; k += T) {
         front[k] = g0;
@@ -554,10 +575,16 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
         // into tk_exact for the verification
         const uint8_t* dsrc = approx ? dfound : dguess;
         double* tout = approx ? tk_exact : tk;
+        int done_upto = 0;
         for (int g = g0; g < G; ++g) {
-          if (approx) {  // every vertex done with the group: every leaf is
-            for (int j = 0; j < nleaves; ++j) spec_wait<false>(&front[leaves[j]], g + 1);
+          if (approx && done_upto <= g) {  // every vertex done with the group: every leaf is
+            int lo = 0x7fffffff;
+            for (int j = 0; j < nleaves; ++j) {
+              spec_wait<false>(&front[leaves[j]], g + 1);
+              lo = min(lo, spec_load(&front[leaves[j]]));
+            }
             spec_fence();
+            done_upto = lo;  // the leaves are done through group lo - 1: no polling until then
           }
           const int i0 = g << 5, i = i0 + lane;
           const bool valid = i < cn;
@@ -622,9 +649,13 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
                 // prefix of the te-descending order)
                 int c = 0;
                 if (arr) {
-                  const double t = tk[i];
+                  if (approx && k == 0) {
+                    c = cls0[i];
+                  } else {
+                    const double t = tk[i];
 #pragma unroll 4
-                  for (int j = 0; j < deg; ++j) c += t <= tes[eb + j];
+                    for (int j = 0; j < deg; ++j) c += t <= tes[eb + j];
+                  }
                 }
                 const unsigned fm = __ballot_sync(FULL, arr && c == deg);
                 if (fm == am) {  // every arrival takes the next slot
@@ -637,16 +668,44 @@ __global__ void __launch_bounds__(kSpecThreads, 1) route_masked_spec(
                   // the serial path (p -> nxt[c][p]); the whole warp walks it
                   // in lockstep, the class offsets come from shared memory
                   const int rank = __popc(am & lt), m = __popc(am);
-                  if (arr) wc[rank] = c * W;
-                  __syncwarp();
-                  int my_p = 0;
+                  if (k == 0 && pair_cap > 0) {
+                    // the coordinator: two arrivals per load on the serial path;
+                    // each lane then recovers its own pick from the position
+                    // before it (or before the arrival ahead of it)
+                    if (arr) wc[rank] = c;
+                    __syncwarp();
+                    const int D1 = deg + 1;
+                    int my_pb = 0;
+                    int k2 = 0;
 #pragma unroll 4
-                  for (int k2 = 0; k2 < m; ++k2) {
-                    p = tb[wc[k2] + p];
-                    if (k2 == rank) my_p = p;
+                    for (; k2 + 1 < m; k2 += 2) {
+                      const int o2 = (wc[k2] * D1 + wc[k2 + 1]) * W;
+                      if (k2 == rank) my_pb = p;
+                      if (k2 + 1 == rank) my_pb = -1 - p;
+                      p = nxt2[o2 + p];
+                    }
+                    if (k2 < m) {
+                      if (k2 == rank) my_pb = p;
+                      p = tb[wc[k2] * W + p];
+                    }
+                    __syncwarp();
+                    if (arr) {
+                      const int pb = my_pb >= 0 ? my_pb : tb[wc[rank - 1] * W + (-1 - my_pb)];
+                      const int pa = tb[c * W + pb];
+                      slot = c == 0 ? -1 : (pa == 0 ? W - 1 : pa - 1);
+                    }
+                  } else {
+                    if (arr) wc[rank] = c * W;
+                    __syncwarp();
+                    int my_p = 0;
+#pragma unroll 4
+                    for (int k2 = 0; k2 < m; ++k2) {
+                      p = tb[wc[k2] + p];
+                      if (k2 == rank) my_p = p;
+                    }
+                    __syncwarp();
+                    if (arr) slot = c == 0 ? -1 : (my_p == 0 ? W - 1 : my_p - 1);
                   }
-                  __syncwarp();
-                  if (arr) slot = c == 0 ? -1 : (my_p == 0 ? W - 1 : my_p - 1);
                 }
               }
               if (arr) {
@@ -1091,16 +1150,21 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
           const char* ap = getenv("HELIO_ROUTE_APPROX");
           if (hmax > 32 || nv > 256 || (ap && ap[0] == '0')) hmax = 0;  // exact passes only (route_v is 8-bit)
         }
+        int pair_cap = 0;  // the coordinator's two-step table, when small
+        if (!cl.empty()) {
+          const int64_t d1 = obeg[1] - obeg[0] + 1;
+          if (d1 * d1 * cl[0] <= 8192) pair_cap = (int)(d1 * d1 * cl[0]);
+        }
         int64_t nxt_cap = 0;  // position tables: (deg + 1) * W per vertex
         for (int x = 0; x < nv && !cl.empty(); ++x) {
           const int deg = obeg[x + 1] - obeg[x];
           if (deg > 0) nxt_cap += (int64_t)(deg + 1) * cl[x];
         }
-        const size_t spec_smem = a16(8 * kSpecChunk) + a16((size_t)kSpecChunk * hmax) + 2 * a16(8 * kSpecChunk) + 2 * a16(4 * kSpecChunk) + 2 * a16(2 * kSpecChunk) +
+        const size_t spec_smem = a16(8 * kSpecChunk) + a16(kSpecChunk) + a16((size_t)kSpecChunk * hmax) + 2 * a16(8 * kSpecChunk) + 2 * a16(4 * kSpecChunk) + 2 * a16(2 * kSpecChunk) +
                                  2 * a16(kSpecChunk) + a16(8 * G1) + a16(4 * G1) + a16(2 * (size_t)nvo * G1) +
                                  a16(4 * (nvo + 1)) + a16(4 * nvo) + a16(4 * nv) + a16(8 * nv) +
                                  2 * a16(8 * (size_t)ne) + a16(2 * (size_t)ne) + a16(4 * (nv + 1)) +
-                                 a16(2 * (size_t)nxt_cap) + a16(4 * kSpecThreads) + 16 * 32 + 32 + (size_t)slots * sizeof(SlotRec);
+                                 a16(2 * (size_t)nxt_cap) + a16(4 * kSpecThreads) + a16(2 * (size_t)pair_cap) + 16 * 32 + 32 + (size_t)slots * sizeof(SlotRec);
         const char* sp_env = getenv("HELIO_ROUTE_SPEC");
         const bool use_spec = consistent && !cl.empty() && spec_smem <= 227 * 1024 &&
                               (int)meta.size() <= 3 * nv + 2 + ne && !(sp_env && sp_env[0] == '0');
@@ -1118,7 +1182,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
           if (!rc)
             route_masked_spec<<<1, kSpecThreads, spec_smem, st>>>(
                 R, nv, L, max_hops, ctx->kv_token_layer_bytes, d_obeg, d_odst, d_oes, d_oee, d_node, d_kvcap,
-                d_cyclen, d_cyc, nvo, d_vord, (int)nxt_cap, hmax, d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr,
+                d_cyclen, d_cyc, nvo, d_vord, (int)nxt_cap, pair_cap, hmax, d_in, d_out, d_nh, d_hn, want_se ? d_hs : nullptr,
                 want_se ? d_he : nullptr, d_den, d_passes);
           ctx->launches++;
           if (diag) {  // kernel time and passes (tools/route_spec_probe.py)
