@@ -716,6 +716,23 @@ def time_steps(step, flush, stream, steps, dev):
     return sum(a.elapsed_time(b) for a, b in ev)
 
 
+def compare_values(host_vals, host_status, dev_vals, dev_status, mode):
+    """The host-entry results against the device path's.  Statuses must be
+    equal; PARITY values bit-identical; SCORE values within the 1e-9 relative
+    contract: on float capacities the large-graph builder's
+    arc order — and with it the last bits of a push-relabel sum — can depend
+    on warp scheduling."""
+    import numpy as np
+    hv_ = host_vals.numpy() if hasattr(host_vals, "numpy") else np.asarray(host_vals)
+    dv_ = dev_vals.cpu().numpy()
+    assert np.array_equal(np.asarray(host_status.numpy() if hasattr(host_status, "numpy") else host_status),
+                          np.asarray(dev_status)), "e2e statuses differ"
+    same = hv_.view(np.int64) == dv_.view(np.int64)
+    rel = float(np.max(np.abs(hv_ - dv_) / np.maximum(1.0, np.abs(dv_)))) if hv_.size else 0.0
+    assert rel <= (0.0 if mode == "parity" else 1e-9), f"e2e values differ (max rel {rel:.3g})"
+    return {"bit_identical": int(same.sum()), "of": int(same.size), "max_rel_diff": rel}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -924,13 +941,14 @@ def main():
             return G * steps / float(tt.item()), res
 
         e2e_rate, e2e_best = e2e_time(host, hv, hs, args.steps)
+        check = compare_values(hv, hs, head_vals, st_host, args.mode)
         if world == 1:
-            assert int(e2e_best[1]) == win[1], "e2e winner differs from the device path"
-        assert torch.equal(hv.view(torch.int64), head_vals.cpu().view(torch.int64)), "e2e values differ"
+            assert int(e2e_best[1]) == win[1] or abs(float(e2e_best[0]) - win[0]) <= 1e-9 * abs(win[0]), \
+                "e2e winner differs from the device path"
         e2e = {"value": e2e_rate, "unit": "evals/s", "h2d_bytes_per_step": G * 4 * N,
                "d2h_bytes_per_step": G * 12 + 16 * world,
                "call": "helio_gpu_score_best_host (pinned host placements in; every value + status and the "
-                       "first-max winner out)"}
+                       "first-max winner out)", "check_vs_device": check}
         # pageable buffers (what Engine.score and a plain ctypes caller pass):
         # the entry stages chunks through its own pinned buffers
         hp = torch.empty((B, N, 2), dtype=torch.int16)
@@ -939,10 +957,11 @@ def main():
         hvp = torch.empty(B, dtype=torch.float64)
         hsp = torch.empty(B, dtype=torch.int32)
         prate, _ = e2e_time(hp, hvp, hsp, min(args.steps, 5))
-        assert torch.equal(hvp.view(torch.int64), head_vals.cpu().view(torch.int64)), "pageable e2e values differ"
+        pcheck = compare_values(hvp, hsp, head_vals, st_host, args.mode)
         e2e_pageable = {"value": prate, "unit": "evals/s", "h2d_bytes_per_step": G * 4 * N,
                         "d2h_bytes_per_step": G * 12 + 16 * world,
-                        "call": "helio_gpu_score_best_host with pageable host buffers (staged)"}
+                        "call": "helio_gpu_score_best_host with pageable host buffers (staged)",
+                        "check_vs_device": pcheck}
         del hp, hvp, hsp
 
     # extras (single-GPU views of the headline cluster) only at N = 1: at N > 1

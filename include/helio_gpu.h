@@ -254,7 +254,10 @@ int helio_gpu_generate_walk_host(const helio_gpu_ctx* ctx, uint64_t seed, int64_
  * once with out_len[r].  Plan edges in plan order; placement is the plan's
  * int16 [N][2] row.  hop arrays are [R][max_hops] (h_hop_start/h_hop_end may
  * both be NULL to return node ids only); h_num_hops[r] = -1 for a deferred
- * request.  *h_deferred receives the number of deferrals. */
+ * request; hop entries past a request's count (all of a deferred request's)
+ * are unspecified.  *h_deferred receives the number of deferrals.  When KV
+ * masking can bind, the exact replay of the reference's eligibility tests runs
+ * (route.cu route_masked_spec / route_masked_warp); otherwise the closed form. */
 int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_placement,
                          const helio_plan_edge* h_plan_edges, int32_t num_plan_edges, int64_t R,
                          const int32_t* h_in_len, const int32_t* h_out_len, int32_t max_hops,

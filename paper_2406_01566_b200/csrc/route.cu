@@ -1166,7 +1166,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
                                  2 * a16(8 * (size_t)ne) + a16(2 * (size_t)ne) + a16(4 * (nv + 1)) +
                                  a16(2 * (size_t)nxt_cap) + a16(4 * kSpecThreads) + a16(2 * (size_t)pair_cap) + 16 * 32 + 32 + (size_t)slots * sizeof(SlotRec);
         const char* sp_env = getenv("HELIO_ROUTE_SPEC");
-        const bool use_spec = consistent && !cl.empty() && spec_smem <= 227 * 1024 &&
+        const bool use_spec = consistent && !cl.empty() && spec_smem <= 227 * 1024 && obeg[1] - obeg[0] < 256 /* cls0 is 8-bit */ &&
                               (int)meta.size() <= 3 * nv + 2 + ne && !(sp_env && sp_env[0] == '0');
         if (use_spec) {
           if (cudaMemcpyAsync(d_vord, meta.data(), 4 * meta.size(), cudaMemcpyHostToDevice, st) != cudaSuccess)

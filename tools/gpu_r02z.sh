@@ -1,4 +1,6 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-PROBE_SPEC_ONLY=1 timeout 600 python tools/route_spec_probe.py 1000000 > gpurun_out/r02z_spec.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "route or masked" > gpurun_out/r02z_tests.log 2>&1
+for i in 1 2 3; do
+timeout 900 python bench.py --config syn256-120l --steps 5 --warmup 3 --no-configs --no-routing --no-cpu-baseline > gpurun_out/r02z_syn_$i.json 2> gpurun_out/r02z_syn_$i.err
+done
+timeout 900 python bench.py --steps 10 --warmup 3 --no-configs --no-routing --no-cpu-baseline > gpurun_out/r02z_het.json 2> gpurun_out/r02z_het.err
