@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <optional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -450,10 +451,19 @@ int64_t refh_route(void* cp, const int16_t* pl, int allow_partial, uint64_t seed
   } catch (const std::exception&) {
     return -1;
   }
-  Scheduler sched(c, plan, SchedPolicy::kIwrr, seed);
+  // the reference's ValidationErrors (a plan without a coordinator edge, a
+  // route that does not tile the layers) come back as -2 / -3 instead of
+  // unwinding through the C ABI
   int64_t denied = 0;
+  try {
+  Scheduler sched(c, plan, SchedPolicy::kIwrr, seed);
   for (int64_t r = 0; r < R; ++r) {
-    auto route = sched.admit(static_cast<long>(r), in_len[r]);
+    std::optional<std::vector<RouteHop>> route;
+    try {
+      route = sched.admit(static_cast<long>(r), in_len[r]);
+    } catch (const std::exception&) {
+      return -3;
+    }
     if (!route) {
       ++denied;
       nhops[r] = -1;
@@ -467,6 +477,9 @@ int64_t refh_route(void* cp, const int16_t* pl, int allow_partial, uint64_t seed
       hop_e[r * max_hops + k] = (*route)[k].exec_end;
     }
     sched.complete(static_cast<long>(r), out_len[r]);
+  }
+  } catch (const std::exception&) {
+    return -2;
   }
   return denied;
 }
