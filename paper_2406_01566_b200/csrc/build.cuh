@@ -483,6 +483,11 @@ __device__ int build_graph_score_contract(const ClusterDev& cd, const Gs& g, con
   // kept vertex — s (source arcs), a kept in-vertex (its compute edge) or a
   // kept out-vertex (its dout out-edges).  So deg(in_k) = din + 1,
   // deg(out_k) = 1 + dout, deg(s) = #source arcs, deg(t) = #sink arcs.
+  // Arc order is fixed by construction (no atomic order): at every vertex
+  // its forward arcs first — the source's in node order, an in-vertex's one
+  // compute/contracted edge, an out-vertex's out-links in list order then the
+  // sink arc — and then its reverse arcs sorted by their partners' positions.
+  int16_t* nf = g.h;  // forward arcs per contracted vertex (h is the solver's; free while building)
   int nedges = 0, nsrc = 0, nsnk = 0;
   for (int k = lane; k < N; k += 32) {
     const int32_t w = pse[k];
@@ -496,10 +501,12 @@ __device__ int build_graph_score_contract(const ClusterDev& cd, const Gs& g, con
     const int xi = vin[k], xo = vout[k];
     if (xi >= 0) {
       fill[xi] = din[k] + 1;
+      nf[xi] = 1;
       ++nedges;
     }
     if (xo >= 0) {
       fill[xo] = 1 + dout[k];
+      nf[xo] = (int16_t)dout[k];
       nedges += dout[k];
     }
   }
@@ -507,11 +514,31 @@ __device__ int build_graph_score_contract(const ClusterDev& cd, const Gs& g, con
   nsrc = __reduce_add_sync(FULL, nsrc);
   nsnk = __reduce_add_sync(FULL, nsnk);
   if (2 * nedges > lay.A) return ST_OVERFLOW;
+  // the source's arcs in node order: rank of k among the source-fed nodes
+  // (din is free once the degrees are in)
+  {
+    int run2 = 0;
+    for (int k0 = 0; k0 < N; k0 += 32) {
+      const int k = k0 + lane;
+      bool f = false;
+      if (k < N) {
+        const int32_t w = pse[k];
+        const int s = (int16_t)(w & 0xffff), e = (int16_t)(w >> 16);
+        f = e > s && s == 0 && __ldg(cd.cout_link + k) >= 0;
+      }
+      const unsigned m = __ballot_sync(FULL, f);
+      if (f) din[k] = run2 + __popc(m & ((1u << lane) - 1u));
+      run2 += __popc(m);
+    }
+  }
   if (lane == 0) {
     fill[0] = nsrc;
     fill[1] = nsnk;
+    nf[0] = (int16_t)nsrc;
+    nf[1] = 0;
   }
   __syncwarp();
+  int* rfill = fill + V;  // reverse-arc counters (the ex region holds 2V ints)
   {
     int r2 = 0;
     for (int x0 = 0; x0 < V; x0 += 32) {
@@ -525,17 +552,18 @@ __device__ int build_graph_score_contract(const ClusterDev& cd, const Gs& g, con
       }
       if (x < V) {
         g.abeg[x] = (int16_t)(r2 + incl - d);
-        fill[x] = 0;
+        rfill[x] = 0;
       }
       r2 += __shfl_sync(FULL, incl, 31);
     }
     if (lane == 0) g.abeg[V] = (int16_t)r2;
   }
   __syncwarp();
-  // one walk per contracted edge: forward arc at its start, reverse at its end
-  auto emit = [&](int a, int b, double c) {
-    const int fa = g.abeg[a] + atomicAdd(&fill[a], 1);
-    const int ra = g.abeg[b] + atomicAdd(&fill[b], 1);
+  // one walk per contracted edge: forward arc at its start (slot given),
+  // reverse at its end (claimed, sorted below)
+  auto emit = [&](int a, int fslot, int b, double c) {
+    const int fa = g.abeg[a] + fslot;
+    const int ra = g.abeg[b] + nf[b] + atomicAdd(&rfill[b], 1);
     g.to[fa] = (int16_t)b;
     g.rv[fa] = (int16_t)ra;
     g.cap[fa] = c;
@@ -551,24 +579,43 @@ __device__ int build_graph_score_contract(const ClusterDev& cd, const Gs& g, con
     if (s == 0 && lc >= 0) {
       double c = __ldg(cd.link_cap + lc);
       const int b = contract_walk(cd, pse, vin, vout, succ, k, false, c);
-      emit(0, b, c);
+      emit(0, din[k], b, c);
     }
     const int xi = vin[k];
     if (xi >= 0) {
       double c = __ldg(cd.cap_tab + __ldg(cd.cap_off + k) + (e - s) - 1);
       const int b = contract_walk(cd, pse, vin, vout, succ, k, true, c);
-      emit(xi, b, c);
+      emit(xi, 0, b, c);
     }
     const int xo = vout[k];
     if (xo >= 0) {
+      int fo = 0;
       for_valid_out_links(cd, pse, k, e, partial, [&](int j, int link) {
         double c = __ldg(cd.link_cap + link);
         const int b = contract_walk(cd, pse, vin, vout, succ, j, false, c);
-        emit(xo, b, c);
+        emit(xo, fo++, b, c);
       });
       const int lk = __ldg(cd.cin_link + k);
-      if (e == L && lk >= 0) emit(xo, 1, __ldg(cd.link_cap + lk));
+      if (e == L && lk >= 0) emit(xo, fo, 1, __ldg(cd.link_cap + lk));
     }
+  }
+  __syncwarp();
+  // reverse arcs by partner position (partners are forward arcs, which stay
+  // put), then each partner pointed back at its reverse arc's final slot
+  for (int x = lane; x < V; x += 32) {
+    const int b0 = g.abeg[x] + nf[x], b1 = g.abeg[x + 1];
+    for (int i = b0 + 1; i < b1; ++i) {
+      const int16_t ti = g.to[i], ri = g.rv[i];
+      int j = i - 1;
+      while (j >= b0 && g.rv[j] > ri) {
+        g.to[j + 1] = g.to[j];
+        g.rv[j + 1] = g.rv[j];
+        --j;
+      }
+      g.to[j + 1] = ti;
+      g.rv[j + 1] = ri;
+    }
+    for (int i = b0; i < b1; ++i) g.rv[g.rv[i]] = (int16_t)i;
   }
   __syncwarp();
   E = nedges;
