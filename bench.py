@@ -808,9 +808,11 @@ def main():
     pl = make_rows(first, B)
     vals = torch.empty(B, dtype=torch.float64, device=dev)
     st = torch.empty(B, dtype=torch.int32, device=dev)
-    best = torch.empty(1, dtype=torch.float64, device=dev)
-    bidx = torch.empty(1, dtype=torch.int64, device=dev)
+    # the argmax writes its 16-byte record (value bits, global index) straight
+    # into the all-gather's send buffer
     rec = torch.empty(2, dtype=torch.int64, device=dev)
+    best = rec[0:1].view(torch.float64)
+    bidx = rec[1:2]
     gathered = torch.empty(2 * world, dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
 
@@ -818,8 +820,6 @@ def main():
         eng.score_device(rows.data_ptr(), n, v.data_ptr(), s.data_ptr(), True, sp)
         eng.argmax_device(v.data_ptr(), s.data_ptr(), n, base, best.data_ptr(), bidx.data_ptr(), sp)
         if world > 1:
-            rec[0:1].copy_(best.view(torch.int64))
-            rec[1:2].copy_(bidx)
             dist.all_gather_into_tensor(gathered, rec)
 
     def step():
