@@ -152,6 +152,10 @@ struct helio_gpu_ctx {
   // routing arena (route.cu), grows only
   void* d_route = nullptr;
   size_t route_cap = 0;
+
+  // pinned host staging of the routing entry's pageable buffers, grows only
+  void* h_route_pin = nullptr;
+  size_t route_pin_cap = 0;
 };
 
 
@@ -195,6 +199,25 @@ inline int host_arena(helio_gpu_ctx* ctx, size_t bytes, char** out) {
     ctx->host_arena_cap = cap;
   }
   *out = static_cast<char*>(ctx->d_host_arena);
+  return HELIO_OK;
+}
+
+// Pageable <-> pinned staging copy split over a few host threads (helio_gpu.cu).
+void stage_copy(void* dst, const void* src, size_t bytes);
+// cudaPointerGetAttributes says page-locked host memory.
+bool is_pinned(const void* p);
+
+// The routing entry's pinned staging buffer with at least `bytes`.
+inline int route_pin(helio_gpu_ctx* ctx, size_t bytes, char** out) {
+  if (ctx->route_pin_cap < bytes) {
+    cudaFreeHost(ctx->h_route_pin);
+    ctx->h_route_pin = nullptr;
+    ctx->route_pin_cap = 0;
+    const size_t cap = std::max<size_t>(bytes + bytes / 4, size_t(1) << 20);
+    CK(cudaMallocHost(&ctx->h_route_pin, cap));
+    ctx->route_pin_cap = cap;
+  }
+  *out = static_cast<char*>(ctx->h_route_pin);
   return HELIO_OK;
 }
 

@@ -624,6 +624,9 @@ int ensure_stage(helio_gpu_ctx* ctx, int64_t chunk) {
   return HELIO_OK;
 }
 
+}  // namespace
+
+namespace helio_engine {
 // Pageable <-> pinned staging copies: large ones are split over a few host
 // threads (one thread copies ~10 GB/s; het42's 256k-row chunk is 43 MB).
 void stage_copy(void* dst, const void* src, size_t bytes) {
@@ -652,8 +655,7 @@ bool is_pinned(const void* p) {
   }
   return at.type == cudaMemoryTypeHost;
 }
-
-}  // namespace
+}  // namespace helio_engine
 
 // ===========================================================================
 extern "C" {
@@ -737,6 +739,7 @@ void helio_gpu_destroy(helio_gpu_ctx* ctx) {
   cudaFree(ctx->d_bidx);
   cudaFree(ctx->d_route);
   cudaFree(ctx->d_host_arena);
+  cudaFreeHost(ctx->h_route_pin);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->api_ev) cudaEventDestroy(ctx->api_ev);

@@ -1034,6 +1034,11 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
       else ctx->route_cap = ar.off;
     }
   }
+  // pinned staging of the pageable request stream and outputs (large calls)
+  char* pin = nullptr;
+  const size_t out_bytes = 4 * (size_t)R + (max_hops > 0 ? 4 * HR * (want_se ? 3 : 1) : 0);
+  const bool stage_io = !rc && R >= (int64_t(1) << 18) && !(is_pinned(h_in) && is_pinned(h_nh)) &&
+                        route_pin(ctx, std::max<size_t>(8 * (size_t)R, out_bytes), &pin) == HELIO_OK;
   if (!rc) {
     auto H2D = [&](void* d, const void* h, size_t bytes) {
       if (bytes && !rc && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
@@ -1047,8 +1052,17 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
     H2D(d_node, node_of.data(), 4 * nv);
     H2D(d_kvcap, kv_cap.data(), 8 * nv);
     H2D(d_cycoff, cyc_off.data(), 4 * (nv + 1));
-    H2D(d_in, h_in, 4 * R);
-    H2D(d_out, h_out, 4 * R);
+    // large pageable request streams go through a pinned staging buffer
+    // (threaded host copies, then full-speed DMA), the outputs likewise below
+    if (stage_io && !rc) {
+      stage_copy(pin, h_in, 4 * R);
+      stage_copy(pin + 4 * R, h_out, 4 * R);
+      H2D(d_in, pin, 4 * R);
+      H2D(d_out, pin + 4 * R, 4 * R);
+    } else {
+      H2D(d_in, h_in, 4 * R);
+      H2D(d_out, h_out, 4 * R);
+    }
     if (!rc && (cudaMemsetAsync(d_err, 0, sizeof(int), st) != cudaSuccess ||
                 cudaMemsetAsync(d_den, 0, sizeof(long long), st) != cudaSuccess))
       rc = fail(ctx, HELIO_ERR_CUDA, "route memset failed");
@@ -1220,16 +1234,29 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   }
   int herr = 0;
   if (!rc && R > 0) {
-    bool ok = cudaMemcpyAsync(h_nh, d_nh, 4 * R, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+    // destinations: the caller's buffers, or the pinned staging buffer
+    int32_t* o_nh = stage_io ? reinterpret_cast<int32_t*>(pin) : h_nh;
+    int32_t* o_hn = stage_io ? o_nh + R : h_hn;
+    int32_t* o_hs = stage_io ? o_hn + HR : h_hs;
+    int32_t* o_he = stage_io ? o_hs + HR : h_he;
+    bool ok = cudaMemcpyAsync(o_nh, d_nh, 4 * R, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
               cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, st) == cudaSuccess;
-    if (ok && max_hops > 0) ok = cudaMemcpyAsync(h_hn, d_hn, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+    if (ok && max_hops > 0) ok = cudaMemcpyAsync(o_hn, d_hn, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess;
     if (ok && max_hops > 0 && want_se)
-      ok = cudaMemcpyAsync(h_hs, d_hs, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-           cudaMemcpyAsync(h_he, d_he, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess;
+      ok = cudaMemcpyAsync(o_hs, d_hs, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+           cudaMemcpyAsync(o_he, d_he, 4 * HR, cudaMemcpyDeviceToHost, st) == cudaSuccess;
     long long dd = 0;
     if (ok && !closed) ok = cudaMemcpyAsync(&dd, d_den, sizeof(long long), cudaMemcpyDeviceToHost, st) == cudaSuccess;
     ok = ok && cudaStreamSynchronize(st) == cudaSuccess;
     if (!ok) rc = fail(ctx, HELIO_ERR_CUDA, std::string("route: ") + cudaGetErrorString(cudaGetLastError()));
+    if (!rc && stage_io) {
+      stage_copy(h_nh, o_nh, 4 * R);
+      if (max_hops > 0) stage_copy(h_hn, o_hn, 4 * HR);
+      if (max_hops > 0 && want_se) {
+        stage_copy(h_hs, o_hs, 4 * HR);
+        stage_copy(h_he, o_he, 4 * HR);
+      }
+    }
     if (!rc && closed)
       for (int64_t r = 0; r < R; ++r) den += h_nh[r] < 0;
     else
