@@ -307,10 +307,17 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
 // wrong: everything before f was exact (tokens and positions), so the next
 // pass guesses the deferrals found and restarts from f's group with the
 // positions and chain state saved at that group's start; f moves forward every
-// pass, and after kSpecPasses the chunk is replayed serially instead.  The
-// first pass of a chunk takes every token from the chunk-start mean (no chain:
-// the mean drifts by a fraction of a token over a chunk), which gives the
-// exact pass a guess that is almost always right.
+// pass, and after kSpecPasses the chunk is replayed serially instead.
+//
+// The first pass of a chunk is approximate: every token comes from the
+// chunk-start mean (the mean drifts by a fraction of a token over a chunk), so
+// the vertex warps run without waiting for the chain, and warp 0 runs the
+// exact chain right behind them on the deferrals they found (it waits on the
+// DAG's leaves).  Verification is then parallel: a request whose exact tokens
+// give the same class at every vertex it visited picks the same slots (by
+// induction over the requests), so the pass stands up to the first request
+// where a class differs, and exact passes take over from that request's group.
+// On bench.py's plan 97% of chunks are done after the approximate pass.
 //
 // Picks.  Eligibility of an edge, RN(tk * len) <= thr, is monotone in tk, so
 // each edge has an exact cut-off te (the largest double passing; bisection
@@ -319,7 +326,10 @@ __global__ void route_masked_warp(int64_t R, int nv, int L, int max_hops, double
 // class-deg arrival takes the current slot; a masked one (0 < c < deg) takes
 // nxt[c][p], a per-vertex table of the first slot at or after p whose edge is
 // among the top c (built at launch); class 0 is deferred with the position
-// unchanged.  So a pick is one shared-memory load whatever the mask.
+// unchanged.  So a pick is one shared-memory load whatever the mask.  The
+// coordinator, which every request passes, also gets a two-step table
+// (two arrivals per load) and, in the approximate pass, its classes are
+// computed for the whole chunk before the pass.
 constexpr int kSpecChunk = 2048, kSpecGroups = kSpecChunk / 32, kSpecThreads = 1024, kSpecPasses = 8;
 
 // Frontier flags live in shared memory: relaxed CTA-scope loads/stores on
