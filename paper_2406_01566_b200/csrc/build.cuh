@@ -23,9 +23,13 @@ struct LinkEval {
   int u, v;
 };
 
+__device__ __forceinline__ LinkEval eval_link_pk(const ClusterDev& cd, const Gs& g, uint32_t pk, int partial);
 __device__ __forceinline__ LinkEval eval_link(const ClusterDev& cd, const Gs& g, int l, int partial) {
+  return eval_link_pk(cd, g, __ldg(cd.link_pack + l), partial);
+}
+// (pk = link_pack[l], loaded ahead by callers that scan many links)
+__device__ __forceinline__ LinkEval eval_link_pk(const ClusterDev& cd, const Gs& g, uint32_t pk, int partial) {
   LinkEval r{false, 0, 0};
-  const uint32_t pk = __ldg(cd.link_pack + l);
   const int a = (int)(pk & 0xffffu) - 1;
   const int bb = (int)(pk >> 16) - 1;
   if (a < 0) {  // coordinator -> bb (:89-101)

@@ -153,9 +153,9 @@ struct helio_gpu_ctx {
   void* d_route = nullptr;
   size_t route_cap = 0;
 
-  // pinned host staging of the routing entry's pageable buffers, grows only
-  void* h_route_pin = nullptr;
-  size_t route_pin_cap = 0;
+  // pinned host staging of the routing and flows entries, grows only
+  void* h_stage_pin = nullptr;
+  size_t stage_pin_cap = 0;
 };
 
 
@@ -207,17 +207,17 @@ void stage_copy(void* dst, const void* src, size_t bytes);
 // cudaPointerGetAttributes says page-locked host memory.
 bool is_pinned(const void* p);
 
-// The routing entry's pinned staging buffer with at least `bytes`.
-inline int route_pin(helio_gpu_ctx* ctx, size_t bytes, char** out) {
-  if (ctx->route_pin_cap < bytes) {
-    cudaFreeHost(ctx->h_route_pin);
-    ctx->h_route_pin = nullptr;
-    ctx->route_pin_cap = 0;
+// The host entries' pinned staging buffer with at least `bytes`.
+inline int host_pin(helio_gpu_ctx* ctx, size_t bytes, char** out) {
+  if (ctx->stage_pin_cap < bytes) {
+    cudaFreeHost(ctx->h_stage_pin);
+    ctx->h_stage_pin = nullptr;
+    ctx->stage_pin_cap = 0;
     const size_t cap = std::max<size_t>(bytes + bytes / 4, size_t(1) << 20);
-    CK(cudaMallocHost(&ctx->h_route_pin, cap));
-    ctx->route_pin_cap = cap;
+    CK(cudaMallocHost(&ctx->h_stage_pin, cap));
+    ctx->stage_pin_cap = cap;
   }
-  *out = static_cast<char*>(ctx->h_route_pin);
+  *out = static_cast<char*>(ctx->h_stage_pin);
   return HELIO_OK;
 }
 

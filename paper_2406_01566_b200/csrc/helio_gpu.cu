@@ -109,7 +109,7 @@ __global__ void HELIO_SCORE_BOUNDS score_kernel(ClusterDev cd, Layout lay, const
                  ? (!GEN && cd.out_mask ? build_graph_score_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E, cut)
                  : GEN                  ? build_graph_score_contract(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
                                         : build_graph_score_r1(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E))
-                 : (cd.less_cout && !fo.edges
+                 : (cd.less_cout
                         ? build_graph_small(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E)
                         : build_graph(cd, g, lay, pl + b * 2 * cd.N, partial, lane, V, E));
     if (st == ST_OVERFLOW) {
@@ -521,6 +521,21 @@ void launch_score_mode(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t
   const bool glob = ctx->glob_ok[MODE] && ctx->d_glob != nullptr;
   if (timed) cudaEventRecord(ctx->ev0, st);
   const Layout& sl = ctx->slot_small[MODE];
+  if (B == 1 && !timed) {
+    // one candidate (the per-call entries): straight into the biggest shared
+    // slot — one warp either way, and the small and middle tiers' launches
+    // are saved; only a graph beyond one SM goes on to the global tier
+    const Layout& bl1 = ctx->slot_big_ok[MODE] ? ctx->slot_big[MODE] : sl;
+    auto K1 = score_kernel<MODE, GEN>;
+    K1<<<1, 32, bl1.bytes, st>>>(ctx->cd, bl1, d_pl, B, partial, d_val, d_st, work + 2, nullptr, nullptr,
+                                 glob ? l3 : nullptr, oc + 2, nullptr, fo);
+    if (glob) {
+      score_kernel<MODE, GEN, true><<<1, 32, 0, st>>>(ctx->cd, ctx->slot_glob[MODE], d_pl, B, partial, d_val, d_st,
+                                                      work + 3, l3, oc + 2, nullptr, nullptr, ctx->d_glob, fo);
+      ctx->launches += 1;
+    }
+    return;
+  }
   const int warps = ctx->slot_warps[MODE];
   const int grid = (int)std::min<int64_t>(ctx->small_blocks[MODE], (B + warps - 1) / warps);
   auto K = score_kernel<MODE, GEN>;
@@ -573,7 +588,7 @@ int launch_score(helio_gpu_ctx* ctx, int set, const int16_t* d_pl, int64_t B, in
   else
     launch_score_mode<HELIO_MODE_PARITY>(ctx, set, d_pl, B, partial, d_val, d_st, st, fo, timed);
   CK(cudaGetLastError());
-  ctx->launches += 2;
+  ctx->launches += (B == 1 && !timed) ? 1 : 2;
   if (timed) ctx->timed = true;
   return HELIO_OK;
 }
@@ -739,7 +754,7 @@ void helio_gpu_destroy(helio_gpu_ctx* ctx) {
   cudaFree(ctx->d_bidx);
   cudaFree(ctx->d_route);
   cudaFree(ctx->d_host_arena);
-  cudaFreeHost(ctx->h_route_pin);
+  cudaFreeHost(ctx->h_stage_pin);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->api_ev) cudaEventDestroy(ctx->api_ev);
@@ -1284,19 +1299,50 @@ int helio_gpu_flows_host(helio_gpu_ctx* ctx, const int16_t* h_pl, int64_t K, int
   if (rc) return rc;
   carve(c, d_pl, d_val, d_st, d_nv, d_ne, d_ed);
   CK(api_begin(ctx, st));
-  CK(cudaMemcpyAsync(d_pl, h_pl, row * K, cudaMemcpyHostToDevice, st));
+  // small calls (the per-call entries) go through the pinned staging buffer
+  // both ways: the outputs are one carved range, copied back in one DMA
+  const char* d_first = reinterpret_cast<const char*>(d_val);
+  const size_t span = (size_t)(reinterpret_cast<const char*>(d_ed + ne_alloc) - d_first);
+  char* pin = nullptr;
+  const bool staged = span <= (size_t(32) << 20) && host_pin(ctx, std::max(span, row * K), &pin) == HELIO_OK;
+  if (staged) {
+    std::memcpy(pin, h_pl, row * K);
+    CK(cudaMemcpyAsync(d_pl, pin, row * K, cudaMemcpyHostToDevice, st));
+  } else {
+    CK(cudaMemcpyAsync(d_pl, h_pl, row * K, cudaMemcpyHostToDevice, st));
+  }
   FlowOut fo{d_ed, d_nv, d_ne, max_edges};
   rc = launch_score(ctx, helio_gpu_ctx::kApiSet, d_pl, K, allow_partial ? 1 : 0, d_val, d_st, st, fo, false,
                     HELIO_MODE_PARITY);
   CK(api_end(ctx, st));
   if (rc) return rc;
-  CK(cudaMemcpyAsync(h_values, d_val, 8 * K, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(h_status, d_st, 4 * K, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(h_nv, d_nv, 4 * K, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(h_ne, d_ne, 4 * K, cudaMemcpyDeviceToHost, st));
-  if (max_edges > 0)
-    CK(cudaMemcpyAsync(h_edges, d_ed, sizeof(helio_edge) * (size_t)K * max_edges, cudaMemcpyDeviceToHost, st));
+  // the outputs are one carved range: a single DMA into pinned staging, then
+  // host copies (one round trip instead of five pageable copies; only each
+  // candidate's ne edges are copied out)
+  if (!staged) {  // large batches: direct copies
+    CK(cudaMemcpyAsync(h_values, d_val, 8 * K, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_status, d_st, 4 * K, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_nv, d_nv, 4 * K, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_ne, d_ne, 4 * K, cudaMemcpyDeviceToHost, st));
+    if (max_edges > 0)
+      CK(cudaMemcpyAsync(h_edges, d_ed, sizeof(helio_edge) * (size_t)K * max_edges, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return HELIO_OK;
+  }
+  CK(cudaMemcpyAsync(pin, d_first, span, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  auto at = [&](const void* d) { return pin + (reinterpret_cast<const char*>(d) - d_first); };
+  std::memcpy(h_values, at(d_val), 8 * K);
+  std::memcpy(h_status, at(d_st), 4 * K);
+  std::memcpy(h_nv, at(d_nv), 4 * K);
+  std::memcpy(h_ne, at(d_ne), 4 * K);
+  if (max_edges > 0) {
+    const helio_edge* src = reinterpret_cast<const helio_edge*>(at(d_ed));
+    for (int64_t k = 0; k < K; ++k) {
+      const int64_t n = std::min<int64_t>(std::max<int32_t>(h_ne[k], 0), max_edges);
+      std::memcpy(h_edges + k * max_edges, src + k * max_edges, sizeof(helio_edge) * n);
+    }
+  }
   return HELIO_OK;
 }
 

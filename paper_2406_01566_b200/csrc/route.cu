@@ -1048,7 +1048,7 @@ extern "C" int helio_gpu_route_host(helio_gpu_ctx* ctx, const int16_t* h_pl,
   char* pin = nullptr;
   const size_t out_bytes = 4 * (size_t)R + (max_hops > 0 ? 4 * HR * (want_se ? 3 : 1) : 0);
   const bool stage_io = !rc && R >= (int64_t(1) << 18) && !(is_pinned(h_in) && is_pinned(h_nh)) &&
-                        route_pin(ctx, std::max<size_t>(8 * (size_t)R, out_bytes), &pin) == HELIO_OK;
+                        host_pin(ctx, std::max<size_t>(8 * (size_t)R, out_bytes), &pin) == HELIO_OK;
   if (!rc) {
     auto H2D = [&](void* d, const void* h, size_t bytes) {
       if (bytes && !rc && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)

@@ -371,10 +371,23 @@ __device__ void emit_edges(const ClusterDev& cd, const Gs& g, int U, int partial
   for (int x = lane; x < 2 + 2 * U; x += 32) g.cur[x] = x >= 2 ? 1 : 0;
   __syncwarp();
   int eidx = U;
+  // link_pack a few batches ahead: one warp scans every link, and each
+  // batch's evaluation would otherwise wait on its own global load
+  constexpr int kAhead = 2;
+  uint32_t ahead[kAhead];
+#pragma unroll
+  for (int q = 0; q < kAhead; ++q) ahead[q] = 32 * q + lane < cd.Mv ? __ldg(cd.link_pack + 32 * q + lane) : 0u;
   for (int l0 = 0; l0 < cd.Mv; l0 += 32) {
     const int l = l0 + lane;
+    uint32_t pk = ahead[0];
+#pragma unroll
+    for (int q = 0; q + 1 < kAhead; ++q) ahead[q] = ahead[q + 1];
+    {
+      const int ln = l + 32 * kAhead;
+      ahead[kAhead - 1] = ln < cd.Mv ? __ldg(cd.link_pack + ln) : 0u;
+    }
     LinkEval le{false, 0, 0};
-    if (l < cd.Mv) le = eval_link(cd, g, l, partial);
+    if (l < cd.Mv) le = eval_link_pk(cd, g, pk, partial);
     const unsigned vm = __ballot_sync(FULL, le.valid);
     if (vm == 0u) continue;
     unsigned pu = 0;
